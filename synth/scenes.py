@@ -1,0 +1,332 @@
+"""Seeded synthetic LiDAR-like scenes for the MCS hot path (test/bench input only).
+
+This module is the ONE thing the oracle side and the CUDA side share: it makes
+inputs and holds none of the method's arithmetic (no SE(3) exp/log, no
+likelihood, no relative poses, no weights).  Poses are built from scipy
+rotation vectors and plain 4x4 products; covariances follow the GICP
+convention the paper cites as boundary inputs (R9).
+
+Recipe:
+  1. ray-cast analytic primitives (axis-aligned boxes, vertical cylinders, a
+     ground plane) with a MID-360-like pattern: 360 deg x [-7, +52] deg,
+     range 0.1-40 m, sigma_range = 0.01 m (sensor of P:202);
+  2. voxel-downsample on the fp32 cell grid floor(p * (1/r)) — one point per cell;
+  3. random-subsample to exactly the requested count;
+  4. covariances from the k = 10 nearest neighbours, plane-regularised to
+     eigenvalues (1, 1, 1e-3), i.e. Sigma = I - (1 - eps) n n^T.
+Every random draw comes from a Philox stream keyed (seed, purpose).
+"""
+from __future__ import annotations
+
+import functools
+import zlib
+from dataclasses import dataclass, field
+
+import numpy as np
+from scipy.spatial import cKDTree
+from scipy.spatial.transform import Rotation
+
+EPS_PLANE = 1e-3
+
+
+def rng(seed: int, purpose: str) -> np.random.Generator:
+    key = (int(seed) << 32) | zlib.crc32(purpose.encode())
+    return np.random.Generator(np.random.Philox(key=key))
+
+
+# ------------------------------------------------------------------ poses
+def pose(rotvec=(0.0, 0.0, 0.0), t=(0.0, 0.0, 0.0)) -> np.ndarray:
+    """4x4 fp64 pose from a rotation vector and a translation."""
+    T = np.eye(4)
+    T[:3, :3] = Rotation.from_rotvec(np.asarray(rotvec, np.float64)).as_matrix()
+    T[:3, 3] = t
+    return T
+
+
+def perturb(T: np.ndarray, sig_t: float, sig_r: float, g: np.random.Generator, n: int):
+    """n poses T @ [R(phi) | rho], rho ~ N(0, sig_t^2 I), phi ~ N(0, sig_r^2 I); (n, 4, 4)."""
+    rho = g.normal(0.0, sig_t, (n, 3))
+    phi = g.normal(0.0, sig_r, (n, 3))
+    D = np.tile(np.eye(4), (n, 1, 1))
+    D[:, :3, :3] = Rotation.from_rotvec(phi).as_matrix()
+    D[:, :3, 3] = rho
+    return T @ D if T.ndim == 3 else np.einsum("ij,njk->nik", T, D)
+
+
+def to12(T: np.ndarray) -> np.ndarray:
+    """(..., 4, 4) fp64 -> (..., 12) fp32 row-major [R|t]."""
+    return np.ascontiguousarray(T[..., :3, :4].reshape(T.shape[:-2] + (12,)), dtype=np.float32)
+
+
+# ------------------------------------------------------------------ primitives
+@dataclass
+class World:
+    boxes: np.ndarray = field(default_factory=lambda: np.zeros((0, 2, 3)))   # (nb, lo/hi, xyz)
+    cylinders: np.ndarray = field(default_factory=lambda: np.zeros((0, 5)))  # (x, y, radius, z0, z1)
+    ground_z: float | None = None
+
+
+def _ray_boxes(o, d, boxes, tbest, chunk=32768):
+    """Slab test of every ray against every box (torch CPU, multi-threaded)."""
+    if len(boxes) == 0:
+        return tbest
+    import torch
+    lo = torch.from_numpy(np.ascontiguousarray(boxes[:, 0, :] - o, np.float32))[None]
+    hi = torch.from_numpy(np.ascontiguousarray(boxes[:, 1, :] - o, np.float32))[None]
+    out = torch.from_numpy(tbest)
+    for s in range(0, len(d), chunk):
+        dd = torch.from_numpy(np.ascontiguousarray(d[s:s + chunk], np.float32))
+        dd = torch.where(dd.abs() < 1e-12, torch.full_like(dd, 1e-12), dd)
+        inv = (1.0 / dd)[:, None, :]
+        t1 = lo * inv
+        t2 = hi * inv
+        tmin = torch.minimum(t1, t2).amax(dim=2)
+        tmax = torch.maximum(t1, t2).amin(dim=2)
+        tmin = torch.where((tmax >= tmin) & (tmin > 1e-6), tmin, torch.full_like(tmin, np.inf))
+        out[s:s + chunk] = torch.minimum(out[s:s + chunk], tmin.amin(dim=1).double())
+    return out.numpy()
+
+
+def _ray_cylinders(o, d, cyl, tbest):
+    for cx, cy, rad, z0, z1 in cyl:
+        ox, oy = o[0] - cx, o[1] - cy
+        a = d[:, 0] ** 2 + d[:, 1] ** 2
+        b = 2 * (ox * d[:, 0] + oy * d[:, 1])
+        c = ox * ox + oy * oy - rad * rad
+        disc = b * b - 4 * a * c
+        ok = (disc > 0) & (a > 1e-12)
+        t = (-b - np.sqrt(np.where(ok, disc, 0))) / (2 * np.where(ok, a, 1))
+        z = o[2] + t * d[:, 2]
+        hit = ok & (t > 1e-6) & (z >= z0) & (z <= z1)
+        tbest = np.where(hit & (t < tbest), t, tbest)
+    return tbest
+
+
+def raycast(world: World, T_sensor: np.ndarray, n_az: int, n_el: int, g: np.random.Generator,
+            el_range=(-7.0, 52.0), rmin=0.1, rmax=40.0, sigma=0.01) -> np.ndarray:
+    """World-frame hit points of a jittered MID-360-like ray pattern from T_sensor."""
+    az = (np.arange(n_az) + g.random(n_az)) * (2 * np.pi / n_az)
+    el = np.deg2rad(el_range[0] + (np.arange(n_el) + g.random(n_el)) *
+                    ((el_range[1] - el_range[0]) / n_el))
+    A, E = np.meshgrid(az, el, indexing="ij")
+    ds = np.stack([np.cos(E) * np.cos(A), np.cos(E) * np.sin(A), np.sin(E)], -1).reshape(-1, 3)
+    d = ds @ T_sensor[:3, :3].T
+    o = T_sensor[:3, 3]
+    t = np.full(len(d), np.inf)
+    t = _ray_boxes(o, d, world.boxes, t)
+    t = _ray_cylinders(o, d, world.cylinders, t)
+    if world.ground_z is not None:
+        tg = (world.ground_z - o[2]) / np.where(np.abs(d[:, 2]) < 1e-12, -1e-12, d[:, 2])
+        t = np.where((tg > 1e-6) & (tg < t), tg, t)
+    keep = (t >= rmin) & (t <= rmax)
+    t = t[keep] + g.normal(0.0, sigma, keep.sum())
+    return o + d[keep] * t[:, None]
+
+
+# ------------------------------------------------------------------ cloud processing
+def downsample(p32: np.ndarray, r: float, g: np.random.Generator) -> np.ndarray:
+    """One point per fp32 cell floor(p * (1/r)) (same grid the map uses, R27)."""
+    p32 = np.ascontiguousarray(p32, np.float32)
+    perm = g.permutation(len(p32))
+    p32 = p32[perm]
+    cells = np.floor(p32 * np.float32(1.0 / r)).astype(np.int64)
+    _, first = np.unique(cells, axis=0, return_index=True)
+    return p32[np.sort(first)]
+
+
+def covariances(p: np.ndarray, k: int = 10, eps: float = EPS_PLANE) -> np.ndarray:
+    """Plane-regularised GICP covariances, (n, 6) fp32 (xx, xy, xz, yy, yz, zz)."""
+    p = np.asarray(p, np.float64)
+    tree = cKDTree(p)
+    _, nn = tree.query(p, k=min(k, len(p)))
+    Q = p[nn] - p[nn].mean(axis=1, keepdims=True)
+    cov = np.einsum("nki,nkj->nij", Q, Q) / max(nn.shape[1] - 1, 1)
+    _, vec = np.linalg.eigh(cov)
+    n = vec[:, :, 0]  # smallest-eigenvalue direction = surface normal
+    Sig = np.eye(3)[None] - (1.0 - eps) * np.einsum("ni,nj->nij", n, n)
+    out = np.stack([Sig[:, 0, 0], Sig[:, 0, 1], Sig[:, 0, 2], Sig[:, 1, 1], Sig[:, 1, 2],
+                    Sig[:, 2, 2]], -1)
+    return np.ascontiguousarray(out, np.float32)
+
+
+def sensor_cloud(world: World, T_sensor: np.ndarray, r: float, count: int | None,
+                 g: np.random.Generator, n_az: int, n_el: int):
+    """Ray cast -> sensor frame -> downsample at r -> (subsample to count) -> covariances."""
+    pw = raycast(world, T_sensor, n_az, n_el, g)
+    Ti = np.linalg.inv(T_sensor)
+    ps = (pw @ Ti[:3, :3].T + Ti[:3, 3]).astype(np.float32)
+    ds = downsample(ps, r, g)
+    cov_all = covariances(ds)
+    if count is not None:
+        if len(ds) < count:
+            raise ValueError(f"only {len(ds)} cells after downsampling, need {count}")
+        sel = np.sort(g.choice(len(ds), count, replace=False))
+        ds, cov_all = ds[sel], cov_all[sel]
+    return np.ascontiguousarray(ds, np.float32), np.ascontiguousarray(cov_all, np.float32)
+
+
+# ------------------------------------------------------------------ worlds
+def _slab(lo, hi):
+    return np.array([lo, hi], np.float64)
+
+
+def box_room(seed: int) -> World:
+    """20 x 10 x 3 m room (C1) with a few boxes inside to constrain every axis."""
+    g = rng(seed, "box_room")
+    w = 0.2
+    boxes = [
+        _slab([-w, -w, -w], [20 + w, 10 + w, 0]),       # floor
+        _slab([-w, -w, 3], [20 + w, 10 + w, 3 + w]),    # ceiling
+        _slab([-w, -w, 0], [0, 10 + w, 3]),             # walls
+        _slab([20, -w, 0], [20 + w, 10 + w, 3]),
+        _slab([-w, -w, 0], [20 + w, 0, 3]),
+        _slab([-w, 10, 0], [20 + w, 10 + w, 3]),
+    ]
+    for _ in range(8):
+        c = g.uniform([1, 1, 0], [19, 9, 0])
+        s = g.uniform([0.4, 0.4, 0.5], [1.2, 1.2, 2.0])
+        boxes.append(_slab([c[0], c[1], 0], [c[0] + s[0], c[1] + s[1], s[2]]))
+    return World(boxes=np.array(boxes))
+
+
+def loop_corridor(seed: int, outer=(60.0, 40.0), width=10.0, height=8.0, n_clutter=160) -> World:
+    """Rectangular loop corridor, warehouse-sized: 60 x 40 m, 10 m wide, 8 m high,
+    with wall-side clutter (shelves, crates) so every axis is constrained."""
+    g = rng(seed, "loop_corridor")
+    X, Y = outer
+    w = 0.3
+    boxes = [
+        _slab([-w, -w, -w], [X + w, Y + w, 0]),
+        _slab([-w, -w, height], [X + w, Y + w, height + w]),
+        _slab([-w, -w, 0], [0, Y + w, height]),
+        _slab([X, -w, 0], [X + w, Y + w, height]),
+        _slab([-w, -w, 0], [X + w, 0, height]),
+        _slab([-w, Y, 0], [X + w, Y + w, height]),
+        _slab([width, width, 0], [X - width, Y - width, height]),  # inner block
+    ]
+    # clutter: boxes against the outer and inner walls, and a few pillars mid-corridor
+    for _ in range(n_clutter):
+        side = g.integers(0, 4)
+        along = g.uniform(0.0, 1.0)
+        s = g.uniform([0.3, 0.3, 0.4], [2.5, 2.0, 5.0])
+        inner = g.random() < 0.5
+        off = (width - s[1]) if inner else 0.0
+        if side == 0:    # y = 0 side
+            x, y = along * (X - s[0]), off
+        elif side == 1:  # y = Y side
+            x, y = along * (X - s[0]), Y - s[1] - off
+        elif side == 2:  # x = 0 side
+            x, y = off, along * (Y - s[0])
+            s = s[[1, 0, 2]]
+        else:            # x = X side
+            x, y = X - s[1] - off, along * (Y - s[0])
+            s = s[[1, 0, 2]]
+        boxes.append(_slab([x, y, 0], [x + s[0], y + s[1], s[2]]))
+    return World(boxes=np.array(boxes))
+
+
+def loop_path(arc: float, outer=(60.0, 40.0), width=10.0, z=1.5) -> np.ndarray:
+    """Pose on the corridor centre line at arc length `arc` (counter-clockwise), heading along it."""
+    X, Y = outer
+    h = width / 2
+    L1, L2 = X - 2 * h, Y - 2 * h
+    P = 2 * (L1 + L2)
+    s = arc % P
+    if s < L1:
+        p, yaw = (h + s, h), 0.0
+    elif s < L1 + L2:
+        p, yaw = (X - h, h + s - L1), np.pi / 2
+    elif s < 2 * L1 + L2:
+        p, yaw = (X - h - (s - L1 - L2), Y - h), np.pi
+    else:
+        p, yaw = (h, Y - h - (s - 2 * L1 - L2)), 1.5 * np.pi
+    return pose((0, 0, yaw), (p[0], p[1], z))
+
+
+def loop_perimeter(outer=(60.0, 40.0), width=10.0) -> float:
+    return 2 * ((outer[0] - width) + (outer[1] - width))
+
+
+# ------------------------------------------------------------------ configs
+@dataclass
+class Scene:
+    name: str
+    r: float
+    gap: int
+    keyframes: list            # [(mean3 (n,3) f32, cov6 (n,6) f32)] in each keyframe's own frame
+    D: np.ndarray              # (K,) f64 cumulative odometry path length at each keyframe
+    D_now: float
+    scan_mean3: np.ndarray     # (S, 3) f32, sensor frame
+    scan_cov6: np.ndarray      # (S, 6) f32
+    pose12: np.ndarray         # (N, 12) f32 current poses T_t^i
+    kf_pose12: np.ndarray      # (N, K, 12) f32 per-particle keyframe poses T_k^i
+    U: int                     # resampling uniform (uint32)
+    T_gt: np.ndarray = None    # (4, 4) true scan pose
+    kf_gt: np.ndarray = None   # (K, 4, 4) true keyframe poses
+
+    @property
+    def N(self):
+        return self.pose12.shape[0]
+
+    @property
+    def K(self):
+        return len(self.keyframes)
+
+    @property
+    def S(self):
+        return self.scan_mean3.shape[0]
+
+
+@functools.lru_cache(maxsize=8)
+def c1(seed: int = 0, N: int = 1000, S: int = 512, n_kf_pts: int = 2048) -> Scene:
+    """C1: box room (r = 0.25 m), 1 keyframe of 2,048 points, 512-point scan 0.3 m / 3 deg away, gap 0."""
+    world = box_room(seed)
+    r = 0.25
+    T_kf = pose((0, 0, 0.3), (6.0, 4.5, 1.4))
+    T_gt = T_kf @ pose(np.deg2rad([0.0, 0.0, 3.0]), (0.3, 0.0, 0.0))
+    kf = sensor_cloud(world, T_kf, r, n_kf_pts, rng(seed, "c1/kf"), 720, 160)
+    scan = sensor_cloud(world, T_gt, r, S, rng(seed, "c1/scan"), 720, 160)
+    g = rng(seed, "c1/particles")
+    Tt = perturb(T_gt, 0.1, 0.02, g, N)
+    Tk = perturb(T_kf, 0.0, 0.0, g, N)[:, None]
+    return Scene("C1", r, 0, [kf], np.array([0.0]), 0.3, scan[0], scan[1], to12(Tt), to12(Tk),
+                 int(rng(seed, "c1/U").integers(0, 2**32)), T_gt, T_kf[None])
+
+
+@functools.lru_cache(maxsize=4)
+def c2(seed: int = 0, N: int = 100_000, S: int = 4096, K: int = 20, gap: int = 10,
+       sig_t: float = 0.2, sig_r: float = 0.02, drift_t: float = 0.01, drift_r: float = 0.001,
+       n_az: int = 900, n_el: int = 150) -> Scene:
+    """C2: loop corridor, K keyframes around the loop, scan back near keyframe 1 after a lap.
+
+    Every particle's neighbours {0, 1, 2} are old (<= latest - gap), so every particle
+    takes the full loop path (a2-a4).  Keyframe clouds downsampled at r = 0.5 m; the
+    scan at r/2 then subsampled to exactly S points.
+    """
+    world = loop_corridor(seed)
+    r = 0.5
+    P = loop_perimeter()
+    D = np.arange(K) * (P / K)
+    kf_gt = np.stack([loop_path(d) for d in D])
+    kfs = [sensor_cloud(world, kf_gt[k], r, None, rng(seed, f"c2/kf{k}"), n_az, n_el)
+           for k in range(K)]
+    arc_now = P + D[1] + 0.4
+    T_gt = loop_path(arc_now) @ pose((0.01, -0.01, 0.02), (0.0, 0.15, 0.0))
+    scan = sensor_cloud(world, T_gt, r / 2, S, rng(seed, "c2/scan"), n_az, n_el)
+    g = rng(seed, "c2/particles")
+    Tt = perturb(T_gt, sig_t, sig_r, g, N)
+    # per-particle keyframe poses: GT composed with a random-walk drift growing with k
+    Tk = np.empty((N, K, 4, 4))
+    drift = np.tile(np.eye(4), (N, 1, 1))
+    for k in range(K):
+        drift = perturb(drift, drift_t, drift_r, g, N) if k > 0 else drift
+        Tk[:, k] = np.einsum("ij,njk->nik", kf_gt[k], drift)
+    return Scene("C2", r, gap, kfs, D, float(P + D[1] + 0.4), scan[0], scan[1], to12(Tt),
+                 to12(Tk), int(rng(seed, "c2/U").integers(0, 2**32)), T_gt, kf_gt)
+
+
+def subset(scene: Scene, N: int) -> Scene:
+    """The first N particles of a scene (same keyframes and scan)."""
+    import dataclasses
+    return dataclasses.replace(scene, pose12=np.ascontiguousarray(scene.pose12[:N]),
+                               kf_pose12=np.ascontiguousarray(scene.kf_pose12[:N]))
