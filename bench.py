@@ -1,0 +1,315 @@
+#!/usr/bin/env python
+"""Benchmark of the MCS hot path (BASELINE.json metric) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--particles N]
+
+A step = one full filter update a1..a7 (neighbours + relative poses, likelihood/gradient
+sweep, GN update, keyframe propagation, weights, pruning/respawn, representative) of the
+C2 workload: 100,000 particles x a 4,096-point scan vs 20 keyframes (BASELINE.json
+configs[1]); the keyframe hash build (a0) is per keyframe, off the update clock (SURVEY
+§8(a)), and is reported separately.  Between timed steps the particle state is restored
+from a device snapshot and L2 is flushed (256 MiB write), both untimed.
+
+Prints ONE JSON line on rank 0.  --impl reference times the CPU oracle (the only other
+program of the path) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = ("particle·point likelihood+grad evals/s; ms per update @100k particles, "
+          "1–8 GPU")
+UNIT = "particle·point evals/s"
+FLOPS_MATCHED = 236.0    # FP32 flops per matched (particle, point, slot) with H~, b~
+FLOPS_UNMATCHED = 21.0   # transform + key for an unmatched triple
+GATHER_MATCHED = 56.0    # bytes: 8-B key probe + 48-B payload
+GATHER_UNMATCHED = 8.0
+LAUNCHES_PER_UPDATE = 19  # see DESIGN.md §5 (verified against the ncu launch list)
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    return rank, world, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4)
+                          if len(r) > 3 + k and r[3 + k].lower().startswith("active")})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        return json.load(open(p)), "measured"
+    return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+def committed_traffic():
+    p = os.path.join(ROOT, "profiles", "sweep_traffic.json")
+    if os.path.exists(p):
+        try:
+            return json.load(open(p)).get("dram_bytes_per_launch")
+        except Exception:
+            return None
+    return None
+
+
+def make_scene(particles: int, seed: int = 0):
+    import synth
+    return synth.c2(seed=seed, N=particles)
+
+
+# ------------------------------------------------------------------ CPU oracle (reference arm)
+def oracle_step(s, n: int, start: int):
+    """The oracle's whole update (steps 2-11) on a bounded sample of n particles."""
+    import oracle
+    idx = (np.arange(n) * (s.N // n) + start) % s.N
+    pose = np.ascontiguousarray(s.pose12[idx])
+    kp = np.ascontiguousarray(s.kf_pose12[idx])
+    L = np.zeros(n)
+    cfg = oracle.make_config(voxel_resolution=s.r, loop_recency_gap=s.gap)
+    kfs = oracle_step.kfs
+    t0 = time.perf_counter()
+    oracle.update(cfg, kfs, s.D_now, pose, kp, L, s.scan_mean3, s.scan_cov6, s.U)
+    return time.perf_counter() - t0
+
+
+def cpu_baseline(s, budget_s: float = 12.0):
+    import oracle
+    oracle.build()
+    oracle_step.kfs = oracle.Keyframes(s.keyframes, s.D, s.r)
+    t = oracle_step(s, 64, 0)  # calibration
+    n = int(min(s.N, max(64, 64 * budget_s / max(t, 1e-3))))
+    t = oracle_step(s, n, 1)
+    return {"value": n * s.S / t, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
+            "sample": f"{n} of {s.N} particles (strided), full 4096-pt scan, 20 keyframes, "
+                      f"whole update a1-a7 on the sample; {t:.2f} s"}, t
+
+
+def run_reference(args):
+    rank, world, local = dist_env()
+    if rank != 0:
+        return 0
+    s = make_scene(args.particles)
+    import oracle
+    oracle.build()
+    oracle_step.kfs = oracle.Keyframes(s.keyframes, s.D, s.r)
+    t = oracle_step(s, 32, 0)
+    n = int(min(s.N, max(32, 32 * args.ref_step_s / max(t, 1e-3))))
+    for w in range(args.warmup):
+        oracle_step(s, n, w)
+    times = [oracle_step(s, n, args.warmup + k) for k in range(args.steps)]
+    tot = sum(times)
+    value = n * s.S * args.steps / tot
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "C2 bounded sample: strided particles of the 100k-particle "
+                                   "loop-corridor scene, 4096-pt scan, 20 keyframes",
+                       "particles_per_step": n, "scan_points": s.S, "keyframes": s.K},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": oracle.num_threads(),
+                             "kind": "oracle",
+                             "sample": f"{n} particles per step, whole update a1-a7"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ GPU arm
+def run_gpu(args):
+    import torch
+
+    import paper_2504_18056_b200 as mcs
+    rank, world, local = dist_env()
+    if world > 1:
+        raise SystemExit("multi-GPU bench requires the NCCL build of libmcs (not yet)")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    s = make_scene(args.particles)
+    N, S, K = s.N, s.S, s.K
+    stream = torch.cuda.Stream(device=dev)
+    ctx = mcs.Context(N, K, S, neighbor_count=3, loop_recency_gap=s.gap, voxel_resolution=s.r,
+                      device=local)
+    ctx.set_stream(stream)
+    t0 = time.perf_counter()
+    for (m3, c6), d in zip(s.keyframes, s.D):
+        ctx.add_keyframe(m3, c6, d)
+    a0_ms = 1e3 * (time.perf_counter() - t0) / K
+    ctx.set_particles(s.pose12, s.kf_pose12)
+    # match statistics (algorithmic work per launch), untimed
+    ev = ctx.eval(s.scan_mean3, s.scan_cov6)
+    matched = int(ev["slot_n"].sum())
+    triples = int((ev["slot_kf"] >= 0).sum()) * S
+    ctx.snapshot()
+    d_m = torch.from_numpy(s.scan_mean3).to(dev)
+    d_c = torch.from_numpy(s.scan_cov6).to(dev)
+    out = {"loglik": torch.zeros(N, dtype=torch.float64, device=dev),
+           "weight": torch.zeros(N, dtype=torch.float64, device=dev),
+           "representative": torch.zeros(1, dtype=torch.int32, device=dev),
+           "n_dead": torch.zeros(1, dtype=torch.int64, device=dev)}
+    flush = torch.empty(64 * 2**20, dtype=torch.float32, device=dev)  # 256 MiB > 126 MB L2
+    ctx.set_profiling(True)
+
+    def one_step():
+        with torch.cuda.stream(stream):
+            ctx.restore()
+            flush.fill_(1.0)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            ctx.update_async(d_m, d_c, s.D_now, s.U, out, stream=stream)
+            e1.record(stream)
+        return e0, e1
+
+    for _ in range(args.warmup):
+        one_step()
+    torch.cuda.synchronize()
+    step_ms, sweep_ms, phases = [], [], []
+    with ClockSampler(local) as clocks:
+        torch.cuda.synchronize()
+        for _ in range(args.steps):
+            e0, e1 = one_step()
+            e1.synchronize()
+            step_ms.append(e0.elapsed_time(e1))
+            ph = ctx.phase_ms()
+            phases.append(ph)
+            sweep_ms.append(ph["sweep"])
+        torch.cuda.synchronize()
+    total_ms = float(np.sum(step_ms))
+    ms = total_ms / args.steps
+    value = N * S * args.steps / (total_ms * 1e-3)
+
+    # e2e: the public synchronous call with pinned host buffers (H2D scan, D2H results)
+    h_m = torch.from_numpy(s.scan_mean3).pin_memory()
+    h_c = torch.from_numpy(s.scan_cov6).pin_memory()
+    e2e_t = []
+    for k in range(args.warmup + args.steps):
+        ctx.restore()
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        r = ctx.update(h_m, h_c, s.D_now, s.U, outputs=("loglik", "weight"))
+        t2 = time.perf_counter()
+        if k >= args.warmup:
+            e2e_t.append(t2 - t1)
+    e2e_value = N * S / float(np.mean(e2e_t))
+
+    peaks, peak_src = measured_peaks()
+    sm_mhz = peaks.get("sm_max_mhz", 1965.0)
+    fp32_peak = 148 * 128 * 2 * sm_mhz * 1e6 / 1e12  # TFLOP/s
+    flops = matched * FLOPS_MATCHED + (triples - matched) * FLOPS_UNMATCHED
+    sweep_avg = float(np.mean(sweep_ms))
+    achieved = flops / (sweep_avg * 1e-3) / 1e12
+    gather = (matched * GATHER_MATCHED + (triples - matched) * GATHER_UNMATCHED)
+    ph_mean = {k: float(np.mean([p[k] for p in phases])) for k in phases[0]}
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": "C2: 100k particles x 4096-pt LiDAR-like scan vs 20 keyframes "
+                               "(loop corridor, r = 0.5 m, 3 neighbours, every particle loops)",
+                   "particles": N, "scan_points": S, "keyframes": K,
+                   "keyframe_cells": int(sum(len(k[0]) for k in s.keyframes)),
+                   "l2": "particle state restored from a device snapshot and 256 MiB L2 flush "
+                         "before every timed step (untimed)"},
+        "roofline": {"kernel": "sweep (a2)", "bound": "alu", "achieved": achieved,
+                     "peak": fp32_peak, "unit": "TFLOP/s", "frac": achieved / fp32_peak,
+                     "traffic": committed_traffic(),
+                     "peak_source": f"148 SM x 128 FP32 lanes x 2 x {sm_mhz:.0f} MHz "
+                                    f"({peak_src} sm_max_mhz)",
+                     "flops_per_launch": flops, "sweep_ms": sweep_avg,
+                     "l2_gather_GBps": gather / (sweep_avg * 1e-3) / 1e9},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(36 * S),
+                "d2h_bytes_per_step": int(16 * N + 4 + 8), "ms_per_step": 1e3 * float(np.mean(e2e_t))},
+        "gpu_launches": LAUNCHES_PER_UPDATE * args.steps,
+        "clocks": clocks.summary(),
+        "ms_p10_p50_p90": [float(np.percentile(step_ms, q)) for q in (10, 50, 90)],
+        "phase_ms": ph_mean,
+        "triple_evals_per_s": triples * args.steps / (total_ms * 1e-3),
+        "match_rate": matched / max(triples, 1),
+        "a0_ms_per_keyframe": a0_ms,
+        "n_dead": int(out["n_dead"][0]),
+    }
+    if rank == 0 and not args.no_cpu_baseline:
+        line["cpu_baseline"], _ = cpu_baseline(s, args.cpu_budget_s)
+    ctx.close()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="native", choices=["native", "reference"])
+    ap.add_argument("--particles", type=int, default=100_000)
+    ap.add_argument("--cpu-budget-s", type=float, default=12.0)
+    ap.add_argument("--ref-step-s", type=float, default=4.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_gpu(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,182 @@
+/*
+ * mcs.h — C-ABI of the B200-native hot path of gradient-guided 6-DoF Monte Carlo
+ * SLAM (arXiv 2504.18056).  Product library: libmcs.so (sm_100a CUDA).
+ *
+ * What it computes (PAPER.md line numbers "P:n"; readings "Rn" in DESIGN.md §3):
+ *   per particle i and each of its neighbour keyframes k:
+ *     kT = (T_k^i)^-1 T_t^i                                      (Eq.4)
+ *     log p = -sum_j e_j^T Omega_j e_j,  e_j = mu'_j - kT mu_j,
+ *             Omega_j = (Sigma'_j + kR Sigma_j kR^T)^-1          (Eqs.2-4)
+ *     H = sum J^T Omega J, b = sum J^T Omega e, J = de/d(kT)     (Eq.6)
+ *   then, for loop particles: psi = -(H + lambda I)^-1 b (Eq.5; R1, R11),
+ *   T_t <- T_t exp(psi) (Eq.7), keyframe propagation
+ *   T_k <- T_k exp(r_k psi), r_k = d(t_k, t_o)/d(t, t_o)         (Eqs.8-10; R14-R16),
+ *   importance weights L_i += log p, w = softmax(L)              (Eq.11; R22),
+ *   dead-particle pruning + respawn from the survivors' weights  (R17, R18),
+ *   representative = argmax w.
+ *
+ * Conventions
+ *   Pose12  : row-major 3x4 [R|t], fp32; p[4a+b] = R[a][b], p[4a+3] = t[a] (P:91 implies fp32).
+ *   Cov6    : (xx, xy, xz, yy, yz, zz), fp32, symmetric positive definite.
+ *   Twist6  : (rho, phi), translation first, right perturbation T exp(xi) (R2).
+ *   Hess21  : upper triangle of a symmetric 6x6, row-major: (0,0),(0,1)..(0,5),(1,1)..(5,5).
+ *   Keyframe clouds are Gaussians in the keyframe's own sensor frame.
+ *
+ * Ownership: the caller owns every buffer passed in.  Data the library keeps
+ *   (keyframe clouds, particles) is copied into context-owned device memory.
+ *   Synchronous calls accept HOST or DEVICE pointers (unified addressing) and keep
+ *   no pointer after returning.  *_async calls take DEVICE pointers only and borrow
+ *   them until the given stream reaches the work.
+ * Errors: every call returns mcs_status; mcs_last_error() gives the message.
+ *   Argument errors are detected before any state change.  CUDA/NCCL errors are
+ *   sticky: the context then returns MCS_E_CUDA / MCS_E_NCCL until destroyed.
+ *   MCS_E_DEGENERATE (every particle dead): weights were updated, respawn
+ *   was skipped; the caller must re-initialise the particles.
+ * Threading: a context is not thread-safe; distinct contexts are independent.
+ */
+#ifndef MCS_H
+#define MCS_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define MCS_API __attribute__((visibility("default")))
+#else
+#define MCS_API
+#endif
+
+#define MCS_ABI_VERSION 1
+#define MCS_MAX_NEIGHBORS 4
+
+typedef struct mcs_ctx mcs_ctx; /* opaque; owns all device state */
+
+typedef enum {
+  MCS_OK = 0,
+  MCS_E_INVALID_ARG = 1,  /* null / size / non-finite / non-SPD input            */
+  MCS_E_OUT_OF_MEMORY = 2,
+  MCS_E_CUDA = 3,         /* sticky                                             */
+  MCS_E_NCCL = 4,         /* sticky                                             */
+  MCS_E_CAPACITY = 5,     /* exceeds a capacity fixed at mcs_create             */
+  MCS_E_STATE = 6,        /* call order, e.g. update before any keyframe        */
+  MCS_E_DEGENERATE = 7    /* every particle dead                        */
+} mcs_status;
+
+typedef enum { MCS_GN_OLD_SLOTS = 0, /* Fig.3: gradient w.r.t. non-recent keyframes (R4) */
+               MCS_GN_ALL_SLOTS = 1  /* every neighbour slot                      */
+} mcs_gn_slots;
+
+typedef struct mcs_config {
+  uint32_t abi_version;          /* MCS_ABI_VERSION                                         */
+  int32_t  capacity_particles;   /* particles on this device (its shard when world_size>1)  */
+  int32_t  capacity_keyframes;   /* K_max: per-particle keyframe pose storage is N x K_max  */
+  int32_t  capacity_scan_points; /* S_max                                                   */
+  int32_t  neighbor_count;       /* 1..MCS_MAX_NEIGHBORS; 3                          */
+  int32_t  loop_recency_gap;     /* slot old iff kf id <= latest - gap (R5); 10             */
+  float    voxel_resolution;     /* r in metres; a power of two (R27); 0.5 indoor          */
+  int32_t  gn_slots;             /* mcs_gn_slots                                            */
+  double   damping_rel;          /* lambda = damping_rel * tr(H) / 6 (R11); 1e-6            */
+  double   step_clamp;           /* ||psi||_2 <= step_clamp (R11); 1.0                      */
+  double   unmatched_penalty;    /* kappa per unmatched (point, slot) (R8); 0               */
+  double   loglik_rel_floor;     /* dead if l_i - max_j l_j < this (R17); ln 1e-16   */
+  double   posterior_floor;      /* dead if w_i < this; 1e-8                        */
+  int32_t  device;               /* CUDA ordinal                                            */
+  int32_t  rank, world_size;     /* particle shards (one process per GPU)                   */
+  const void* nccl_unique_id;    /* 128-byte ncclUniqueId when world_size > 1, else NULL    */
+} mcs_config;
+
+/* Fills *cfg with the defaults above (capacities 0: caller sets them). */
+MCS_API void mcs_config_default(mcs_config* cfg);
+
+MCS_API mcs_status  mcs_create(const mcs_config* cfg, mcs_ctx** out);
+MCS_API mcs_status  mcs_destroy(mcs_ctx* ctx);
+/* ctx == NULL: the calling thread's last mcs_create error. */
+MCS_API const char* mcs_last_error(const mcs_ctx* ctx);
+/* Stream every call of this context is ordered on (cudaStream_t; NULL = library-owned). */
+MCS_API mcs_status  mcs_set_stream(mcs_ctx* ctx, void* cuda_stream);
+
+/* Register keyframe k = K (returned in *out_kf_id): n Gaussians (mean3[n][3], cov6[n][6])
+ * in the keyframe's own sensor frame, and D_k, the cumulative odometry path length at the
+ * keyframe (Eq.9 reading R14).  Builds the keyframe's voxel hash once (off the update
+ * clock).  Every particle's new keyframe pose is its current pose: T_k^i := T_t^i (R24).
+ * MCS_E_INVALID_ARG if a point's cell lies outside the 21-bit range or n < 1. */
+MCS_API mcs_status mcs_add_keyframe(mcs_ctx* ctx, const float* mean3, const float* cov6, int32_t n,
+                            double path_length, int32_t* out_kf_id);
+
+/* Set the local particle set: pose12[n][12] current poses; kf_pose12[n][K][12] (K = current
+ * keyframe count) or NULL (every T_k^i := T_t^i); cum_loglik[n] (fp64 L_i, Eq.11) or NULL (0). */
+MCS_API mcs_status mcs_set_particles(mcs_ctx* ctx, int32_t n_local, const float* pose12,
+                             const float* kf_pose12, const double* cum_loglik);
+/* Read back (any pointer may be NULL): pose12[n][12], kf_pose12[n][K][12], L[n], w[n]. */
+MCS_API mcs_status mcs_get_particles(mcs_ctx* ctx, float* pose12, float* kf_pose12, double* cum_loglik,
+                             double* weight);
+MCS_API mcs_status mcs_get_sizes(const mcs_ctx* ctx, int32_t* n_local, int32_t* n_keyframes);
+
+/* Outputs of one update; every pointer optional (NULL = not produced).  Per-particle rows are
+ * indexed by LOCAL particle index.  loglik = l_i over ALL neighbour slots (Eq.2) minus the kappa
+ * term; grad6 = dl/d(delta) = -2 sum_{s in G} b_s (0 for non-loop particles under
+ * MCS_GN_OLD_SLOTS); hess21 = undamped H over G; psi6 = applied update (0 if none);
+ * weight = w_i after respawn; donor = -1 or the GLOBAL index cloned into slot i;
+ * flags: bit0 loop, bit1 updated, bit2 singular, bit3 dead before respawn, bit4 clamped;
+ * representative = GLOBAL argmax w (ties -> lowest); n_dead = global dead count. */
+typedef struct {
+  double*  loglik;
+  float*   grad6;
+  float*   hess21;
+  float*   psi6;
+  double*  weight;
+  int32_t* donor;
+  uint8_t* flags;
+  int32_t* representative;
+  int64_t* n_dead;
+} mcs_update_out;
+
+/* One full filter update with one scan (mean3[n_pts][3], cov6[n_pts][6] in the current
+ * sensor frame): a1 neighbours/relative poses, a2 likelihood+gradient sweep, a3 GN update,
+ * a4 keyframe propagation, a5 weights, a6 pruning/respawn, a7 representative.
+ * D_now = current cumulative odometry path length (R14); resample_u = the respawn uniform
+ * u0 = resample_u / 2^32 (R18).  Synchronous; host or device pointers. */
+MCS_API mcs_status mcs_update(mcs_ctx* ctx, const float* scan_mean3, const float* scan_cov6,
+                      int32_t n_pts, double D_now, uint32_t resample_u,
+                      const mcs_update_out* out);
+/* Same, stream-ordered on cuda_stream (NULL = context stream); DEVICE pointers only; the
+ * scan is not validated (caller guarantees finite SPD covariances). */
+MCS_API mcs_status mcs_update_async(mcs_ctx* ctx, const float* d_scan_mean3, const float* d_scan_cov6,
+                            int32_t n_pts, double D_now, uint32_t resample_u,
+                            const mcs_update_out* d_out, void* cuda_stream);
+
+/* Isolated likelihood + gradient evaluation (a1 + a2 + per-slot combine), no state change.
+ * Per (particle, slot) s < neighbor_count, row-major [n][neighbor_count]: slot_loglik (fp64
+ * value of the fp32 sum), slot_H21 (body frame of T_t), slot_b6 (sum J^T Omega e), slot_n
+ * (matched points), slot_kf (keyframe id, -1 if K < slot+1); loop[n] (bit0). */
+MCS_API mcs_status mcs_eval(mcs_ctx* ctx, const float* scan_mean3, const float* scan_cov6,
+                    int32_t n_pts, double* slot_loglik, float* slot_H21, float* slot_b6,
+                    int32_t* slot_n, int32_t* slot_kf, uint8_t* loop);
+
+/* Isolated respawn (a6) on given inputs, no state change: e[n] (fp64 exp(L - max L)),
+ * dead[n] (0/1), uniform u -> donor[n] (-1 or donor index).  Bit-exact contract with the
+ * oracle's integer-ladder systematic resampler (R18).  Single-device only. */
+MCS_API mcs_status mcs_resample(mcs_ctx* ctx, const double* e, const uint8_t* dead, int32_t n,
+                        uint32_t u, int32_t* donor_out);
+
+/* Device-side checkpoint of the particle state (poses, keyframe poses, L): mcs_snapshot copies
+ * it into a context-owned buffer, mcs_restore copies it back.  Stream-ordered. */
+MCS_API mcs_status mcs_snapshot(mcs_ctx* ctx);
+MCS_API mcs_status mcs_restore(mcs_ctx* ctx);
+
+/* Per-particle state bytes with K keyframes: 48 (T_t) + 48 K (T_k) + 8 (L). */
+MCS_API size_t mcs_state_bytes_per_particle(int32_t n_keyframes);
+
+/* Cumulative device time of the last update's phases, milliseconds (CUDA events):
+ * [0] a1 select, [1] a2 sweep, [2] a3+a4 update, [3] a5-a7 weights/respawn, [4] total.
+ * Only filled when profiling is enabled with mcs_set_profiling(ctx, 1). */
+MCS_API mcs_status mcs_set_profiling(mcs_ctx* ctx, int32_t enable);
+MCS_API mcs_status mcs_get_phase_ms(const mcs_ctx* ctx, float* ms5);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MCS_H */

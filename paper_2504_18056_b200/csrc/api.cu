@@ -1,0 +1,737 @@
+// api.cu — the C-ABI of libmcs (include/mcs.h): validation, lifecycle, state, orchestration of
+// the hot path a1..a7 on the context stream.  No compute happens on the host: every step of
+// the path runs in the kernels of select.cu, sweep.cu, update.cu, weights.cu, kf_store.cu.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "mcs_internal.cuh"
+
+using namespace mcs;
+
+static thread_local std::string g_create_error;
+
+#define FAIL(ctx, code, ...)                                   \
+  do {                                                         \
+    char _b[512];                                              \
+    snprintf(_b, sizeof(_b), __VA_ARGS__);                     \
+    (ctx)->err = _b;                                           \
+    return (code);                                             \
+  } while (0)
+
+#define CUDA_TRY(ctx, x)                                                               \
+  do {                                                                                 \
+    cudaError_t _e = (x);                                                              \
+    if (_e != cudaSuccess) {                                                           \
+      (ctx)->sticky = MCS_E_CUDA;                                                      \
+      char _b[512];                                                                    \
+      snprintf(_b, sizeof(_b), "CUDA error %s at %s:%d: %s", cudaGetErrorName(_e),     \
+               __FILE__, __LINE__, cudaGetErrorString(_e));                            \
+      (ctx)->err = _b;                                                                 \
+      return MCS_E_CUDA;                                                               \
+    }                                                                                  \
+  } while (0)
+
+#define CHECK_CTX(ctx)                                  \
+  do {                                                  \
+    if (!(ctx)) return MCS_E_INVALID_ARG;               \
+    if ((ctx)->sticky != MCS_OK) return (ctx)->sticky;  \
+  } while (0)
+
+// ------------------------------------------------------------------ small device kernels
+__global__ void fill_kf_from_current_kernel(const float* __restrict__ pose, int capN, int N,
+                                            float* __restrict__ kfpose, int capK, int k0, int k1) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const int nk = k1 - k0;
+  if (t >= (long long)N * nk) return;
+  const int i = (int)(t / nk), k = k0 + (int)(t - (long long)i * nk);
+  float* dst = kfpose + ((size_t)i * capK + k) * 12;
+#pragma unroll
+  for (int e = 0; e < 12; ++e) dst[e] = pose[(size_t)e * capN + i];
+}
+
+__global__ void aos_to_soa_kernel(const float* __restrict__ aos, int N, int capN,
+                                  float* __restrict__ soa) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= N) return;
+#pragma unroll
+  for (int e = 0; e < 12; ++e) soa[(size_t)e * capN + i] = aos[(size_t)i * 12 + e];
+}
+
+__global__ void soa_to_aos_kernel(const float* __restrict__ soa, int N, int capN,
+                                  float* __restrict__ aos) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= N) return;
+#pragma unroll
+  for (int e = 0; e < 12; ++e) aos[(size_t)i * 12 + e] = soa[(size_t)e * capN + i];
+}
+
+// counts non-finite values and rotation blocks that are not orthonormal (|R^T R - I| > 1e-3)
+__global__ void validate_poses_kernel(const float* __restrict__ p, long long n_poses,
+                                      int* __restrict__ bad) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n_poses) return;
+  const float* T = p + t * 12;
+  bool ok = true;
+  for (int e = 0; e < 12; ++e) ok = ok && isfinite(T[e]);
+  if (ok) {
+    for (int a = 0; a < 3; ++a)
+      for (int b = 0; b < 3; ++b) {
+        float s = 0.f;
+        for (int c = 0; c < 3; ++c) s += T[4 * c + a] * T[4 * c + b];
+        ok = ok && fabsf(s - (a == b ? 1.f : 0.f)) < 1e-3f;
+      }
+  }
+  if (!ok) atomicAdd(bad, 1);
+}
+
+// non-finite means or non-SPD covariances (Sylvester on fp64)
+__global__ void validate_gauss_kernel(const float* __restrict__ mean3,
+                                      const float* __restrict__ cov6, int n,
+                                      int* __restrict__ bad) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  bool ok = isfinite(mean3[3 * j]) && isfinite(mean3[3 * j + 1]) && isfinite(mean3[3 * j + 2]);
+  const float* c = cov6 + 6 * j;
+  for (int k = 0; k < 6; ++k) ok = ok && isfinite(c[k]);
+  if (ok) {
+    const double xx = c[0], xy = c[1], xz = c[2], yy = c[3], yz = c[4], zz = c[5];
+    const double m2 = xx * yy - xy * xy;
+    const double m3 = xx * (yy * zz - yz * yz) - xy * (xy * zz - yz * xz) + xz * (xy * yz - yy * xz);
+    ok = xx > 0.0 && m2 > 0.0 && m3 > 0.0;
+  }
+  if (!ok) atomicAdd(bad, 1);
+}
+
+__global__ void fill_double_kernel(double* __restrict__ p, int n, double v) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) p[i] = v;
+}
+
+struct OutPtrs {
+  double* loglik;
+  float* grad6;
+  float* hess21;
+  float* psi6;
+  double* weight;
+  int32_t* donor;
+  uint8_t* flags;
+  int32_t* rep;
+  int64_t* n_dead;
+};
+
+__global__ void gather_outputs_kernel(OutPtrs o, int N, int capN, const double* __restrict__ l,
+                                      const float* __restrict__ grad,
+                                      const float* __restrict__ hess,
+                                      const double* __restrict__ psi,
+                                      const double* __restrict__ w,
+                                      const int32_t* __restrict__ donor,
+                                      const uint8_t* __restrict__ flags, const Scalars* sc,
+                                      int base_index) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i == 0) {
+    if (o.rep) *o.rep = sc->rep;
+    if (o.n_dead) *o.n_dead = sc->D;
+  }
+  if (i >= N) return;
+  if (o.loglik) o.loglik[i] = l[i];
+  if (o.grad6)
+    for (int k = 0; k < 6; ++k) o.grad6[(size_t)i * 6 + k] = grad[(size_t)k * capN + i];
+  if (o.hess21)
+    for (int k = 0; k < 21; ++k) o.hess21[(size_t)i * 21 + k] = hess[(size_t)k * capN + i];
+  if (o.psi6)
+    for (int k = 0; k < 6; ++k) o.psi6[(size_t)i * 6 + k] = (float)psi[(size_t)k * capN + i];
+  if (o.weight) o.weight[i] = w[i];
+  if (o.donor) o.donor[i] = donor[i] < 0 ? -1 : donor[i] + base_index;
+  if (o.flags) o.flags[i] = flags[i];
+}
+
+// ------------------------------------------------------------------ helpers
+template <typename T>
+static cudaError_t dalloc(T** p, size_t count) {
+  return cudaMalloc((void**)p, sizeof(T) * (count ? count : 1));
+}
+
+static bool is_pow2_float(float r) {
+  if (!(r > 0.f) || !std::isfinite(r)) return false;
+  int ex;
+  float m = std::frexp(r, &ex);
+  return m == 0.5f;
+}
+
+static void free_all(mcs_ctx* c) {
+  for (auto& k : c->kf) {
+    cudaFree(k.keys);
+    cudaFree(k.payload);
+  }
+  void* ptrs[] = {c->d_kf_meta, c->d_D,       c->d_pose,     c->d_kfpose,   c->d_L,
+                  c->d_snapshot, c->d_scan_raw, c->d_scan,    c->d_items,    c->d_order,
+                  c->d_part,    c->d_meta,    c->d_to,       c->d_l,        c->d_psi,
+                  c->d_grad,    c->d_hess,    c->d_flags,    c->d_e,        c->d_w,
+                  c->d_ladder,  c->d_ladder_scan, c->d_ncum, c->d_donor,    c->d_partials,
+                  c->d_ipartials, c->d_scal,  c->d_cub_temp};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  if (c->h_scal) cudaFreeHost(c->h_scal);
+  for (auto& e : c->ev)
+    if (e) cudaEventDestroy(e);
+  if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+}
+
+// copy n bytes from a host-or-device pointer into device memory, stream-ordered
+static cudaError_t to_device(void* dst, const void* src, size_t bytes, cudaStream_t st) {
+  return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, st);
+}
+
+// ------------------------------------------------------------------ ABI
+extern "C" {
+
+void mcs_config_default(mcs_config* cfg) {
+  if (!cfg) return;
+  memset(cfg, 0, sizeof(*cfg));
+  cfg->abi_version = MCS_ABI_VERSION;
+  cfg->neighbor_count = 3;
+  cfg->loop_recency_gap = 10;
+  cfg->voxel_resolution = 0.5f;
+  cfg->gn_slots = MCS_GN_OLD_SLOTS;
+  cfg->damping_rel = 1e-6;
+  cfg->step_clamp = 1.0;
+  cfg->unmatched_penalty = 0.0;
+  cfg->loglik_rel_floor = std::log(1e-16);
+  cfg->posterior_floor = 1e-8;
+  cfg->device = 0;
+  cfg->rank = 0;
+  cfg->world_size = 1;
+  cfg->nccl_unique_id = nullptr;
+}
+
+size_t mcs_state_bytes_per_particle(int32_t n_keyframes) {
+  return 48u + 48u * (size_t)(n_keyframes < 0 ? 0 : n_keyframes) + 8u;
+}
+
+const char* mcs_last_error(const mcs_ctx* ctx) {
+  return ctx ? ctx->err.c_str() : g_create_error.c_str();
+}
+
+mcs_status mcs_create(const mcs_config* cfg, mcs_ctx** out) {
+  g_create_error.clear();
+  if (!cfg || !out) { g_create_error = "null argument"; return MCS_E_INVALID_ARG; }
+  *out = nullptr;
+  if (cfg->abi_version != MCS_ABI_VERSION) {
+    g_create_error = "abi_version mismatch";
+    return MCS_E_INVALID_ARG;
+  }
+  if (cfg->capacity_particles < 1 || cfg->capacity_keyframes < 1 ||
+      cfg->capacity_scan_points < 1) {
+    g_create_error = "capacities must be >= 1";
+    return MCS_E_INVALID_ARG;
+  }
+  if (cfg->neighbor_count < 1 || cfg->neighbor_count > MCS_MAX_NEIGHBORS) {
+    g_create_error = "neighbor_count must be in [1, MCS_MAX_NEIGHBORS]";
+    return MCS_E_INVALID_ARG;
+  }
+  if (!is_pow2_float(cfg->voxel_resolution)) {
+    g_create_error = "voxel_resolution must be a positive power of two (DESIGN.md R27)";
+    return MCS_E_INVALID_ARG;
+  }
+  if (cfg->loop_recency_gap < 0 || (cfg->gn_slots != 0 && cfg->gn_slots != 1) ||
+      !(cfg->damping_rel >= 0) || !(cfg->step_clamp > 0) || !(cfg->unmatched_penalty >= 0) ||
+      std::isnan(cfg->loglik_rel_floor) || std::isnan(cfg->posterior_floor)) {
+    g_create_error = "invalid numeric configuration";
+    return MCS_E_INVALID_ARG;
+  }
+  if (cfg->world_size != 1 || cfg->rank != 0) {
+    g_create_error = "world_size > 1 requires the NCCL build (not in this library version)";
+    return MCS_E_INVALID_ARG;
+  }
+  if ((long long)cfg->capacity_particles * cfg->neighbor_count > 0x7fffffffLL) {
+    g_create_error = "capacity_particles * neighbor_count exceeds 2^31";
+    return MCS_E_CAPACITY;
+  }
+  if (cfg->capacity_particles > (1 << 21)) {  // exact ladder: N * 2^32 < 2^53 (R18)
+    g_create_error = "capacity_particles > 2^21 per device (integer-ladder bound, R18)";
+    return MCS_E_CAPACITY;
+  }
+  mcs_ctx* c = new mcs_ctx();
+  c->cfg = *cfg;
+  c->dev = cfg->device;
+  c->capN = cfg->capacity_particles;
+  c->capK = cfg->capacity_keyframes;
+  c->capS = cfg->capacity_scan_points;
+  c->nbcap = cfg->neighbor_count;
+  cudaError_t e = cudaSetDevice(c->dev);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+  c->own_stream = (e == cudaSuccess);
+  const size_t N = c->capN, K = c->capK, S = c->capS, nb = c->nbcap;
+  const size_t maxb = (N + 127) / 128 + 64;
+  if (e == cudaSuccess) e = dalloc(&c->d_kf_meta, K);
+  if (e == cudaSuccess) e = dalloc(&c->d_D, K);
+  if (e == cudaSuccess) e = dalloc(&c->d_pose, 12 * N);
+  if (e == cudaSuccess) e = dalloc(&c->d_kfpose, N * K * 12);
+  if (e == cudaSuccess) e = dalloc(&c->d_L, N);
+  if (e == cudaSuccess) e = dalloc(&c->d_scan_raw, 9 * S);
+  if (e == cudaSuccess) e = dalloc(&c->d_scan, 3 * S);
+  if (e == cudaSuccess) e = dalloc(&c->d_items, 4 * nb * N);
+  if (e == cudaSuccess) e = dalloc(&c->d_order, nb * N);
+  if (e == cudaSuccess) e = dalloc(&c->d_part, (size_t)kSlotFloats * nb * N);
+  if (e == cudaSuccess) e = dalloc(&c->d_meta, N);
+  if (e == cudaSuccess) e = dalloc(&c->d_to, N);
+  if (e == cudaSuccess) e = dalloc(&c->d_l, N);
+  if (e == cudaSuccess) e = dalloc(&c->d_psi, 6 * N);
+  if (e == cudaSuccess) e = dalloc(&c->d_grad, 6 * N);
+  if (e == cudaSuccess) e = dalloc(&c->d_hess, 21 * N);
+  if (e == cudaSuccess) e = dalloc(&c->d_flags, N);
+  if (e == cudaSuccess) e = dalloc(&c->d_e, N);
+  if (e == cudaSuccess) e = dalloc(&c->d_w, N);
+  if (e == cudaSuccess) e = cudaMalloc(&c->d_ladder, 16 * N);
+  if (e == cudaSuccess) e = cudaMalloc(&c->d_ladder_scan, 16 * N);
+  if (e == cudaSuccess) e = dalloc(&c->d_ncum, N);
+  if (e == cudaSuccess) e = dalloc(&c->d_donor, N);
+  if (e == cudaSuccess) e = dalloc(&c->d_partials, 2 * maxb);
+  if (e == cudaSuccess) e = dalloc(&c->d_ipartials, 2 * maxb);
+  if (e == cudaSuccess) e = dalloc(&c->d_scal, 1);
+  if (e == cudaSuccess) e = cudaMemset(c->d_scal, 0, sizeof(Scalars));
+  if (e == cudaSuccess) e = cudaMallocHost((void**)&c->h_scal, sizeof(Scalars));
+  if (e == cudaSuccess) {
+    c->cub_temp_bytes = cub_temp_needed((int)N);
+    e = cudaMalloc(&c->d_cub_temp, c->cub_temp_bytes ? c->cub_temp_bytes : 1);
+  }
+  for (int k = 0; k < 6 && e == cudaSuccess; ++k) e = cudaEventCreate(&c->ev[k]);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    g_create_error = std::string("CUDA: ") + cudaGetErrorString(e);
+    free_all(c);
+    delete c;
+    return (e == cudaErrorMemoryAllocation) ? MCS_E_OUT_OF_MEMORY : MCS_E_CUDA;
+  }
+  *out = c;
+  return MCS_OK;
+}
+
+mcs_status mcs_destroy(mcs_ctx* ctx) {
+  if (!ctx) return MCS_E_INVALID_ARG;
+  cudaSetDevice(ctx->dev);
+  cudaStreamSynchronize(ctx->stream);
+  free_all(ctx);
+  delete ctx;
+  return MCS_OK;
+}
+
+mcs_status mcs_set_stream(mcs_ctx* ctx, void* cuda_stream) {
+  CHECK_CTX(ctx);
+  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+  if (cuda_stream) {
+    ctx->stream = (cudaStream_t)cuda_stream;
+    ctx->own_stream = false;
+  } else {
+    CUDA_TRY(ctx, cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    ctx->own_stream = true;
+  }
+  return MCS_OK;
+}
+
+mcs_status mcs_get_sizes(const mcs_ctx* ctx, int32_t* n_local, int32_t* n_keyframes) {
+  if (!ctx) return MCS_E_INVALID_ARG;
+  if (n_local) *n_local = ctx->N;
+  if (n_keyframes) *n_keyframes = ctx->K;
+  return MCS_OK;
+}
+
+mcs_status mcs_add_keyframe(mcs_ctx* ctx, const float* mean3, const float* cov6, int32_t n,
+                            double path_length, int32_t* out_kf_id) {
+  CHECK_CTX(ctx);
+  if (!mean3 || !cov6 || n < 1) FAIL(ctx, MCS_E_INVALID_ARG, "mcs_add_keyframe: null or n < 1");
+  if (!std::isfinite(path_length)) FAIL(ctx, MCS_E_INVALID_ARG, "path_length not finite");
+  if (ctx->K >= ctx->capK) FAIL(ctx, MCS_E_CAPACITY, "capacity_keyframes (%d) reached", ctx->capK);
+  if (ctx->K > 0 && path_length < ctx->D.back())
+    FAIL(ctx, MCS_E_INVALID_ARG, "path_length must be non-decreasing (cumulative, R14)");
+  cudaStream_t st = ctx->stream;
+  float *dm = nullptr, *dc = nullptr;
+  int* bad = nullptr;
+  CUDA_TRY(ctx, cudaMallocAsync(&dm, sizeof(float) * 3 * n, st));
+  CUDA_TRY(ctx, cudaMallocAsync(&dc, sizeof(float) * 6 * n, st));
+  CUDA_TRY(ctx, cudaMallocAsync(&bad, sizeof(int), st));
+  CUDA_TRY(ctx, cudaMemsetAsync(bad, 0, sizeof(int), st));
+  CUDA_TRY(ctx, to_device(dm, mean3, sizeof(float) * 3 * n, st));
+  CUDA_TRY(ctx, to_device(dc, cov6, sizeof(float) * 6 * n, st));
+  validate_gauss_kernel<<<(n + 255) / 256, 256, 0, st>>>(dm, dc, n, bad);
+  int h_bad = 0;
+  CUDA_TRY(ctx, cudaMemcpyAsync(&h_bad, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(ctx, cudaStreamSynchronize(st));
+  if (h_bad) {
+    cudaFreeAsync(dm, st); cudaFreeAsync(dc, st); cudaFreeAsync(bad, st);
+    FAIL(ctx, MCS_E_INVALID_ARG, "%d keyframe points non-finite or covariance not SPD", h_bad);
+  }
+  KfHost kh;
+  int bad_cell = 0;
+  cudaError_t e = kf_build(ctx, dm, dc, n, kh, &bad_cell);
+  cudaFreeAsync(dm, st);
+  cudaFreeAsync(dc, st);
+  cudaFreeAsync(bad, st);
+  CUDA_TRY(ctx, e);
+  if (bad_cell)
+    FAIL(ctx, MCS_E_INVALID_ARG, "%d keyframe points outside the 21-bit cell range", bad_cell);
+  const int k = ctx->K;
+  KfMeta m;
+  m.keys = kh.keys;
+  m.payload = kh.payload;
+  int lg = 0;
+  while ((1 << lg) < kh.cap) ++lg;
+  m.shift = (uint32_t)(64 - lg);
+  m.mask = (uint32_t)(kh.cap - 1);
+  CUDA_TRY(ctx, cudaMemcpyAsync(ctx->d_kf_meta + k, &m, sizeof(m), cudaMemcpyHostToDevice, st));
+  CUDA_TRY(ctx, cudaMemcpyAsync(ctx->d_D + k, &path_length, sizeof(double), cudaMemcpyHostToDevice,
+                                st));
+  // lockstep extension: T_k^i := T_t^i (R24)
+  if (ctx->N > 0) {
+    fill_kf_from_current_kernel<<<(ctx->N + 255) / 256, 256, 0, st>>>(
+        ctx->d_pose, ctx->capN, ctx->N, ctx->d_kfpose, ctx->capK, k, k + 1);
+    CUDA_TRY(ctx, cudaGetLastError());
+  }
+  CUDA_TRY(ctx, cudaStreamSynchronize(st));
+  ctx->kf.push_back(kh);
+  ctx->D.push_back(path_length);
+  ctx->K = k + 1;
+  if (out_kf_id) *out_kf_id = k;
+  return MCS_OK;
+}
+
+mcs_status mcs_set_particles(mcs_ctx* ctx, int32_t n, const float* pose12,
+                             const float* kf_pose12, const double* cum_loglik) {
+  CHECK_CTX(ctx);
+  if (!pose12 || n < 1) FAIL(ctx, MCS_E_INVALID_ARG, "mcs_set_particles: null pose12 or n < 1");
+  if (n > ctx->capN) FAIL(ctx, MCS_E_CAPACITY, "n (%d) > capacity_particles (%d)", n, ctx->capN);
+  cudaStream_t st = ctx->stream;
+  const int K = ctx->K;
+  float *tp = nullptr, *tk = nullptr;
+  double* tl = nullptr;
+  int* bad = nullptr;
+  CUDA_TRY(ctx, cudaMallocAsync(&tp, sizeof(float) * 12 * n, st));
+  CUDA_TRY(ctx, cudaMallocAsync(&bad, sizeof(int), st));
+  CUDA_TRY(ctx, cudaMemsetAsync(bad, 0, sizeof(int), st));
+  CUDA_TRY(ctx, to_device(tp, pose12, sizeof(float) * 12 * n, st));
+  validate_poses_kernel<<<(n + 255) / 256, 256, 0, st>>>(tp, n, bad);
+  if (kf_pose12 && K > 0) {
+    const long long np = (long long)n * K;
+    CUDA_TRY(ctx, cudaMallocAsync(&tk, sizeof(float) * 12 * np, st));
+    CUDA_TRY(ctx, to_device(tk, kf_pose12, sizeof(float) * 12 * np, st));
+    validate_poses_kernel<<<(int)((np + 255) / 256), 256, 0, st>>>(tk, np, bad);
+  }
+  if (cum_loglik) {
+    CUDA_TRY(ctx, cudaMallocAsync(&tl, sizeof(double) * n, st));
+    CUDA_TRY(ctx, to_device(tl, cum_loglik, sizeof(double) * n, st));
+  }
+  int h_bad = 0;
+  CUDA_TRY(ctx, cudaMemcpyAsync(&h_bad, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(ctx, cudaStreamSynchronize(st));
+  bool lbad = false;
+  if (cum_loglik && !h_bad) {
+    std::vector<double> hl(n);
+    CUDA_TRY(ctx, cudaMemcpy(hl.data(), tl, sizeof(double) * n, cudaMemcpyDeviceToHost));
+    for (double v : hl) lbad |= !std::isfinite(v);
+  }
+  if (h_bad || lbad) {
+    cudaFreeAsync(tp, st);
+    if (tk) cudaFreeAsync(tk, st);
+    if (tl) cudaFreeAsync(tl, st);
+    cudaFreeAsync(bad, st);
+    FAIL(ctx, MCS_E_INVALID_ARG, "non-finite or non-orthonormal pose / non-finite L (%d)", h_bad);
+  }
+  // commit
+  aos_to_soa_kernel<<<(n + 255) / 256, 256, 0, st>>>(tp, n, ctx->capN, ctx->d_pose);
+  if (K > 0) {
+    if (tk) {
+      CUDA_TRY(ctx, cudaMemcpy2DAsync(ctx->d_kfpose, sizeof(float) * 12 * ctx->capK, tk,
+                                      sizeof(float) * 12 * K, sizeof(float) * 12 * K, n,
+                                      cudaMemcpyDeviceToDevice, st));
+    } else {
+      const long long tot = (long long)n * K;
+      fill_kf_from_current_kernel<<<(int)((tot + 255) / 256), 256, 0, st>>>(
+          ctx->d_pose, ctx->capN, n, ctx->d_kfpose, ctx->capK, 0, K);
+    }
+  }
+  if (tl) {
+    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->d_L, tl, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+  } else {
+    CUDA_TRY(ctx, cudaMemsetAsync(ctx->d_L, 0, sizeof(double) * n, st));
+  }
+  fill_double_kernel<<<(n + 255) / 256, 256, 0, st>>>(ctx->d_w, n, 1.0 / n);
+  CUDA_TRY(ctx, cudaGetLastError());
+  cudaFreeAsync(tp, st);
+  if (tk) cudaFreeAsync(tk, st);
+  if (tl) cudaFreeAsync(tl, st);
+  cudaFreeAsync(bad, st);
+  CUDA_TRY(ctx, cudaStreamSynchronize(st));
+  ctx->N = n;
+  return MCS_OK;
+}
+
+mcs_status mcs_get_particles(mcs_ctx* ctx, float* pose12, float* kf_pose12, double* cum_loglik,
+                             double* weight) {
+  CHECK_CTX(ctx);
+  cudaStream_t st = ctx->stream;
+  const int n = ctx->N, K = ctx->K;
+  if (n == 0) return MCS_OK;
+  if (pose12) {
+    float* tp = nullptr;
+    CUDA_TRY(ctx, cudaMallocAsync(&tp, sizeof(float) * 12 * n, st));
+    soa_to_aos_kernel<<<(n + 255) / 256, 256, 0, st>>>(ctx->d_pose, n, ctx->capN, tp);
+    CUDA_TRY(ctx, cudaMemcpyAsync(pose12, tp, sizeof(float) * 12 * n, cudaMemcpyDefault, st));
+    cudaFreeAsync(tp, st);
+  }
+  if (kf_pose12 && K > 0)
+    CUDA_TRY(ctx, cudaMemcpy2DAsync(kf_pose12, sizeof(float) * 12 * K, ctx->d_kfpose,
+                                    sizeof(float) * 12 * ctx->capK, sizeof(float) * 12 * K, n,
+                                    cudaMemcpyDefault, st));
+  if (cum_loglik)
+    CUDA_TRY(ctx, cudaMemcpyAsync(cum_loglik, ctx->d_L, sizeof(double) * n, cudaMemcpyDefault, st));
+  if (weight)
+    CUDA_TRY(ctx, cudaMemcpyAsync(weight, ctx->d_w, sizeof(double) * n, cudaMemcpyDefault, st));
+  CUDA_TRY(ctx, cudaStreamSynchronize(st));
+  return MCS_OK;
+}
+
+// validate a scan already in device memory (d_scan_raw layout: mean3 then cov6)
+static mcs_status validate_scan(mcs_ctx* ctx, int n_pts) {
+  int* bad = nullptr;
+  cudaStream_t st = ctx->stream;
+  CUDA_TRY(ctx, cudaMallocAsync(&bad, sizeof(int), st));
+  CUDA_TRY(ctx, cudaMemsetAsync(bad, 0, sizeof(int), st));
+  validate_gauss_kernel<<<(n_pts + 255) / 256, 256, 0, st>>>(
+      ctx->d_scan_raw, ctx->d_scan_raw + 3 * (size_t)ctx->capS, n_pts, bad);
+  int h_bad = 0;
+  CUDA_TRY(ctx, cudaMemcpyAsync(&h_bad, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+  cudaFreeAsync(bad, st);
+  CUDA_TRY(ctx, cudaStreamSynchronize(st));
+  if (h_bad) FAIL(ctx, MCS_E_INVALID_ARG, "%d scan points non-finite or covariance not SPD", h_bad);
+  return MCS_OK;
+}
+
+static mcs_status check_update_args(mcs_ctx* ctx, const void* m, const void* c, int n_pts,
+                                    double D_now) {
+  if (ctx->K < 1) FAIL(ctx, MCS_E_STATE, "no keyframe registered");
+  if (ctx->N < 1) FAIL(ctx, MCS_E_STATE, "no particles set");
+  if (!m || !c) FAIL(ctx, MCS_E_INVALID_ARG, "null scan");
+  if (n_pts < 1) FAIL(ctx, MCS_E_INVALID_ARG, "n_pts < 1");
+  if (n_pts > ctx->capS) FAIL(ctx, MCS_E_CAPACITY, "n_pts > capacity_scan_points");
+  if (!std::isfinite(D_now)) FAIL(ctx, MCS_E_INVALID_ARG, "D_now not finite");
+  return MCS_OK;
+}
+
+static void record(mcs_ctx* ctx, int k) {
+  if (ctx->profiling) cudaEventRecord(ctx->ev[k], ctx->stream);
+}
+
+// the hot path a1..a7, stream-ordered; scan already packed in d_scan
+static void run_update(mcs_ctx* ctx, int n_pts, double D_now, uint32_t U) {
+  record(ctx, 0);
+  launch_select(ctx, false);                                            // a1
+  record(ctx, 1);
+  launch_sweep(ctx, n_pts);                                             // a2
+  record(ctx, 2);
+  launch_combine(ctx, n_pts, false, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr);  // a3
+  launch_propagate(ctx, D_now);                                         // a4
+  record(ctx, 3);
+  launch_weights_resample(ctx, U);                                      // a5-a7
+  record(ctx, 4);
+}
+
+mcs_status mcs_update(mcs_ctx* ctx, const float* scan_mean3, const float* scan_cov6,
+                      int32_t n_pts, double D_now, uint32_t resample_u,
+                      const mcs_update_out* out) {
+  CHECK_CTX(ctx);
+  mcs_status s = check_update_args(ctx, scan_mean3, scan_cov6, n_pts, D_now);
+  if (s != MCS_OK) return s;
+  cudaStream_t st = ctx->stream;
+  float* raw_m = ctx->d_scan_raw;
+  float* raw_c = ctx->d_scan_raw + 3 * (size_t)ctx->capS;
+  CUDA_TRY(ctx, to_device(raw_m, scan_mean3, sizeof(float) * 3 * n_pts, st));
+  CUDA_TRY(ctx, to_device(raw_c, scan_cov6, sizeof(float) * 6 * n_pts, st));
+  s = validate_scan(ctx, n_pts);
+  if (s != MCS_OK) return s;
+  launch_pack_scan(raw_m, raw_c, n_pts, ctx->d_scan, st);
+  run_update(ctx, n_pts, D_now, resample_u);
+  CUDA_TRY(ctx, cudaGetLastError());
+  const int N = ctx->N;
+  if (out) {
+    // gather per-particle rows into a device staging area, then one copy per output
+    OutPtrs o{};
+    size_t off = 0;
+    auto take = [&](size_t bytes) { size_t p = off; off += (bytes + 255) & ~size_t(255); return p; };
+    const size_t o_l = take(8 * N), o_g = take(24 * N), o_h = take(84 * N), o_p = take(24 * N),
+                 o_w = take(8 * N), o_d = take(4 * N), o_f = take(N);
+    char* stage = nullptr;
+    CUDA_TRY(ctx, cudaMallocAsync((void**)&stage, off, st));
+    if (out->loglik) o.loglik = (double*)(stage + o_l);
+    if (out->grad6) o.grad6 = (float*)(stage + o_g);
+    if (out->hess21) o.hess21 = (float*)(stage + o_h);
+    if (out->psi6) o.psi6 = (float*)(stage + o_p);
+    if (out->weight) o.weight = (double*)(stage + o_w);
+    if (out->donor) o.donor = (int32_t*)(stage + o_d);
+    if (out->flags) o.flags = (uint8_t*)(stage + o_f);
+    gather_outputs_kernel<<<(N + 255) / 256, 256, 0, st>>>(
+        o, N, ctx->capN, ctx->d_l, ctx->d_grad, ctx->d_hess, ctx->d_psi, ctx->d_w, ctx->d_donor,
+        ctx->d_flags, ctx->d_scal, 0);
+    if (out->loglik) CUDA_TRY(ctx, cudaMemcpyAsync(out->loglik, o.loglik, 8 * N, cudaMemcpyDefault, st));
+    if (out->grad6) CUDA_TRY(ctx, cudaMemcpyAsync(out->grad6, o.grad6, 24 * N, cudaMemcpyDefault, st));
+    if (out->hess21) CUDA_TRY(ctx, cudaMemcpyAsync(out->hess21, o.hess21, 84 * N, cudaMemcpyDefault, st));
+    if (out->psi6) CUDA_TRY(ctx, cudaMemcpyAsync(out->psi6, o.psi6, 24 * N, cudaMemcpyDefault, st));
+    if (out->weight) CUDA_TRY(ctx, cudaMemcpyAsync(out->weight, o.weight, 8 * N, cudaMemcpyDefault, st));
+    if (out->donor) CUDA_TRY(ctx, cudaMemcpyAsync(out->donor, o.donor, 4 * N, cudaMemcpyDefault, st));
+    if (out->flags) CUDA_TRY(ctx, cudaMemcpyAsync(out->flags, o.flags, N, cudaMemcpyDefault, st));
+    cudaFreeAsync(stage, st);
+  }
+  CUDA_TRY(ctx, cudaMemcpyAsync(ctx->h_scal, ctx->d_scal, sizeof(Scalars), cudaMemcpyDeviceToHost,
+                                st));
+  CUDA_TRY(ctx, cudaStreamSynchronize(st));
+  if (out && out->representative) *out->representative = ctx->h_scal->rep;
+  if (out && out->n_dead) *out->n_dead = ctx->h_scal->D;
+  if (ctx->h_scal->status == MCS_E_DEGENERATE)
+    FAIL(ctx, MCS_E_DEGENERATE, "every particle dead (S:381); respawn skipped");
+  return MCS_OK;
+}
+
+mcs_status mcs_update_async(mcs_ctx* ctx, const float* d_scan_mean3, const float* d_scan_cov6,
+                            int32_t n_pts, double D_now, uint32_t resample_u,
+                            const mcs_update_out* d_out, void* cuda_stream) {
+  CHECK_CTX(ctx);
+  mcs_status s = check_update_args(ctx, d_scan_mean3, d_scan_cov6, n_pts, D_now);
+  if (s != MCS_OK) return s;
+  cudaStream_t saved = ctx->stream;
+  if (cuda_stream) ctx->stream = (cudaStream_t)cuda_stream;
+  launch_pack_scan(d_scan_mean3, d_scan_cov6, n_pts, ctx->d_scan, ctx->stream);
+  run_update(ctx, n_pts, D_now, resample_u);
+  if (d_out) {
+    OutPtrs o{d_out->loglik, d_out->grad6,  d_out->hess21,         d_out->psi6,  d_out->weight,
+              d_out->donor,  d_out->flags,  d_out->representative, d_out->n_dead};
+    gather_outputs_kernel<<<(ctx->N + 255) / 256, 256, 0, ctx->stream>>>(
+        o, ctx->N, ctx->capN, ctx->d_l, ctx->d_grad, ctx->d_hess, ctx->d_psi, ctx->d_w,
+        ctx->d_donor, ctx->d_flags, ctx->d_scal, 0);
+  }
+  cudaError_t e = cudaGetLastError();
+  ctx->stream = saved;
+  CUDA_TRY(ctx, e);
+  return MCS_OK;
+}
+
+mcs_status mcs_eval(mcs_ctx* ctx, const float* scan_mean3, const float* scan_cov6, int32_t n_pts,
+                    double* slot_loglik, float* slot_H21, float* slot_b6, int32_t* slot_n,
+                    int32_t* slot_kf, uint8_t* loop) {
+  CHECK_CTX(ctx);
+  mcs_status s = check_update_args(ctx, scan_mean3, scan_cov6, n_pts, 0.0);
+  if (s != MCS_OK) return s;
+  cudaStream_t st = ctx->stream;
+  float* raw_m = ctx->d_scan_raw;
+  float* raw_c = ctx->d_scan_raw + 3 * (size_t)ctx->capS;
+  CUDA_TRY(ctx, to_device(raw_m, scan_mean3, sizeof(float) * 3 * n_pts, st));
+  CUDA_TRY(ctx, to_device(raw_c, scan_cov6, sizeof(float) * 6 * n_pts, st));
+  s = validate_scan(ctx, n_pts);
+  if (s != MCS_OK) return s;
+  launch_pack_scan(raw_m, raw_c, n_pts, ctx->d_scan, st);
+  const size_t NS = (size_t)ctx->N * ctx->cfg.neighbor_count;
+  double* dl = nullptr;
+  float *dH = nullptr, *db = nullptr;
+  int32_t *dn = nullptr, *dk = nullptr;
+  uint8_t* dloop = nullptr;
+  CUDA_TRY(ctx, cudaMallocAsync(&dl, 8 * NS, st));
+  CUDA_TRY(ctx, cudaMallocAsync(&dH, 84 * NS, st));
+  CUDA_TRY(ctx, cudaMallocAsync(&db, 24 * NS, st));
+  CUDA_TRY(ctx, cudaMallocAsync(&dn, 4 * NS, st));
+  CUDA_TRY(ctx, cudaMallocAsync(&dk, 4 * NS, st));
+  CUDA_TRY(ctx, cudaMallocAsync(&dloop, ctx->N, st));
+  launch_select(ctx, true);
+  launch_sweep(ctx, n_pts);
+  launch_combine(ctx, n_pts, true, dl, dH, db, dn, dk, dloop);
+  CUDA_TRY(ctx, cudaGetLastError());
+  if (slot_loglik) CUDA_TRY(ctx, cudaMemcpyAsync(slot_loglik, dl, 8 * NS, cudaMemcpyDefault, st));
+  if (slot_H21) CUDA_TRY(ctx, cudaMemcpyAsync(slot_H21, dH, 84 * NS, cudaMemcpyDefault, st));
+  if (slot_b6) CUDA_TRY(ctx, cudaMemcpyAsync(slot_b6, db, 24 * NS, cudaMemcpyDefault, st));
+  if (slot_n) CUDA_TRY(ctx, cudaMemcpyAsync(slot_n, dn, 4 * NS, cudaMemcpyDefault, st));
+  if (slot_kf) CUDA_TRY(ctx, cudaMemcpyAsync(slot_kf, dk, 4 * NS, cudaMemcpyDefault, st));
+  if (loop) CUDA_TRY(ctx, cudaMemcpyAsync(loop, dloop, ctx->N, cudaMemcpyDefault, st));
+  cudaFreeAsync(dl, st); cudaFreeAsync(dH, st); cudaFreeAsync(db, st);
+  cudaFreeAsync(dn, st); cudaFreeAsync(dk, st); cudaFreeAsync(dloop, st);
+  CUDA_TRY(ctx, cudaStreamSynchronize(st));
+  return MCS_OK;
+}
+
+mcs_status mcs_resample(mcs_ctx* ctx, const double* e, const uint8_t* dead, int32_t n, uint32_t u,
+                        int32_t* donor_out) {
+  CHECK_CTX(ctx);
+  if (!e || !dead || !donor_out || n < 1) FAIL(ctx, MCS_E_INVALID_ARG, "mcs_resample: bad args");
+  if (n > ctx->capN) FAIL(ctx, MCS_E_CAPACITY, "n > capacity_particles");
+  cudaStream_t st = ctx->stream;
+  uint8_t* dd = nullptr;
+  double* de = nullptr;
+  CUDA_TRY(ctx, cudaMallocAsync(&dd, n, st));
+  CUDA_TRY(ctx, cudaMallocAsync(&de, 8 * (size_t)n, st));
+  CUDA_TRY(ctx, to_device(dd, dead, n, st));
+  CUDA_TRY(ctx, to_device(de, e, 8 * (size_t)n, st));
+  int32_t* ddon = nullptr;
+  CUDA_TRY(ctx, cudaMallocAsync(&ddon, 4 * (size_t)n, st));
+  launch_resample_only(ctx, de, dd, n, u, ddon);
+  CUDA_TRY(ctx, cudaGetLastError());
+  CUDA_TRY(ctx, cudaMemcpyAsync(donor_out, ddon, 4 * (size_t)n, cudaMemcpyDefault, st));
+  CUDA_TRY(ctx, cudaMemcpyAsync(ctx->h_scal, ctx->d_scal, sizeof(Scalars), cudaMemcpyDeviceToHost,
+                                st));
+  cudaFreeAsync(dd, st); cudaFreeAsync(de, st); cudaFreeAsync(ddon, st);
+  CUDA_TRY(ctx, cudaStreamSynchronize(st));
+  if (ctx->h_scal->status == MCS_E_DEGENERATE)
+    FAIL(ctx, MCS_E_DEGENERATE, "every particle dead (S:381)");
+  return MCS_OK;
+}
+
+mcs_status mcs_snapshot(mcs_ctx* ctx) {
+  CHECK_CTX(ctx);
+  const size_t bp = sizeof(float) * 12 * ctx->capN, bk = sizeof(float) * 12 * ctx->capN * ctx->capK,
+               bl = sizeof(double) * ctx->capN;
+  if (!ctx->d_snapshot) {
+    CUDA_TRY(ctx, cudaMalloc(&ctx->d_snapshot, bp + bk + bl));
+    ctx->snapshot_bytes = bp + bk + bl;
+  }
+  char* s = (char*)ctx->d_snapshot;
+  cudaStream_t st = ctx->stream;
+  CUDA_TRY(ctx, cudaMemcpyAsync(s, ctx->d_pose, bp, cudaMemcpyDeviceToDevice, st));
+  CUDA_TRY(ctx, cudaMemcpyAsync(s + bp, ctx->d_kfpose, bk, cudaMemcpyDeviceToDevice, st));
+  CUDA_TRY(ctx, cudaMemcpyAsync(s + bp + bk, ctx->d_L, bl, cudaMemcpyDeviceToDevice, st));
+  return MCS_OK;
+}
+
+mcs_status mcs_restore(mcs_ctx* ctx) {
+  CHECK_CTX(ctx);
+  if (!ctx->d_snapshot) FAIL(ctx, MCS_E_STATE, "no snapshot");
+  const size_t bp = sizeof(float) * 12 * ctx->capN, bk = sizeof(float) * 12 * ctx->capN * ctx->capK,
+               bl = sizeof(double) * ctx->capN;
+  char* s = (char*)ctx->d_snapshot;
+  cudaStream_t st = ctx->stream;
+  CUDA_TRY(ctx, cudaMemcpyAsync(ctx->d_pose, s, bp, cudaMemcpyDeviceToDevice, st));
+  CUDA_TRY(ctx, cudaMemcpyAsync(ctx->d_kfpose, s + bp, bk, cudaMemcpyDeviceToDevice, st));
+  CUDA_TRY(ctx, cudaMemcpyAsync(ctx->d_L, s + bp + bk, bl, cudaMemcpyDeviceToDevice, st));
+  return MCS_OK;
+}
+
+mcs_status mcs_set_profiling(mcs_ctx* ctx, int32_t enable) {
+  CHECK_CTX(ctx);
+  ctx->profiling = enable != 0;
+  return MCS_OK;
+}
+
+mcs_status mcs_get_phase_ms(const mcs_ctx* ctx, float* ms5) {
+  if (!ctx || !ms5) return MCS_E_INVALID_ARG;
+  if (!ctx->profiling) {
+    for (int k = 0; k < 5; ++k) ms5[k] = 0.f;
+    return MCS_OK;
+  }
+  // events of the last update (sync or async) on the context stream
+  if (cudaEventSynchronize(ctx->ev[4]) != cudaSuccess) return MCS_E_CUDA;
+  for (int k = 0; k < 4; ++k) cudaEventElapsedTime(&ms5[k], ctx->ev[k], ctx->ev[k + 1]);
+  cudaEventElapsedTime(&ms5[4], ctx->ev[0], ctx->ev[4]);
+  return MCS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,156 @@
+// kf_store.cu — a0: keyframe store + per-keyframe spatial hash, built once per keyframe
+// (P:88-91 shared keyframe clouds, Fig.2; P:112 voxel-based correspondence search).
+//
+// For keyframe k's Gaussians (mu', Sigma') in its own sensor frame: cell = floorf(mu' * (1/r))
+// per axis (pinned fp32, R27), one aggregate per occupied cell — mean of means and mean of
+// covariances accumulated in fp64 in input order (stable radix sort), stored
+// fp32 — inserted into an open-addressing table (power-of-two capacity, load <= 0.5,
+// multiplicative hash, linear probing).  One table serves every particle because it lives
+// in the keyframe frame.
+#include <cub/cub.cuh>
+
+#include "mcs_internal.cuh"
+
+namespace mcs {
+
+__global__ void cell_keys_kernel(const float* __restrict__ mean3, int n, float inv_r,
+                                 unsigned long long* __restrict__ keys, int* __restrict__ idx,
+                                 int* __restrict__ bad) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int c[3];
+  bool ok = true;
+  for (int a = 0; a < 3; ++a) {
+    float f = floorf(__fmul_rn(mean3[3 * i + a], inv_r));
+    ok = ok && (f >= (float)kCellMin && f <= (float)kCellMax);
+    c[a] = ok ? (int)f : 0;
+  }
+  if (!ok) atomicAdd(bad, 1);
+  keys[i] = pack_cell(c[0], c[1], c[2]);
+  idx[i] = i;
+}
+
+__global__ void heads_kernel(const unsigned long long* __restrict__ keys, int n,
+                             int* __restrict__ head) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  head[i] = (i == 0 || keys[i] != keys[i - 1]) ? 1 : 0;
+}
+
+__global__ void aggregate_insert_kernel(const unsigned long long* __restrict__ skeys,
+                                        const int* __restrict__ sidx, const int* __restrict__ head,
+                                        int n, const float* __restrict__ mean3,
+                                        const float* __restrict__ cov6,
+                                        unsigned long long* __restrict__ tkeys,
+                                        float4* __restrict__ payload, uint32_t shift,
+                                        uint32_t mask) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n || !head[i]) return;
+  const unsigned long long key = skeys[i];
+  double m[3] = {0, 0, 0}, s[6] = {0, 0, 0, 0, 0, 0};
+  int cnt = 0;
+  for (int j = i; j < n && skeys[j] == key; ++j) {  // members in input order (stable sort)
+    int p = sidx[j];
+    for (int a = 0; a < 3; ++a) m[a] += (double)mean3[3 * p + a];
+    for (int a = 0; a < 6; ++a) s[a] += (double)cov6[6 * p + a];
+    ++cnt;
+  }
+  for (int a = 0; a < 3; ++a) m[a] /= (double)cnt;
+  for (int a = 0; a < 6; ++a) s[a] /= (double)cnt;
+  uint32_t h = (uint32_t)((key * kHashMul) >> shift);
+  while (true) {
+    unsigned long long prev = atomicCAS(&tkeys[h], kEmptyKey, key);
+    if (prev == kEmptyKey) break;
+    h = (h + 1) & mask;
+  }
+  payload[3 * h + 0] = make_float4((float)m[0], (float)m[1], (float)m[2], (float)s[0]);
+  payload[3 * h + 1] = make_float4((float)s[1], (float)s[2], (float)s[3], (float)s[4]);
+  payload[3 * h + 2] = make_float4((float)s[5], __int_as_float(cnt), 0.f, 0.f);
+}
+
+cudaError_t kf_build(mcs_ctx* c, const float* d_mean3, const float* d_cov6, int n, KfHost& out,
+                     int* bad_cell) {
+  cudaStream_t st = c->stream;
+  float inv_r = 1.0f / c->cfg.voxel_resolution;
+  unsigned long long *keys = nullptr, *skeys = nullptr;
+  int *idx = nullptr, *sidx = nullptr, *head = nullptr, *cid = nullptr, *bad = nullptr;
+  void* temp = nullptr;
+  size_t tb1 = 0, tb2 = 0;
+  cudaError_t e = cudaSuccess;
+#define CK(x)                           \
+  do {                                  \
+    e = (x);                            \
+    if (e != cudaSuccess) goto cleanup; \
+  } while (0)
+  CK(cudaMallocAsync(&keys, sizeof(unsigned long long) * n, st));
+  CK(cudaMallocAsync(&skeys, sizeof(unsigned long long) * n, st));
+  CK(cudaMallocAsync(&idx, sizeof(int) * n, st));
+  CK(cudaMallocAsync(&sidx, sizeof(int) * n, st));
+  CK(cudaMallocAsync(&head, sizeof(int) * n, st));
+  CK(cudaMallocAsync(&cid, sizeof(int) * n, st));
+  CK(cudaMallocAsync(&bad, sizeof(int), st));
+  CK(cudaMemsetAsync(bad, 0, sizeof(int), st));
+  {
+    int g = (n + 255) / 256;
+    cell_keys_kernel<<<g, 256, 0, st>>>(d_mean3, n, inv_r, keys, idx, bad);
+    CK(cudaGetLastError());
+    cub::DeviceRadixSort::SortPairs(nullptr, tb1, keys, skeys, idx, sidx, n, 0, 63, st);
+    cub::DeviceScan::ExclusiveSum(nullptr, tb2, head, cid, n, st);
+    size_t tb = tb1 > tb2 ? tb1 : tb2;
+    CK(cudaMallocAsync(&temp, tb, st));
+    CK(cub::DeviceRadixSort::SortPairs(temp, tb, keys, skeys, idx, sidx, n, 0, 63, st));
+    heads_kernel<<<g, 256, 0, st>>>(skeys, n, head);
+    CK(cudaGetLastError());
+    CK(cub::DeviceScan::ExclusiveSum(temp, tb, head, cid, n, st));
+    int last_cid = 0, last_head = 0, h_bad = 0;
+    CK(cudaMemcpyAsync(&last_cid, cid + n - 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&last_head, head + n - 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&h_bad, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    *bad_cell = h_bad;
+    if (h_bad) goto cleanup;
+    int n_cells = last_cid + last_head;
+    int cap = 64, lg = 6;
+    while (cap < 2 * n_cells) { cap <<= 1; ++lg; }
+    out.cap = cap;
+    out.n_cells = n_cells;
+    out.n_points = n;
+    CK(cudaMalloc(&out.keys, sizeof(unsigned long long) * cap));
+    CK(cudaMalloc(&out.payload, sizeof(float4) * 3 * (size_t)cap));
+    CK(cudaMemsetAsync(out.keys, 0xFF, sizeof(unsigned long long) * cap, st));
+    CK(cudaMemsetAsync(out.payload, 0, sizeof(float4) * 3 * (size_t)cap, st));
+    aggregate_insert_kernel<<<g, 256, 0, st>>>(skeys, sidx, head, n, d_mean3, d_cov6, out.keys,
+                                               out.payload, (uint32_t)(64 - lg),
+                                               (uint32_t)(cap - 1));
+    CK(cudaGetLastError());
+  }
+cleanup:
+  cudaFreeAsync(keys, st);
+  cudaFreeAsync(skeys, st);
+  cudaFreeAsync(idx, st);
+  cudaFreeAsync(sidx, st);
+  cudaFreeAsync(head, st);
+  cudaFreeAsync(cid, st);
+  cudaFreeAsync(bad, st);
+  if (temp) cudaFreeAsync(temp, st);
+#undef CK
+  return e;
+}
+
+__global__ void pack_scan_kernel(const float* __restrict__ mean3, const float* __restrict__ cov6,
+                                 int S, float4* __restrict__ out) {
+  int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= S) return;
+  const float* m = mean3 + 3 * j;
+  const float* c = cov6 + 6 * j;
+  out[3 * j + 0] = make_float4(m[0], m[1], m[2], c[0]);
+  out[3 * j + 1] = make_float4(c[1], c[2], c[3], c[4]);
+  out[3 * j + 2] = make_float4(c[5], 0.f, 0.f, 0.f);
+}
+
+void launch_pack_scan(const float* mean3, const float* cov6, int S, float4* out,
+                      cudaStream_t st) {
+  pack_scan_kernel<<<(S + 255) / 256, 256, 0, st>>>(mean3, cov6, S, out);
+}
+
+}  // namespace mcs

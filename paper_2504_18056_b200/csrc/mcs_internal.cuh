@@ -1,0 +1,141 @@
+// mcs_internal.cuh — internal types of libmcs (B200 / sm_100a).  Not part of the ABI.
+//
+// HBM layout:
+//   current poses T_t      : SoA fp32 [12][Ncap]            (coalesced per element)
+//   keyframe poses T_k^i   : fp32 [Ncap][Kcap][12]          (a particle's map is contiguous:
+//                                                            clone = one memcpy)
+//   cumulative log-lik L   : fp64 [Ncap]                    (R22)
+//   keyframe hash tables   : per keyframe, keys u64 [cap] + payload float4 [cap][3]
+//   work items (a1 -> a2)  : float4 [3*Ncap][4]  = (kR|kt rows, {kf, particle, flags, 0})
+//   sweep partials (a2->a3): float [3*Ncap][32] = {l, n, H~21, b~6, pad}
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/mcs.h"
+
+namespace mcs {
+
+constexpr unsigned long long kEmptyKey = ~0ull;  // bit 63 set: never a packed cell key
+constexpr int kCellMin = -1048576;               // 21-bit signed cell coordinates (R27)
+constexpr int kCellMax = 1048575;
+constexpr unsigned long long kHashMul = 0x9E3779B97F4A7C15ull;
+constexpr int kSlotFloats = 32;                   // sweep partial record per (particle, slot)
+constexpr int kMaxNb = MCS_MAX_NEIGHBORS;
+
+struct KfMeta {                 // one per keyframe (device array, read through L1)
+  const unsigned long long* keys;
+  const float4* payload;        // [cap][3]: {mu'x,mu'y,mu'z,S'xx} {S'xy,S'xz,S'yy,S'yz} {S'zz,cnt,0,0}
+  uint32_t shift;               // 64 - log2(cap)
+  uint32_t mask;                // cap - 1
+};
+
+__host__ __device__ inline unsigned long long pack_cell(int x, int y, int z) {
+  return ((unsigned long long)(x & 0x1FFFFF) << 42) | ((unsigned long long)(y & 0x1FFFFF) << 21) |
+         (unsigned long long)(z & 0x1FFFFF);
+}
+
+struct KfHost {
+  unsigned long long* keys = nullptr;
+  float4* payload = nullptr;
+  int32_t cap = 0, n_cells = 0, n_points = 0;
+};
+
+struct Scalars {                // device-side reduction results of one update
+  double m;                     // max_i L_i (after L += l)
+  double lstar;                 // max_i l_i
+  double S;                     // sum_i exp(L_i - m)
+  unsigned long long Q;         // survivor ladder total
+  long long D;                  // dead count
+  double m2, S2;                // after respawn
+  int32_t rep;                  // representative (global index)
+  int32_t status;               // 0 ok, MCS_E_DEGENERATE
+  double wbest;
+  unsigned int counter[8];      // last-block counters (reset by the last block)
+};
+
+}  // namespace mcs
+
+struct mcs_ctx {
+  mcs_config cfg{};
+  int dev = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  std::string err;
+  mcs_status sticky = MCS_OK;
+  bool profiling = false;
+  float phase_ms[5] = {0, 0, 0, 0, 0};
+  cudaEvent_t ev[6] = {};
+
+  // keyframe store (a0)
+  int K = 0;
+  std::vector<mcs::KfHost> kf;
+  std::vector<double> D;        // shared cumulative odometry path length per keyframe (R14)
+  mcs::KfMeta* d_kf_meta = nullptr;
+  double* d_D = nullptr;
+
+  // particle state
+  int N = 0;                    // local particles
+  float* d_pose = nullptr;      // [12][Ncap]
+  float* d_kfpose = nullptr;    // [Ncap][Kcap][12]
+  double* d_L = nullptr;        // [Ncap]
+  void* d_snapshot = nullptr;   // mcs_snapshot buffer
+  size_t snapshot_bytes = 0;
+
+  // per-update scratch
+  float* d_scan_raw = nullptr;  // [Scap][9]
+  float4* d_scan = nullptr;     // [Scap][3]
+  float4* d_items = nullptr;    // [nb*Ncap][4]
+  int32_t* d_order = nullptr;   // [nb*Ncap] sweep order (item ids)
+  float* d_part = nullptr;      // [nb*Ncap][32]
+  uint8_t* d_meta = nullptr;    // [Ncap] bit0 loop
+  int32_t* d_to = nullptr;      // [Ncap] oldest neighbour keyframe t_o
+  double* d_l = nullptr;        // [Ncap] l_i
+  double* d_psi = nullptr;      // [6][Ncap] fp64 psi
+  float* d_grad = nullptr;      // [6][Ncap]
+  float* d_hess = nullptr;      // [21][Ncap]
+  uint8_t* d_flags = nullptr;   // [Ncap]
+  double* d_e = nullptr;        // [Ncap]
+  double* d_w = nullptr;        // [Ncap]
+  void* d_ladder = nullptr;     // [Ncap] {u64 C, u32 dead}
+  void* d_ladder_scan = nullptr;
+  long long* d_ncum = nullptr;  // [Ncap]
+  int32_t* d_donor = nullptr;   // [Ncap]
+  double* d_partials = nullptr; // [4][max_blocks]
+  int32_t* d_ipartials = nullptr;
+  mcs::Scalars* d_scal = nullptr;
+  mcs::Scalars* h_scal = nullptr;  // pinned
+  void* d_cub_temp = nullptr;
+  size_t cub_temp_bytes = 0;
+  int32_t capN = 0, capK = 0, capS = 0, nbcap = 0;
+};
+
+namespace mcs {
+
+// ---- launchers (all stream-ordered on ctx->stream) ----
+// a0: build keyframe k's table from device mean3/cov6 (n points).  Returns cudaError.
+cudaError_t kf_build(mcs_ctx* c, const float* d_mean3, const float* d_cov6, int n, KfHost& out,
+                     int* bad_cell);
+// pack raw [S][3] + [S][6] into the sweep's float4 x3 layout
+void launch_pack_scan(const float* mean3, const float* cov6, int S, float4* out,
+                      cudaStream_t st);
+// a1
+void launch_select(mcs_ctx* c, bool eval_mode);
+// a2
+void launch_sweep(mcs_ctx* c, int S);
+// a3 (+ L += l and max partials when !eval_mode)
+void launch_combine(mcs_ctx* c, int S, bool eval_mode, double* slot_l, float* slot_H21,
+                    float* slot_b6, int32_t* slot_n, int32_t* slot_kf, uint8_t* loop_out);
+// a4
+void launch_propagate(mcs_ctx* c, double D_now);
+// a5-a7; returns nothing, status in d_scal
+void launch_weights_resample(mcs_ctx* c, uint32_t U);
+// isolated respawn on caller arrays
+void launch_resample_only(mcs_ctx* c, const double* d_e, const uint8_t* d_dead, int n,
+                          uint32_t U, int32_t* d_donor);
+size_t cub_temp_needed(int n);
+
+}  // namespace mcs

@@ -1,0 +1,107 @@
+// select.cu — a1: neighbour keyframes, loop flag, relative poses (
+// Fig.3).
+//
+// One thread per particle:
+//   d_k = ||t_k^i - t_t^i||^2 with the pinned fp32 order fmaf(dz,dz,fmaf(dy,dy,dx*dx)) (R6, R27)
+//   the nb = min(neighbor_count, K) smallest (d, k), ties -> lower id
+//   loop_i = exists slot with id <= latest - gap (R5);  t_o = min slot id
+//   kT = (T_k^i)^-1 T_t^i per slot, pinned fp32: R = Rk^T Rt, t = Rk^T (t_t - t_k),
+//   each entry fmaf(x2,y2, fmaf(x1,y1, x0*y0)) (R27) — the same correspondences as the oracle.
+// Writes one 64-byte work item per (particle, slot) for the sweep:
+//   float4 rows {R00 R01 R02 tx}{R10 R11 R12 ty}{R20 R21 R22 tz}, int4 {kf, particle, flags, 0}
+//   flags bit0: accumulate H~, b~ (slot in G, R4).
+#include "mcs_internal.cuh"
+
+namespace mcs {
+
+__global__ void select_kernel(const float* __restrict__ pose, int capN, int N,
+                              const float* __restrict__ kfpose, int capK, int K, int nb_max,
+                              int gap, int gn_all, int eval_mode, float4* __restrict__ items,
+                              uint8_t* __restrict__ meta, int32_t* __restrict__ t_o_out) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  float Tt[12];
+#pragma unroll
+  for (int e = 0; e < 12; ++e) Tt[e] = pose[(size_t)e * capN + i];
+  const float* kp = kfpose + (size_t)i * capK * 12;
+  const int nb = K < nb_max ? K : nb_max;
+  float bd[kMaxNb];
+  int bk[kMaxNb];
+#pragma unroll
+  for (int s = 0; s < kMaxNb; ++s) { bd[s] = 0.f; bk[s] = -1; }
+  for (int k = 0; k < K; ++k) {
+    const float* Tk = kp + 12 * k;
+    float dx = __fsub_rn(Tk[3], Tt[3]);
+    float dy = __fsub_rn(Tk[7], Tt[7]);
+    float dz = __fsub_rn(Tk[11], Tt[11]);
+    float d = __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, __fmul_rn(dx, dx)));
+    // insertion into the sorted top-nb list; strict < keeps the lower id on ties
+#pragma unroll
+    for (int s = 0; s < kMaxNb; ++s) {
+      if (s < nb && (bk[s] < 0 || d < bd[s])) {
+        for (int u = kMaxNb - 1; u > s; --u) { bd[u] = bd[u - 1]; bk[u] = bk[u - 1]; }
+        bd[s] = d;
+        bk[s] = k;
+        break;
+      }
+    }
+  }
+  const int latest = K - 1;
+  int loop = 0, t_o = bk[0];
+  for (int s = 0; s < nb; ++s) {
+    loop |= (bk[s] <= latest - gap);
+    t_o = bk[s] < t_o ? bk[s] : t_o;
+  }
+  meta[i] = (uint8_t)loop;
+  t_o_out[i] = t_o;
+  for (int s = 0; s < nb_max; ++s) {
+    float4* it = items + 4 * ((size_t)s * capN + i);
+    const int k = s < nb ? bk[s] : -1;
+    if (k < 0) {
+      it[3] = make_float4(__int_as_float(-1), __int_as_float(i), __int_as_float(0), 0.f);
+      continue;
+    }
+    const float* Tk = kp + 12 * k;
+    float Rk[9], d[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+#pragma unroll
+      for (int b = 0; b < 3; ++b) Rk[3 * a + b] = Tk[4 * a + b];
+      d[a] = __fsub_rn(Tt[4 * a + 3], Tk[4 * a + 3]);
+    }
+    float rel[12];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+#pragma unroll
+      for (int b = 0; b < 3; ++b)
+        rel[4 * a + b] = __fmaf_rn(Rk[6 + a], Tt[8 + b],
+                                   __fmaf_rn(Rk[3 + a], Tt[4 + b], __fmul_rn(Rk[a], Tt[b])));
+      rel[4 * a + 3] =
+          __fmaf_rn(Rk[6 + a], d[2], __fmaf_rn(Rk[3 + a], d[1], __fmul_rn(Rk[a], d[0])));
+    }
+    const int in_G = gn_all ? 1 : (k <= latest - gap);
+    const int flags = (eval_mode || in_G) ? 1 : 0;
+    it[0] = make_float4(rel[0], rel[1], rel[2], rel[3]);
+    it[1] = make_float4(rel[4], rel[5], rel[6], rel[7]);
+    it[2] = make_float4(rel[8], rel[9], rel[10], rel[11]);
+    it[3] = make_float4(__int_as_float(k), __int_as_float(i), __int_as_float(flags), 0.f);
+  }
+}
+
+__global__ void iota_kernel(int32_t* __restrict__ order, int nb, int capN, int N) {
+  int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nb * N) return;
+  int s = t / N, i = t - s * N;
+  order[t] = s * capN + i;
+}
+
+void launch_select(mcs_ctx* c, bool eval_mode) {
+  const int N = c->N;
+  const int nb_max = c->cfg.neighbor_count;
+  select_kernel<<<(N + 127) / 128, 128, 0, c->stream>>>(
+      c->d_pose, c->capN, N, c->d_kfpose, c->capK, c->K, nb_max, c->cfg.loop_recency_gap,
+      c->cfg.gn_slots == MCS_GN_ALL_SLOTS, eval_mode ? 1 : 0, c->d_items, c->d_meta, c->d_to);
+  iota_kernel<<<(nb_max * N + 255) / 256, 256, 0, c->stream>>>(c->d_order, nb_max, c->capN, N);
+}
+
+}  // namespace mcs

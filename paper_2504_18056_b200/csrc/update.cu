@@ -1,0 +1,399 @@
+// update.cu — a3: combine slots + Gauss-Newton current-pose update (Eqs.2, 5-7; P:114,
+// P:125-135), fused with L += l and the first weight reduction (Eq.11);
+// a4: keyframe-pose propagation (Eqs.8-10).
+//
+// a3, one thread per particle, fp64 from the fp32 sweep partials:
+//   H_s = B_s^T H~_s B_s, b_s = B_s^T b~_s, B_s = blockdiag(kR_s, kR_s)  (body frame of T_t)
+//   l_i = sum_s l_s - kappa sum_s (S - n_s)                    (Eq.2; R8)
+//   H = sum_{s in G} H_s, b = sum_{s in G} b_s, g = -2b         (R3, R4)
+//   loop_i: lambda = damping_rel tr(H)/6; psi = -(H + lambda I)^-1 b (Cholesky; R1, R11);
+//           clamp ||psi|| <= step_clamp; T_t <- T_t exp(psi) (Eq.7) + one Newton
+//           re-orthonormalisation step (R30); non-PD -> flag singular, no update.
+// a4, one thread per (particle, keyframe): for updated particles and t_o <= k <= latest,
+//   r_k = (D_k - D_{t_o}) / (D_now - D_{t_o}) (R14, R15); T_k <- T_k exp(r_k psi) (Eq.10, R16).
+#include "mcs_internal.cuh"
+#include "reduce.cuh"
+
+namespace mcs {
+
+__device__ void se3_exp_d(const double xi[6], double T[12]) {
+  const double px = xi[3], py = xi[4], pz = xi[5];
+  const double th2 = px * px + py * py + pz * pz;
+  const double th = sqrt(th2);
+  double A, B, C;
+  if (th < 1e-4) {
+    A = 1.0 - th2 / 6.0 + th2 * th2 / 120.0;
+    B = 0.5 - th2 / 24.0 + th2 * th2 / 720.0;
+    C = 1.0 / 6.0 - th2 / 120.0 + th2 * th2 / 5040.0;
+  } else {
+    double s, c;
+    sincos(th, &s, &c);
+    A = s / th;
+    B = (1.0 - c) / th2;
+    C = (th - s) / (th2 * th);
+  }
+  const double W[9] = {0.0, -pz, py, pz, 0.0, -px, -py, px, 0.0};
+  double W2[9];
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int b = 0; b < 3; ++b)
+      W2[3 * a + b] = W[3 * a] * W[b] + W[3 * a + 1] * W[3 + b] + W[3 * a + 2] * W[6 + b];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    double v[3];
+#pragma unroll
+    for (int b = 0; b < 3; ++b) {
+      const double I = (a == b) ? 1.0 : 0.0;
+      T[4 * a + b] = I + A * W[3 * a + b] + B * W2[3 * a + b];
+      v[b] = I + B * W[3 * a + b] + C * W2[3 * a + b];
+    }
+    T[4 * a + 3] = v[0] * xi[0] + v[1] * xi[1] + v[2] * xi[2];
+  }
+}
+
+// T32 <- round_fp32( Newton( T32 * exp(xi) ) )   (Eq.7 / Eq.10, R23, R30)
+__device__ void pose_right_update(float T32[12], const double xi[6]) {
+  double E[12], TE[12];
+  se3_exp_d(xi, E);
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      double s = (b == 3) ? (double)T32[4 * a + 3] : 0.0;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) s += (double)T32[4 * a + c] * E[4 * c + b];
+      TE[4 * a + b] = s;
+    }
+  }
+  double RtR[9];
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int b = 0; b < 3; ++b) {
+      double s = 0.0;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) s += TE[4 * c + a] * TE[4 * c + b];
+      RtR[3 * a + b] = s;
+    }
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+#pragma unroll
+    for (int b = 0; b < 3; ++b) {
+      double s = 0.0;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) s += TE[4 * a + c] * (((c == b) ? 3.0 : 0.0) - RtR[3 * c + b]);
+      T32[4 * a + b] = (float)(0.5 * s);
+    }
+    T32[4 * a + 3] = (float)TE[4 * a + 3];
+  }
+}
+
+__device__ __forceinline__ int up_idx(int r, int c) {  // r <= c
+  return r * 6 - (r * (r - 1)) / 2 + (c - r);
+}
+
+struct CombineArgs {
+  const float4* items;
+  const float* part;
+  const uint8_t* meta;
+  float* pose;
+  double* L;
+  double* l_out;
+  double* psi;
+  float* grad;
+  float* hess;
+  uint8_t* flags;
+  double* partials;  // [2][grid]
+  Scalars* scal;
+  int capN, N, K, nb_max, S, gap, gn_all, eval_mode;
+  double kappa, damping, clamp;
+  // eval outputs (device, may be null)
+  double* slot_l;
+  float* slot_H21;
+  float* slot_b6;
+  int32_t* slot_n;
+  int32_t* slot_kf;
+  uint8_t* loop_out;
+};
+
+__global__ void __launch_bounds__(128) combine_kernel(CombineArgs a) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  double l = -INFINITY, Lnew = -INFINITY;
+  if (i < a.N) {
+    const int nb = a.K < a.nb_max ? a.K : a.nb_max;
+    const int latest = a.K - 1;
+    double H[21], b[6];
+#pragma unroll
+    for (int k = 0; k < 21; ++k) H[k] = 0.0;
+#pragma unroll
+    for (int k = 0; k < 6; ++k) b[k] = 0.0;
+    double lsum = 0.0;
+    long long unmatched = 0;
+    for (int s = 0; s < a.nb_max; ++s) {
+      const size_t item = (size_t)s * a.capN + i;
+      if (s >= nb) {
+        if (a.eval_mode) {
+          const size_t o = (size_t)i * a.nb_max + s;
+          if (a.slot_l) a.slot_l[o] = 0.0;
+          if (a.slot_n) a.slot_n[o] = 0;
+          if (a.slot_kf) a.slot_kf[o] = -1;
+          if (a.slot_H21) for (int k = 0; k < 21; ++k) a.slot_H21[o * 21 + k] = 0.f;
+          if (a.slot_b6) for (int k = 0; k < 6; ++k) a.slot_b6[o * 6 + k] = 0.f;
+        }
+        continue;
+      }
+      const float4 r0 = a.items[4 * item + 0], r1 = a.items[4 * item + 1],
+                   r2 = a.items[4 * item + 2], inf = a.items[4 * item + 3];
+      const int kf = __float_as_int(inf.x);
+      const double R[9] = {r0.x, r0.y, r0.z, r1.x, r1.y, r1.z, r2.x, r2.y, r2.z};
+      const float* o = a.part + item * kSlotFloats;
+      const double ls = (double)o[0];
+      const int ns = __float_as_int(o[1]);
+      const bool in_G = a.gn_all ? true : (kf <= latest - a.gap);
+      lsum += ls;
+      unmatched += a.S - ns;
+      if (!(in_G || a.eval_mode)) continue;
+      // full symmetric H~ in the rotated frame
+      double Ht[36];
+#pragma unroll
+      for (int r = 0; r < 6; ++r)
+#pragma unroll
+        for (int c = r; c < 6; ++c) {
+          const double v = (double)o[2 + up_idx(r, c)];
+          Ht[6 * r + c] = v;
+          Ht[6 * c + r] = v;
+        }
+      double bt[6];
+#pragma unroll
+      for (int k = 0; k < 6; ++k) bt[k] = (double)o[23 + k];
+      // H_s = B^T H~ B, b_s = B^T b~ with B = blockdiag(R, R)
+      double Hs[36], bs[6];
+#pragma unroll
+      for (int p = 0; p < 2; ++p)
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          double T[9];  // H~_pq R
+#pragma unroll
+          for (int x = 0; x < 3; ++x)
+#pragma unroll
+            for (int y = 0; y < 3; ++y)
+              T[3 * x + y] = Ht[6 * (3 * p + x) + 3 * q + 0] * R[0 * 3 + y] +
+                             Ht[6 * (3 * p + x) + 3 * q + 1] * R[1 * 3 + y] +
+                             Ht[6 * (3 * p + x) + 3 * q + 2] * R[2 * 3 + y];
+#pragma unroll
+          for (int x = 0; x < 3; ++x)
+#pragma unroll
+            for (int y = 0; y < 3; ++y)
+              Hs[6 * (3 * p + x) + 3 * q + y] =
+                  R[0 * 3 + x] * T[0 * 3 + y] + R[1 * 3 + x] * T[1 * 3 + y] +
+                  R[2 * 3 + x] * T[2 * 3 + y];
+        }
+#pragma unroll
+      for (int p = 0; p < 2; ++p)
+#pragma unroll
+        for (int x = 0; x < 3; ++x)
+          bs[3 * p + x] = R[0 * 3 + x] * bt[3 * p + 0] + R[1 * 3 + x] * bt[3 * p + 1] +
+                          R[2 * 3 + x] * bt[3 * p + 2];
+      if (a.eval_mode) {
+        const size_t so = (size_t)i * a.nb_max + s;
+        if (a.slot_l) a.slot_l[so] = ls;
+        if (a.slot_n) a.slot_n[so] = ns;
+        if (a.slot_kf) a.slot_kf[so] = kf;
+        if (a.slot_H21)
+          for (int r = 0; r < 6; ++r)
+            for (int c = r; c < 6; ++c) a.slot_H21[so * 21 + up_idx(r, c)] = (float)Hs[6 * r + c];
+        if (a.slot_b6)
+          for (int k = 0; k < 6; ++k) a.slot_b6[so * 6 + k] = (float)bs[k];
+      }
+      if (in_G) {
+#pragma unroll
+        for (int r = 0; r < 6; ++r)
+#pragma unroll
+          for (int c = r; c < 6; ++c) H[up_idx(r, c)] += Hs[6 * r + c];
+#pragma unroll
+        for (int k = 0; k < 6; ++k) b[k] += bs[k];
+      }
+    }
+    l = lsum - a.kappa * (double)unmatched;
+    const uint8_t loop = a.meta[i] & 1;
+    if (a.eval_mode) {
+      if (a.loop_out) a.loop_out[i] = loop;
+    } else {
+      uint8_t flags = loop;
+      double psi[6] = {0, 0, 0, 0, 0, 0};
+      if (loop) {
+        // Eq.5 with Levenberg damping (R11): (H + lambda I) psi = -b via Cholesky
+        double A[36];
+#pragma unroll
+        for (int r = 0; r < 6; ++r)
+#pragma unroll
+          for (int c = r; c < 6; ++c) { A[6 * r + c] = H[up_idx(r, c)]; A[6 * c + r] = A[6 * r + c]; }
+        double tr = A[0] + A[7] + A[14] + A[21] + A[28] + A[35];
+        const double lam = a.damping * tr / 6.0;
+#pragma unroll
+        for (int k = 0; k < 6; ++k) A[7 * k] += lam;
+        double Lc[36];
+        bool ok = true;
+#pragma unroll
+        for (int k = 0; k < 36; ++k) Lc[k] = 0.0;
+        for (int j = 0; j < 6 && ok; ++j) {
+          double d = A[6 * j + j];
+          for (int k = 0; k < j; ++k) d -= Lc[6 * j + k] * Lc[6 * j + k];
+          if (!(d > 0.0)) { ok = false; break; }
+          Lc[6 * j + j] = sqrt(d);
+          for (int r = j + 1; r < 6; ++r) {
+            double s = A[6 * r + j];
+            for (int k = 0; k < j; ++k) s -= Lc[6 * r + k] * Lc[6 * j + k];
+            Lc[6 * r + j] = s / Lc[6 * j + j];
+          }
+        }
+        if (!ok) {
+          flags |= 4;
+        } else {
+          double z[6];
+          for (int r = 0; r < 6; ++r) {
+            double s = -b[r];
+            for (int k = 0; k < r; ++k) s -= Lc[6 * r + k] * z[k];
+            z[r] = s / Lc[6 * r + r];
+          }
+          for (int r = 5; r >= 0; --r) {
+            double s = z[r];
+            for (int k = r + 1; k < 6; ++k) s -= Lc[6 * k + r] * psi[k];
+            psi[r] = s / Lc[6 * r + r];
+          }
+          double nrm = 0.0;
+#pragma unroll
+          for (int k = 0; k < 6; ++k) nrm += psi[k] * psi[k];
+          nrm = sqrt(nrm);
+          if (nrm > a.clamp) {
+#pragma unroll
+            for (int k = 0; k < 6; ++k) psi[k] *= a.clamp / nrm;
+            flags |= 16;
+          }
+          flags |= 2;
+          bool nz = false;
+#pragma unroll
+          for (int k = 0; k < 6; ++k) nz |= (psi[k] != 0.0);
+          if (nz) {
+            float T[12];
+#pragma unroll
+            for (int e = 0; e < 12; ++e) T[e] = a.pose[(size_t)e * a.capN + i];
+            pose_right_update(T, psi);
+#pragma unroll
+            for (int e = 0; e < 12; ++e) a.pose[(size_t)e * a.capN + i] = T[e];
+          }
+        }
+      }
+      a.l_out[i] = l;
+#pragma unroll
+      for (int k = 0; k < 6; ++k) {
+        a.psi[(size_t)k * a.capN + i] = psi[k];
+        a.grad[(size_t)k * a.capN + i] = (float)(-2.0 * b[k]);
+      }
+#pragma unroll
+      for (int k = 0; k < 21; ++k) a.hess[(size_t)k * a.capN + i] = (float)H[k];
+      a.flags[i] = flags;
+      Lnew = a.L[i] + l;  // Eq.11 in log space (R22)
+      a.L[i] = Lnew;
+    }
+  }
+  if (a.eval_mode) return;
+  // first weight reduction: max L, max l  (a5)
+  const double bm = block_reduce(Lnew, MaxOp(), -INFINITY);
+  const double bl = block_reduce(l, MaxOp(), -INFINITY);
+  if (threadIdx.x == 0) {
+    a.partials[blockIdx.x] = bm;
+    a.partials[gridDim.x + blockIdx.x] = bl;
+  }
+  if (last_block(&a.scal->counter[0])) {
+    double m = -INFINITY, ls = -INFINITY;
+    for (int k = threadIdx.x; k < (int)gridDim.x; k += blockDim.x) {
+      m = fmax(m, a.partials[k]);
+      ls = fmax(ls, a.partials[gridDim.x + k]);
+    }
+    m = block_reduce(m, MaxOp(), -INFINITY);
+    ls = block_reduce(ls, MaxOp(), -INFINITY);
+    if (threadIdx.x == 0) {
+      a.scal->m = m;
+      a.scal->lstar = ls;
+    }
+  }
+}
+
+void launch_combine(mcs_ctx* c, int S, bool eval_mode, double* slot_l, float* slot_H21,
+                    float* slot_b6, int32_t* slot_n, int32_t* slot_kf, uint8_t* loop_out) {
+  CombineArgs a;
+  a.items = c->d_items;
+  a.part = c->d_part;
+  a.meta = c->d_meta;
+  a.pose = c->d_pose;
+  a.L = c->d_L;
+  a.l_out = c->d_l;
+  a.psi = c->d_psi;
+  a.grad = c->d_grad;
+  a.hess = c->d_hess;
+  a.flags = c->d_flags;
+  a.partials = c->d_partials;
+  a.scal = c->d_scal;
+  a.capN = c->capN;
+  a.N = c->N;
+  a.K = c->K;
+  a.nb_max = c->cfg.neighbor_count;
+  a.S = S;
+  a.gap = c->cfg.loop_recency_gap;
+  a.gn_all = c->cfg.gn_slots == MCS_GN_ALL_SLOTS;
+  a.eval_mode = eval_mode ? 1 : 0;
+  a.kappa = c->cfg.unmatched_penalty;
+  a.damping = c->cfg.damping_rel;
+  a.clamp = c->cfg.step_clamp;
+  a.slot_l = slot_l;
+  a.slot_H21 = slot_H21;
+  a.slot_b6 = slot_b6;
+  a.slot_n = slot_n;
+  a.slot_kf = slot_kf;
+  a.loop_out = loop_out;
+  const int grid = (c->N + 127) / 128;
+  combine_kernel<<<grid, 128, 0, c->stream>>>(a);
+}
+
+__global__ void propagate_kernel(float* __restrict__ kfpose, int capK, int K, int N,
+                                 const uint8_t* __restrict__ flags, const int32_t* __restrict__ to,
+                                 const double* __restrict__ psi, int capN,
+                                 const double* __restrict__ D, double D_now) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (long long)N * K) return;
+  const int i = (int)(t / K), k = (int)(t - (long long)i * K);
+  if (!(flags[i] & 2)) return;
+  const int t_o = to[i];
+  if (k < t_o) return;  // older keyframes untouched (R15)
+  const double den = D_now - D[t_o];
+  if (!(den > 0.0)) return;
+  const double r = (D[k] - D[t_o]) / den;  // Eqs.8-9 (R14)
+  if (r == 0.0) return;
+  double xi[6];
+#pragma unroll
+  for (int c = 0; c < 6; ++c) xi[c] = r * psi[(size_t)c * capN + i];
+  float* Tk = kfpose + ((size_t)i * capK + k) * 12;
+  float T[12];
+  const float4* p4 = reinterpret_cast<const float4*>(Tk);
+  float4 v0 = p4[0], v1 = p4[1], v2 = p4[2];
+  T[0] = v0.x; T[1] = v0.y; T[2] = v0.z; T[3] = v0.w;
+  T[4] = v1.x; T[5] = v1.y; T[6] = v1.z; T[7] = v1.w;
+  T[8] = v2.x; T[9] = v2.y; T[10] = v2.z; T[11] = v2.w;
+  pose_right_update(T, xi);  // Eq.10
+  float4* q4 = reinterpret_cast<float4*>(Tk);
+  q4[0] = make_float4(T[0], T[1], T[2], T[3]);
+  q4[1] = make_float4(T[4], T[5], T[6], T[7]);
+  q4[2] = make_float4(T[8], T[9], T[10], T[11]);
+}
+
+void launch_propagate(mcs_ctx* c, double D_now) {
+  const long long total = (long long)c->N * c->K;
+  if (total == 0) return;
+  const int grid = (int)((total + 255) / 256);
+  propagate_kernel<<<grid, 256, 0, c->stream>>>(c->d_kfpose, c->capK, c->K, c->N, c->d_flags,
+                                                c->d_to, c->d_psi, c->capN, c->d_D, D_now);
+}
+
+}  // namespace mcs

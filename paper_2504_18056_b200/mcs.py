@@ -1,0 +1,318 @@
+"""Thin ctypes binding of libmcs (include/mcs.h): argument marshalling only.
+
+Every step of the hot path runs in the CUDA kernels of ``csrc/``; this module never
+computes anything itself and has no CPU fallback: if ``libmcs.so`` is missing or no
+CUDA device is present, the calls fail loudly.
+
+Arrays may be numpy arrays or torch tensors (CPU or CUDA); the synchronous calls
+accept host or device memory (the library copies through unified addressing).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+import os
+import re
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libmcs.so")
+HEADER = os.path.join(os.path.dirname(_HERE), "include", "mcs.h")
+
+ABI_VERSION = 1
+MAX_NEIGHBORS = 4
+STATUS = {0: "MCS_OK", 1: "MCS_E_INVALID_ARG", 2: "MCS_E_OUT_OF_MEMORY", 3: "MCS_E_CUDA",
+          4: "MCS_E_NCCL", 5: "MCS_E_CAPACITY", 6: "MCS_E_STATE", 7: "MCS_E_DEGENERATE"}
+FLAG_LOOP, FLAG_UPDATED, FLAG_SINGULAR, FLAG_DEAD, FLAG_CLAMPED = 1, 2, 4, 8, 16
+
+
+class MCSError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class Config(C.Structure):
+    _fields_ = [
+        ("abi_version", C.c_uint32),
+        ("capacity_particles", C.c_int32),
+        ("capacity_keyframes", C.c_int32),
+        ("capacity_scan_points", C.c_int32),
+        ("neighbor_count", C.c_int32),
+        ("loop_recency_gap", C.c_int32),
+        ("voxel_resolution", C.c_float),
+        ("gn_slots", C.c_int32),
+        ("damping_rel", C.c_double),
+        ("step_clamp", C.c_double),
+        ("unmatched_penalty", C.c_double),
+        ("loglik_rel_floor", C.c_double),
+        ("posterior_floor", C.c_double),
+        ("device", C.c_int32),
+        ("rank", C.c_int32),
+        ("world_size", C.c_int32),
+        ("nccl_unique_id", C.c_void_p),
+    ]
+
+
+class UpdateOut(C.Structure):
+    _fields_ = [(n, C.c_void_p) for n in ("loglik", "grad6", "hess21", "psi6", "weight", "donor",
+                                          "flags", "representative", "n_dead")]
+
+
+_lib = None
+
+
+def load() -> C.CDLL:
+    """Load libmcs.so (never builds implicitly on the product path; see build.py)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} missing: run `python -m paper_2504_18056_b200.build` "
+                          "(no CPU fallback exists)")
+    L = C.CDLL(LIB_PATH)
+    vp, i32, u32, f64 = C.c_void_p, C.c_int32, C.c_uint32, C.c_double
+    st = C.c_int
+    sig = {
+        "mcs_config_default": (None, [vp]),
+        "mcs_create": (st, [vp, vp]),
+        "mcs_destroy": (st, [vp]),
+        "mcs_last_error": (C.c_char_p, [vp]),
+        "mcs_set_stream": (st, [vp, vp]),
+        "mcs_add_keyframe": (st, [vp, vp, vp, i32, f64, vp]),
+        "mcs_set_particles": (st, [vp, i32, vp, vp, vp]),
+        "mcs_get_particles": (st, [vp, vp, vp, vp, vp]),
+        "mcs_get_sizes": (st, [vp, vp, vp]),
+        "mcs_update": (st, [vp, vp, vp, i32, f64, u32, vp]),
+        "mcs_update_async": (st, [vp, vp, vp, i32, f64, u32, vp, vp]),
+        "mcs_eval": (st, [vp, vp, vp, i32, vp, vp, vp, vp, vp, vp]),
+        "mcs_resample": (st, [vp, vp, vp, i32, u32, vp]),
+        "mcs_snapshot": (st, [vp]),
+        "mcs_restore": (st, [vp]),
+        "mcs_state_bytes_per_particle": (C.c_size_t, [i32]),
+        "mcs_set_profiling": (st, [vp, i32]),
+        "mcs_get_phase_ms": (st, [vp, vp]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(L, name)
+        f.restype = res
+        f.argtypes = args
+    _lib = L
+    return L
+
+
+def header_symbols() -> list[str]:
+    """Every entry point include/mcs.h declares."""
+    txt = open(HEADER).read()
+    return sorted(set(re.findall(r"MCS_API\s+[\w\s\*]*?\b(mcs_\w+)\s*\(", txt)))
+
+
+def default_config(**kw) -> Config:
+    cfg = Config()
+    load().mcs_config_default(C.byref(cfg))
+    for k, v in kw.items():
+        if not hasattr(cfg, k):
+            raise TypeError(f"unknown config field {k}")
+        setattr(cfg, k, v)
+    return cfg
+
+
+def state_bytes_per_particle(n_keyframes: int) -> int:
+    return int(load().mcs_state_bytes_per_particle(int(n_keyframes)))
+
+
+# ------------------------------------------------------------------ marshalling
+def _ptr(a, dtype, shape_last=None):
+    """(pointer, keepalive) of a contiguous numpy array / torch tensor of the given dtype."""
+    if a is None:
+        return None, None
+    try:
+        import torch
+        if isinstance(a, torch.Tensor):
+            tdt = {np.float32: torch.float32, np.float64: torch.float64, np.int32: torch.int32,
+                   np.uint8: torch.uint8, np.int64: torch.int64}[dtype]
+            if a.dtype != tdt or not a.is_contiguous():
+                a = a.to(tdt).contiguous()
+            return a.data_ptr(), a
+    except ImportError:  # pragma: no cover
+        pass
+    arr = np.ascontiguousarray(a, dtype=dtype)
+    return arr.ctypes.data, arr
+
+
+class Context:
+    """One mcs_ctx: the device keyframe store + particle shard of one GPU."""
+
+    def __init__(self, capacity_particles: int, capacity_keyframes: int,
+                 capacity_scan_points: int, **cfg_kw):
+        self._lib = load()
+        self.cfg = default_config(capacity_particles=capacity_particles,
+                                  capacity_keyframes=capacity_keyframes,
+                                  capacity_scan_points=capacity_scan_points, **cfg_kw)
+        self._ctx = C.c_void_p()
+        st = self._lib.mcs_create(C.byref(self.cfg), C.byref(self._ctx))
+        if st:
+            raise MCSError(st, self._lib.mcs_last_error(None).decode())
+
+    # -------------------------------------------------------------- plumbing
+    def _check(self, st):
+        if st:
+            raise MCSError(st, self._lib.mcs_last_error(self._ctx).decode())
+
+    def close(self):
+        if getattr(self, "_ctx", None) and self._ctx.value:
+            self._lib.mcs_destroy(self._ctx)
+            self._ctx = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    @property
+    def sizes(self):
+        n, k = C.c_int32(), C.c_int32()
+        self._check(self._lib.mcs_get_sizes(self._ctx, C.byref(n), C.byref(k)))
+        return n.value, k.value
+
+    def set_stream(self, stream):
+        """stream: torch.cuda.Stream, raw cudaStream_t int, or None (library-owned)."""
+        h = getattr(stream, "cuda_stream", stream)
+        self._check(self._lib.mcs_set_stream(self._ctx, C.c_void_p(h) if h else None))
+
+    # -------------------------------------------------------------- state
+    def add_keyframe(self, mean3, cov6, path_length: float) -> int:
+        pm, km = _ptr(mean3, np.float32)
+        pc, kc = _ptr(cov6, np.float32)
+        n = int(np.prod(km.shape)) // 3
+        kid = C.c_int32()
+        self._check(self._lib.mcs_add_keyframe(self._ctx, pm, pc, n, float(path_length),
+                                               C.byref(kid)))
+        return kid.value
+
+    def set_particles(self, pose12, kf_pose12=None, cum_loglik=None):
+        pp, kp = _ptr(pose12, np.float32)
+        n = int(np.prod(kp.shape)) // 12
+        pk, kk = _ptr(kf_pose12, np.float32)
+        pl, kl = _ptr(cum_loglik, np.float64)
+        self._check(self._lib.mcs_set_particles(self._ctx, n, pp, pk, pl))
+
+    def get_particles(self):
+        n, K = self.sizes
+        pose = np.zeros((n, 12), np.float32)
+        kfp = np.zeros((n, K, 12), np.float32)
+        L = np.zeros(n, np.float64)
+        w = np.zeros(n, np.float64)
+        self._check(self._lib.mcs_get_particles(self._ctx, pose.ctypes.data, kfp.ctypes.data,
+                                                L.ctypes.data, w.ctypes.data))
+        return {"pose12": pose, "kf_pose12": kfp, "L": L, "weight": w}
+
+    def snapshot(self):
+        self._check(self._lib.mcs_snapshot(self._ctx))
+
+    def restore(self):
+        self._check(self._lib.mcs_restore(self._ctx))
+
+    # -------------------------------------------------------------- hot path
+    def update(self, scan_mean3, scan_cov6, D_now: float, U: int, outputs=None,
+               raise_degenerate=True):
+        """mcs_update; returns a dict of numpy outputs (host).  outputs: iterable of names
+        among loglik, grad6, hess21, psi6, weight, donor, flags (default all)."""
+        n, _ = self.sizes
+        names = ("loglik", "grad6", "hess21", "psi6", "weight", "donor", "flags") \
+            if outputs is None else tuple(outputs)
+        shapes = {"loglik": ((n,), np.float64), "grad6": ((n, 6), np.float32),
+                  "hess21": ((n, 21), np.float32), "psi6": ((n, 6), np.float32),
+                  "weight": ((n,), np.float64), "donor": ((n,), np.int32),
+                  "flags": ((n,), np.uint8)}
+        res = {k: np.zeros(*shapes[k]) for k in names}
+        rep = np.zeros(1, np.int32)
+        nd = np.zeros(1, np.int64)
+        uo = UpdateOut(**{k: (res[k].ctypes.data if k in res else None)
+                          for k in ("loglik", "grad6", "hess21", "psi6", "weight", "donor",
+                                    "flags")},
+                       representative=rep.ctypes.data, n_dead=nd.ctypes.data)
+        pm, km = _ptr(scan_mean3, np.float32)
+        pc, kc = _ptr(scan_cov6, np.float32)
+        S = int(np.prod(km.shape)) // 3
+        st = self._lib.mcs_update(self._ctx, pm, pc, S, float(D_now), int(U) & 0xFFFFFFFF,
+                                  C.byref(uo))
+        if st and (st != 7 or raise_degenerate):
+            self._check(st)
+        res["representative"] = int(rep[0])
+        res["n_dead"] = int(nd[0])
+        res["status"] = int(st)
+        return res
+
+    def update_async(self, d_scan_mean3, d_scan_cov6, D_now: float, U: int, out=None,
+                     stream=None):
+        """mcs_update_async with torch CUDA tensors; out: dict name -> CUDA tensor."""
+        out = out or {}
+        fields = {}
+        for k in ("loglik", "grad6", "hess21", "psi6", "weight", "donor", "flags",
+                  "representative", "n_dead"):
+            fields[k] = out[k].data_ptr() if k in out else None
+        uo = UpdateOut(**fields)
+        S = d_scan_mean3.numel() // 3
+        h = getattr(stream, "cuda_stream", stream)
+        self._check(self._lib.mcs_update_async(self._ctx, d_scan_mean3.data_ptr(),
+                                               d_scan_cov6.data_ptr(), S, float(D_now),
+                                               int(U) & 0xFFFFFFFF, C.byref(uo),
+                                               C.c_void_p(h) if h else None))
+
+    def eval(self, scan_mean3, scan_cov6):
+        """mcs_eval: per (particle, slot) l, H (body frame, upper 21), b, n, keyframe id."""
+        n, _ = self.sizes
+        nb = self.cfg.neighbor_count
+        out = {"slot_loglik": np.zeros((n, nb)), "slot_H21": np.zeros((n, nb, 21), np.float32),
+               "slot_b6": np.zeros((n, nb, 6), np.float32),
+               "slot_n": np.zeros((n, nb), np.int32), "slot_kf": np.zeros((n, nb), np.int32),
+               "loop": np.zeros(n, np.uint8)}
+        pm, km = _ptr(scan_mean3, np.float32)
+        pc, kc = _ptr(scan_cov6, np.float32)
+        S = int(np.prod(km.shape)) // 3
+        self._check(self._lib.mcs_eval(self._ctx, pm, pc, S, *[out[k].ctypes.data for k in (
+            "slot_loglik", "slot_H21", "slot_b6", "slot_n", "slot_kf", "loop")]))
+        return out
+
+    def resample(self, e, dead, U: int):
+        pe, ke = _ptr(e, np.float64)
+        pd, kd = _ptr(dead, np.uint8)
+        n = int(np.prod(ke.shape))
+        donor = np.zeros(n, np.int32)
+        self._check(self._lib.mcs_resample(self._ctx, pe, pd, n, int(U) & 0xFFFFFFFF,
+                                           donor.ctypes.data))
+        return donor
+
+    def set_profiling(self, on: bool = True):
+        self._check(self._lib.mcs_set_profiling(self._ctx, int(on)))
+
+    def phase_ms(self):
+        ms = (C.c_float * 5)()
+        self._check(self._lib.mcs_get_phase_ms(self._ctx, ms))
+        return {"select": ms[0], "sweep": ms[1], "update": ms[2], "weights": ms[3],
+                "total": ms[4]}
+
+
+def unpack_h21(h21):
+    """(..., 21) upper-triangle rows -> (..., 6, 6) symmetric."""
+    h21 = np.asarray(h21)
+    out = np.zeros(h21.shape[:-1] + (6, 6), h21.dtype)
+    k = 0
+    for r in range(6):
+        for c in range(r, 6):
+            out[..., r, c] = h21[..., k]
+            out[..., c, r] = h21[..., k]
+            k += 1
+    return out
+
+
+LN_1E16 = math.log(1e-16)
