@@ -5,6 +5,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <algorithm>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -164,16 +165,14 @@ static bool is_pow2_float(float r) {
 }
 
 static void free_all(mcs_ctx* c) {
-  for (auto& k : c->kf) {
-    cudaFree(k.keys);
-    cudaFree(k.payload);
-  }
+  for (auto& k : c->kf) cudaFree(k.slots);
   void* ptrs[] = {c->d_kf_meta, c->d_D,       c->d_pose,     c->d_kfpose,   c->d_L,
                   c->d_snapshot, c->d_scan_raw, c->d_scan,    c->d_items,    c->d_order,
                   c->d_part,    c->d_meta,    c->d_to,       c->d_l,        c->d_psi,
                   c->d_grad,    c->d_hess,    c->d_flags,    c->d_e,        c->d_w,
                   c->d_ladder,  c->d_ladder_scan, c->d_ncum, c->d_donor,    c->d_partials,
-                  c->d_ipartials, c->d_scal,  c->d_cub_temp};
+                  c->d_ipartials, c->d_scal,  c->d_cub_temp, c->d_skeys, c->d_skeys_out,
+                  c->d_sids,    c->d_stage,   c->d_bad};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->h_scal) cudaFreeHost(c->h_scal);
@@ -181,6 +180,18 @@ static void free_all(mcs_ctx* c) {
     if (e) cudaEventDestroy(e);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
 }
+
+// output staging layout of the synchronous mcs_update (per-particle rows, 256-B aligned)
+struct StageLayout {
+  size_t l, g, h, p, w, d, f, total;
+  explicit StageLayout(size_t N) {
+    size_t off = 0;
+    auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 255) & ~size_t(255); return o; };
+    l = take(8 * N); g = take(24 * N); h = take(84 * N); p = take(24 * N);
+    w = take(8 * N); d = take(4 * N); f = take(N);
+    total = off;
+  }
+};
 
 // copy n bytes from a host-or-device pointer into device memory, stream-ordered
 static cudaError_t to_device(void* dst, const void* src, size_t bytes, cudaStream_t st) {
@@ -277,6 +288,21 @@ mcs_status mcs_create(const mcs_config* cfg, mcs_ctx** out) {
   if (e == cudaSuccess) e = dalloc(&c->d_scan, 3 * S);
   if (e == cudaSuccess) e = dalloc(&c->d_items, 4 * nb * N);
   if (e == cudaSuccess) e = dalloc(&c->d_order, nb * N);
+  if (e == cudaSuccess) e = dalloc(&c->d_skeys, nb * N);
+  if (e == cudaSuccess) e = dalloc(&c->d_skeys_out, nb * N);
+  if (e == cudaSuccess) e = dalloc(&c->d_sids, nb * N);
+  if (e == cudaSuccess) e = dalloc(&c->d_bad, 1);
+  if (e == cudaSuccess) {
+    c->stage_bytes = StageLayout(N).total;
+    e = dalloc(&c->d_stage, c->stage_bytes);
+  }
+  if (e == cudaSuccess) {  // keep stream-ordered allocations mapped between calls
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, c->dev) == cudaSuccess) {
+      uint64_t thr = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  }
   if (e == cudaSuccess) e = dalloc(&c->d_part, (size_t)kSlotFloats * nb * N);
   if (e == cudaSuccess) e = dalloc(&c->d_meta, N);
   if (e == cudaSuccess) e = dalloc(&c->d_to, N);
@@ -297,7 +323,7 @@ mcs_status mcs_create(const mcs_config* cfg, mcs_ctx** out) {
   if (e == cudaSuccess) e = cudaMemset(c->d_scal, 0, sizeof(Scalars));
   if (e == cudaSuccess) e = cudaMallocHost((void**)&c->h_scal, sizeof(Scalars));
   if (e == cudaSuccess) {
-    c->cub_temp_bytes = cub_temp_needed((int)N);
+    c->cub_temp_bytes = std::max(cub_temp_needed((int)N), sort_temp_needed((int)(nb * N), (int)K));
     e = cudaMalloc(&c->d_cub_temp, c->cub_temp_bytes ? c->cub_temp_bytes : 1);
   }
   for (int k = 0; k < 6 && e == cudaSuccess; ++k) e = cudaEventCreate(&c->ev[k]);
@@ -368,22 +394,22 @@ mcs_status mcs_add_keyframe(mcs_ctx* ctx, const float* mean3, const float* cov6,
     FAIL(ctx, MCS_E_INVALID_ARG, "%d keyframe points non-finite or covariance not SPD", h_bad);
   }
   KfHost kh;
-  int bad_cell = 0;
-  cudaError_t e = kf_build(ctx, dm, dc, n, kh, &bad_cell);
+  int bad_cell = 0, bad_extent = 0;
+  cudaError_t e = kf_build(ctx, dm, dc, n, kh, &bad_cell, &bad_extent);
   cudaFreeAsync(dm, st);
   cudaFreeAsync(dc, st);
   cudaFreeAsync(bad, st);
   CUDA_TRY(ctx, e);
   if (bad_cell)
     FAIL(ctx, MCS_E_INVALID_ARG, "%d keyframe points outside the 21-bit cell range", bad_cell);
+  if (bad_extent) {
+    if (kh.slots) cudaFree(kh.slots);
+    FAIL(ctx, MCS_E_INVALID_ARG,
+         "keyframe occupied extent exceeds 2047 x 2048 x 1024 cells at r = %g m",
+         (double)ctx->cfg.voxel_resolution);
+  }
   const int k = ctx->K;
-  KfMeta m;
-  m.keys = kh.keys;
-  m.payload = kh.payload;
-  int lg = 0;
-  while ((1 << lg) < kh.cap) ++lg;
-  m.shift = (uint32_t)(64 - lg);
-  m.mask = (uint32_t)(kh.cap - 1);
+  const KfMeta m = kh.meta;
   CUDA_TRY(ctx, cudaMemcpyAsync(ctx->d_kf_meta + k, &m, sizeof(m), cudaMemcpyHostToDevice, st));
   CUDA_TRY(ctx, cudaMemcpyAsync(ctx->d_D + k, &path_length, sizeof(double), cudaMemcpyHostToDevice,
                                 st));
@@ -498,16 +524,14 @@ mcs_status mcs_get_particles(mcs_ctx* ctx, float* pose12, float* kf_pose12, doub
 
 // validate a scan already in device memory (d_scan_raw layout: mean3 then cov6)
 static mcs_status validate_scan(mcs_ctx* ctx, int n_pts) {
-  int* bad = nullptr;
   cudaStream_t st = ctx->stream;
-  CUDA_TRY(ctx, cudaMallocAsync(&bad, sizeof(int), st));
-  CUDA_TRY(ctx, cudaMemsetAsync(bad, 0, sizeof(int), st));
+  CUDA_TRY(ctx, cudaMemsetAsync(ctx->d_bad, 0, sizeof(int), st));
   validate_gauss_kernel<<<(n_pts + 255) / 256, 256, 0, st>>>(
-      ctx->d_scan_raw, ctx->d_scan_raw + 3 * (size_t)ctx->capS, n_pts, bad);
-  int h_bad = 0;
-  CUDA_TRY(ctx, cudaMemcpyAsync(&h_bad, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
-  cudaFreeAsync(bad, st);
+      ctx->d_scan_raw, ctx->d_scan_raw + 3 * (size_t)ctx->capS, n_pts, ctx->d_bad);
+  CUDA_TRY(ctx, cudaMemcpyAsync(&ctx->h_scal->status, ctx->d_bad, sizeof(int),
+                                cudaMemcpyDeviceToHost, st));
   CUDA_TRY(ctx, cudaStreamSynchronize(st));
+  const int h_bad = ctx->h_scal->status;
   if (h_bad) FAIL(ctx, MCS_E_INVALID_ARG, "%d scan points non-finite or covariance not SPD", h_bad);
   return MCS_OK;
 }
@@ -561,19 +585,15 @@ mcs_status mcs_update(mcs_ctx* ctx, const float* scan_mean3, const float* scan_c
   if (out) {
     // gather per-particle rows into a device staging area, then one copy per output
     OutPtrs o{};
-    size_t off = 0;
-    auto take = [&](size_t bytes) { size_t p = off; off += (bytes + 255) & ~size_t(255); return p; };
-    const size_t o_l = take(8 * N), o_g = take(24 * N), o_h = take(84 * N), o_p = take(24 * N),
-                 o_w = take(8 * N), o_d = take(4 * N), o_f = take(N);
-    char* stage = nullptr;
-    CUDA_TRY(ctx, cudaMallocAsync((void**)&stage, off, st));
-    if (out->loglik) o.loglik = (double*)(stage + o_l);
-    if (out->grad6) o.grad6 = (float*)(stage + o_g);
-    if (out->hess21) o.hess21 = (float*)(stage + o_h);
-    if (out->psi6) o.psi6 = (float*)(stage + o_p);
-    if (out->weight) o.weight = (double*)(stage + o_w);
-    if (out->donor) o.donor = (int32_t*)(stage + o_d);
-    if (out->flags) o.flags = (uint8_t*)(stage + o_f);
+    const StageLayout lay(N);
+    char* stage = ctx->d_stage;
+    if (out->loglik) o.loglik = (double*)(stage + lay.l);
+    if (out->grad6) o.grad6 = (float*)(stage + lay.g);
+    if (out->hess21) o.hess21 = (float*)(stage + lay.h);
+    if (out->psi6) o.psi6 = (float*)(stage + lay.p);
+    if (out->weight) o.weight = (double*)(stage + lay.w);
+    if (out->donor) o.donor = (int32_t*)(stage + lay.d);
+    if (out->flags) o.flags = (uint8_t*)(stage + lay.f);
     gather_outputs_kernel<<<(N + 255) / 256, 256, 0, st>>>(
         o, N, ctx->capN, ctx->d_l, ctx->d_grad, ctx->d_hess, ctx->d_psi, ctx->d_w, ctx->d_donor,
         ctx->d_flags, ctx->d_scal, 0);
@@ -584,7 +604,6 @@ mcs_status mcs_update(mcs_ctx* ctx, const float* scan_mean3, const float* scan_c
     if (out->weight) CUDA_TRY(ctx, cudaMemcpyAsync(out->weight, o.weight, 8 * N, cudaMemcpyDefault, st));
     if (out->donor) CUDA_TRY(ctx, cudaMemcpyAsync(out->donor, o.donor, 4 * N, cudaMemcpyDefault, st));
     if (out->flags) CUDA_TRY(ctx, cudaMemcpyAsync(out->flags, o.flags, N, cudaMemcpyDefault, st));
-    cudaFreeAsync(stage, st);
   }
   CUDA_TRY(ctx, cudaMemcpyAsync(ctx->h_scal, ctx->d_scal, sizeof(Scalars), cudaMemcpyDeviceToHost,
                                 st));

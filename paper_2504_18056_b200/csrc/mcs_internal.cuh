@@ -19,18 +19,27 @@
 
 namespace mcs {
 
-constexpr unsigned long long kEmptyKey = ~0ull;  // bit 63 set: never a packed cell key
 constexpr int kCellMin = -1048576;               // 21-bit signed cell coordinates (R27)
 constexpr int kCellMax = 1048575;
-constexpr unsigned long long kHashMul = 0x9E3779B97F4A7C15ull;
 constexpr int kSlotFloats = 32;                   // sweep partial record per (particle, slot)
 constexpr int kMaxNb = MCS_MAX_NEIGHBORS;
 
+// Per-keyframe open-addressing table in the keyframe's own cell grid.  Keys are 32-bit
+// bbox-local cell coordinates (dx << 21 | dy << 10 | dz), so a query outside the keyframe's
+// occupied bounding box is a miss without a probe, and a probe is one 64-byte slot:
+//   float4 {mu'x, mu'y, mu'z, key}  {S'xx, S'xy, S'xz, S'yy}  {S'yz, S'zz, count, 0}  {0,0,0,0}
+// (the key shares the first 16 bytes with the mean, so the first-probe payload loads are
+// issued together with the key).  Load factor <= 1/4.
+constexpr unsigned int kEmptyKey32 = 0xFFFFFFFFu;  // dx = 2047 never occurs (ex <= 2047)
+constexpr int kMaxEx = 2047, kMaxEy = 2048, kMaxEz = 1024;
+constexpr unsigned int kHashMul32 = 0x9E3779B1u;
+
 struct KfMeta {                 // one per keyframe (device array, read through L1)
-  const unsigned long long* keys;
-  const float4* payload;        // [cap][3]: {mu'x,mu'y,mu'z,S'xx} {S'xy,S'xz,S'yy,S'yz} {S'zz,cnt,0,0}
-  uint32_t shift;               // 64 - log2(cap)
-  uint32_t mask;                // cap - 1
+  const float4* slots;          // [cap][4]
+  int ox, oy, oz;               // bbox origin (cell coordinates)
+  unsigned int ex, ey, ez;      // bbox extents (cells)
+  unsigned int shift;           // 32 - log2(cap)
+  unsigned int mask;            // cap - 1
 };
 
 __host__ __device__ inline unsigned long long pack_cell(int x, int y, int z) {
@@ -38,10 +47,19 @@ __host__ __device__ inline unsigned long long pack_cell(int x, int y, int z) {
          (unsigned long long)(z & 0x1FFFFF);
 }
 
+__host__ __device__ inline unsigned int local_key(unsigned int dx, unsigned int dy,
+                                                  unsigned int dz) {
+  return (dx << 21) | (dy << 10) | dz;
+}
+
+__host__ __device__ inline unsigned int slot_hash(unsigned int key, unsigned int shift) {
+  return (key * kHashMul32) >> shift;
+}
+
 struct KfHost {
-  unsigned long long* keys = nullptr;
-  float4* payload = nullptr;
+  float4* slots = nullptr;
   int32_t cap = 0, n_cells = 0, n_points = 0;
+  KfMeta meta{};
 };
 
 struct Scalars {                // device-side reduction results of one update
@@ -89,7 +107,10 @@ struct mcs_ctx {
   float* d_scan_raw = nullptr;  // [Scap][9]
   float4* d_scan = nullptr;     // [Scap][3]
   float4* d_items = nullptr;    // [nb*Ncap][4]
-  int32_t* d_order = nullptr;   // [nb*Ncap] sweep order (item ids)
+  int32_t* d_order = nullptr;   // [nb*Ncap] sweep order (item ids, coherence-sorted)
+  unsigned long long* d_skeys = nullptr;      // [nb*Ncap] coherence keys (a1)
+  unsigned long long* d_skeys_out = nullptr;  // [nb*Ncap]
+  int32_t* d_sids = nullptr;                  // [nb*Ncap] item ids before sorting
   float* d_part = nullptr;      // [nb*Ncap][32]
   uint8_t* d_meta = nullptr;    // [Ncap] bit0 loop
   int32_t* d_to = nullptr;      // [Ncap] oldest neighbour keyframe t_o
@@ -108,6 +129,9 @@ struct mcs_ctx {
   int32_t* d_ipartials = nullptr;
   mcs::Scalars* d_scal = nullptr;
   mcs::Scalars* h_scal = nullptr;  // pinned
+  char* d_stage = nullptr;      // output staging for synchronous calls
+  size_t stage_bytes = 0;
+  int* d_bad = nullptr;         // validation counter
   void* d_cub_temp = nullptr;
   size_t cub_temp_bytes = 0;
   int32_t capN = 0, capK = 0, capS = 0, nbcap = 0;
@@ -116,9 +140,11 @@ struct mcs_ctx {
 namespace mcs {
 
 // ---- launchers (all stream-ordered on ctx->stream) ----
-// a0: build keyframe k's table from device mean3/cov6 (n points).  Returns cudaError.
+// a0: build keyframe k's table from device mean3/cov6 (n points).  Returns cudaError;
+// *bad_cell = number of points outside the 21-bit range, *bad_extent = 1 if the occupied
+// bounding box exceeds 2047 x 2048 x 1024 cells.
 cudaError_t kf_build(mcs_ctx* c, const float* d_mean3, const float* d_cov6, int n, KfHost& out,
-                     int* bad_cell);
+                     int* bad_cell, int* bad_extent);
 // pack raw [S][3] + [S][6] into the sweep's float4 x3 layout
 void launch_pack_scan(const float* mean3, const float* cov6, int S, float4* out,
                       cudaStream_t st);
@@ -137,5 +163,6 @@ void launch_weights_resample(mcs_ctx* c, uint32_t U);
 void launch_resample_only(mcs_ctx* c, const double* d_e, const uint8_t* d_dead, int n,
                           uint32_t U, int32_t* d_donor);
 size_t cub_temp_needed(int n);
+size_t sort_temp_needed(int n, int capK);
 
 }  // namespace mcs

@@ -10,14 +10,45 @@
 // Writes one 64-byte work item per (particle, slot) for the sweep:
 //   float4 rows {R00 R01 R02 tx}{R10 R11 R12 ty}{R20 R21 R22 tz}, int4 {kf, particle, flags, 0}
 //   flags bit0: accumulate H~, b~ (slot in G, R4).
+#include <cub/cub.cuh>
+
 #include "mcs_internal.cuh"
 
 namespace mcs {
 
+// Lane-coherence sort key of a work item: the keyframe id in the top bits, then
+// a 6-D Morton code of where the item's relative pose sends two reference points 8 m out on
+// the x and y axes, at 1/16 m steps (6 bits per coordinate, wrapping every 4 m).  Items that
+// are adjacent in this order probe the same cells for the same scan point, so a warp's
+// gathers coalesce and its hit/miss branches agree.
+constexpr int kMortonBitsPerDim = 6;
+constexpr int kMortonBits = 6 * kMortonBitsPerDim;
+
+__device__ __forceinline__ unsigned long long coherence_key(int kf, const float* rel) {
+  const float d = 8.0f;
+  float q[6];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    q[a] = d * rel[4 * a + 0] + rel[4 * a + 3];
+    q[3 + a] = d * rel[4 * a + 1] + rel[4 * a + 3];
+  }
+  unsigned int c[6];
+#pragma unroll
+  for (int k = 0; k < 6; ++k) c[k] = (unsigned int)__float2int_rd(q[k] * 16.0f) & 63u;
+  unsigned long long m = 0ull;
+#pragma unroll
+  for (int b = kMortonBitsPerDim - 1; b >= 0; --b)
+#pragma unroll
+    for (int k = 0; k < 6; ++k) m = (m << 1) | ((c[k] >> b) & 1u);
+  return ((unsigned long long)kf << kMortonBits) | m;
+}
+
 __global__ void select_kernel(const float* __restrict__ pose, int capN, int N,
                               const float* __restrict__ kfpose, int capK, int K, int nb_max,
                               int gap, int gn_all, int eval_mode, float4* __restrict__ items,
-                              uint8_t* __restrict__ meta, int32_t* __restrict__ t_o_out) {
+                              uint8_t* __restrict__ meta, int32_t* __restrict__ t_o_out,
+                              unsigned long long* __restrict__ skeys, int32_t* __restrict__ sids,
+                              unsigned long long inactive_key) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= N) return;
   float Tt[12];
@@ -57,6 +88,8 @@ __global__ void select_kernel(const float* __restrict__ pose, int capN, int N,
   for (int s = 0; s < nb_max; ++s) {
     float4* it = items + 4 * ((size_t)s * capN + i);
     const int k = s < nb ? bk[s] : -1;
+    skeys[(size_t)s * N + i] = inactive_key;
+    sids[(size_t)s * N + i] = s * capN + i;
     if (k < 0) {
       it[3] = make_float4(__int_as_float(-1), __int_as_float(i), __int_as_float(0), 0.f);
       continue;
@@ -85,23 +118,36 @@ __global__ void select_kernel(const float* __restrict__ pose, int capN, int N,
     it[1] = make_float4(rel[4], rel[5], rel[6], rel[7]);
     it[2] = make_float4(rel[8], rel[9], rel[10], rel[11]);
     it[3] = make_float4(__int_as_float(k), __int_as_float(i), __int_as_float(flags), 0.f);
+    skeys[(size_t)s * N + i] = coherence_key(k, rel);
   }
 }
 
-__global__ void iota_kernel(int32_t* __restrict__ order, int nb, int capN, int N) {
-  int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= nb * N) return;
-  int s = t / N, i = t - s * N;
-  order[t] = s * capN + i;
+static int sort_end_bit(int capK) {
+  int b = 1;
+  while ((1 << b) <= capK) ++b;  // room for kf in [0, capK] (capK = inactive)
+  return kMortonBits + b;
+}
+
+size_t sort_temp_needed(int n, int capK) {
+  size_t b = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, b, (unsigned long long*)nullptr,
+                                  (unsigned long long*)nullptr, (int32_t*)nullptr,
+                                  (int32_t*)nullptr, n, 0, sort_end_bit(capK));
+  return b;
 }
 
 void launch_select(mcs_ctx* c, bool eval_mode) {
   const int N = c->N;
   const int nb_max = c->cfg.neighbor_count;
+  const int end_bit = sort_end_bit(c->capK);
+  const unsigned long long inactive = (end_bit >= 64) ? ~0ull : ((1ull << end_bit) - 1ull);
   select_kernel<<<(N + 127) / 128, 128, 0, c->stream>>>(
       c->d_pose, c->capN, N, c->d_kfpose, c->capK, c->K, nb_max, c->cfg.loop_recency_gap,
-      c->cfg.gn_slots == MCS_GN_ALL_SLOTS, eval_mode ? 1 : 0, c->d_items, c->d_meta, c->d_to);
-  iota_kernel<<<(nb_max * N + 255) / 256, 256, 0, c->stream>>>(c->d_order, nb_max, c->capN, N);
+      c->cfg.gn_slots == MCS_GN_ALL_SLOTS, eval_mode ? 1 : 0, c->d_items, c->d_meta, c->d_to,
+      c->d_skeys, c->d_sids, inactive);
+  size_t tb = c->cub_temp_bytes;
+  cub::DeviceRadixSort::SortPairs(c->d_cub_temp, tb, c->d_skeys, c->d_skeys_out, c->d_sids,
+                                  c->d_order, nb_max * N, 0, end_bit, c->stream);
 }
 
 }  // namespace mcs
