@@ -1,0 +1,60 @@
+"""Experiment harness: build libmcs variants (-D knobs) and time the C2 update phases of each.
+    python bench/sweep_variants.py build   (here)    /  python bench/sweep_variants.py run (GPU)
+"""
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+VARIANTS = {
+    "base": [],
+    "depth2": ["MCS_EXP_DEPTH2"],
+    "magic": ["MCS_EXP_MAGICFLOOR"],
+    "depth2_magic": ["MCS_EXP_DEPTH2", "MCS_EXP_MAGICFLOOR"],
+    "depth2_magic_t64": ["MCS_EXP_DEPTH2", "MCS_EXP_MAGICFLOOR", "MCS_SWEEP_THREADS=64"],
+    "nomath_magic": ["MCS_EXP_NOMATH", "MCS_EXP_MAGICFLOOR"],
+}
+OUT = os.path.join(ROOT, "bench", "_variants")
+
+
+def build():
+    from paper_2504_18056_b200 import build as b
+    for name, d in VARIANTS.items():
+        b.build(defines=d, lib=os.path.join(OUT, f"libmcs_{name}.so"),
+                build_dir=os.path.join(OUT, name))
+        print("built", name)
+
+
+def run_one(name):
+    import numpy as np
+    import paper_2504_18056_b200 as mcs
+    import synth
+    s = synth.c2()
+    ctx = mcs.Context(s.N, s.K, s.S, loop_recency_gap=s.gap, voxel_resolution=s.r)
+    for (m3, c6), d in zip(s.keyframes, s.D):
+        ctx.add_keyframe(m3, c6, d)
+    ctx.set_particles(s.pose12, s.kf_pose12)
+    ctx.snapshot()
+    ctx.set_profiling(True)
+    sw = []
+    for k in range(8):
+        ctx.restore()
+        ctx.update(s.scan_mean3, s.scan_cov6, s.D_now, s.U, outputs=("loglik",))
+        if k >= 3:
+            sw.append(ctx.phase_ms()["sweep"])
+    return float(np.median(sw))
+
+
+if __name__ == "__main__":
+    if sys.argv[1] == "build":
+        build()
+    elif sys.argv[1] == "one":
+        print(json.dumps({"variant": sys.argv[2], "sweep_ms": run_one(sys.argv[2])}))
+    else:
+        for name in VARIANTS:
+            env = dict(os.environ, MCS_LIB=os.path.join(OUT, f"libmcs_{name}.so"))
+            r = subprocess.run([sys.executable, __file__, "one", name], env=env,
+                               capture_output=True, text=True)
+            print(r.stdout.strip() or r.stderr[-500:], flush=True)

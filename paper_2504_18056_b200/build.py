@@ -39,7 +39,21 @@ def _stale(target: str, deps: list[str]) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, defines=(), lib: str | None = None,
+          build_dir: str | None = None) -> str:
+    """Compile every csrc/*.cu for sm_100a and link libmcs.so (or `lib` for experiment
+    variants built with extra -D `defines` into `build_dir`)."""
+    global BUILD, LIB
+    saved = (BUILD, LIB)
+    if lib:
+        LIB, BUILD = lib, build_dir or (lib + ".build")
+    try:
+        return _build(force, verbose, list(defines))
+    finally:
+        BUILD, LIB = saved
+
+
+def _build(force: bool, verbose: bool, defines: list[str]) -> str:
     os.makedirs(BUILD, exist_ok=True)
     hdrs = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(ROOT, "include", "mcs.h"),
                                                         os.path.abspath(__file__)]
@@ -50,7 +64,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         obj = os.path.join(BUILD, s.replace(".cu", ".o"))
         objs.append(obj)
         if force or _stale(obj, [src] + hdrs):
-            cmd = [nvcc(), *NVCC_FLAGS, "-c", src, "-o", obj]
+            cmd = [nvcc(), *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-c", src, "-o", obj]
             if verbose:
                 cmd.insert(1, "-Xptxas=-v")
             jobs.append(cmd)

@@ -578,7 +578,7 @@ mcs_status mcs_update(mcs_ctx* ctx, const float* scan_mean3, const float* scan_c
   CUDA_TRY(ctx, to_device(raw_c, scan_cov6, sizeof(float) * 6 * n_pts, st));
   s = validate_scan(ctx, n_pts);
   if (s != MCS_OK) return s;
-  launch_pack_scan(raw_m, raw_c, n_pts, ctx->d_scan, st);
+  launch_prepare_scan(raw_m, raw_c, n_pts, ctx->d_scan, st);
   run_update(ctx, n_pts, D_now, resample_u);
   CUDA_TRY(ctx, cudaGetLastError());
   const int N = ctx->N;
@@ -623,7 +623,7 @@ mcs_status mcs_update_async(mcs_ctx* ctx, const float* d_scan_mean3, const float
   if (s != MCS_OK) return s;
   cudaStream_t saved = ctx->stream;
   if (cuda_stream) ctx->stream = (cudaStream_t)cuda_stream;
-  launch_pack_scan(d_scan_mean3, d_scan_cov6, n_pts, ctx->d_scan, ctx->stream);
+  launch_prepare_scan(d_scan_mean3, d_scan_cov6, n_pts, ctx->d_scan, ctx->stream);
   run_update(ctx, n_pts, D_now, resample_u);
   if (d_out) {
     OutPtrs o{d_out->loglik, d_out->grad6,  d_out->hess21,         d_out->psi6,  d_out->weight,
@@ -651,7 +651,7 @@ mcs_status mcs_eval(mcs_ctx* ctx, const float* scan_mean3, const float* scan_cov
   CUDA_TRY(ctx, to_device(raw_c, scan_cov6, sizeof(float) * 6 * n_pts, st));
   s = validate_scan(ctx, n_pts);
   if (s != MCS_OK) return s;
-  launch_pack_scan(raw_m, raw_c, n_pts, ctx->d_scan, st);
+  launch_prepare_scan(raw_m, raw_c, n_pts, ctx->d_scan, st);
   const size_t NS = (size_t)ctx->N * ctx->cfg.neighbor_count;
   double* dl = nullptr;
   float *dH = nullptr, *db = nullptr;

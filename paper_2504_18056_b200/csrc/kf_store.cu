@@ -183,20 +183,4 @@ cleanup:
   return e;
 }
 
-__global__ void pack_scan_kernel(const float* __restrict__ mean3, const float* __restrict__ cov6,
-                                 int S, float4* __restrict__ out) {
-  int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= S) return;
-  const float* m = mean3 + 3 * j;
-  const float* c = cov6 + 6 * j;
-  out[3 * j + 0] = make_float4(m[0], m[1], m[2], c[0]);
-  out[3 * j + 1] = make_float4(c[1], c[2], c[3], c[4]);
-  out[3 * j + 2] = make_float4(c[5], 0.f, 0.f, 0.f);
-}
-
-void launch_pack_scan(const float* mean3, const float* cov6, int S, float4* out,
-                      cudaStream_t st) {
-  pack_scan_kernel<<<(S + 255) / 256, 256, 0, st>>>(mean3, cov6, S, out);
-}
-
 }  // namespace mcs

@@ -145,9 +145,10 @@ namespace mcs {
 // bounding box exceeds 2047 x 2048 x 1024 cells.
 cudaError_t kf_build(mcs_ctx* c, const float* d_mean3, const float* d_cov6, int n, KfHost& out,
                      int* bad_cell, int* bad_extent);
-// pack raw [S][3] + [S][6] into the sweep's float4 x3 layout
-void launch_pack_scan(const float* mean3, const float* cov6, int S, float4* out,
-                      cudaStream_t st);
+// raw [S][3] + [S][6] -> the sweep's float4 x3 layout {mu, lambda3} {u, 0} {v, 0}
+// (spectral form Sigma = lambda3 I + u u^T + v v^T, fp64 Jacobi)
+void launch_prepare_scan(const float* mean3, const float* cov6, int S, float4* out,
+                         cudaStream_t st);
 // a1
 void launch_select(mcs_ctx* c, bool eval_mode);
 // a2

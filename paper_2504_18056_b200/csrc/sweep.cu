@@ -14,18 +14,28 @@
 // (R2), so the per-slot rotation back to the body frame happens once in a3, not per point.
 // The table probe of point j+1 (key + payload, one 48-byte slot) is issued before the math of
 // point j, so the L2 gather latency hides behind ~140 FP32 instructions.
+// R Sigma_j R^T uses the per-scan spectral form of Sigma_j (prepare_scan_kernel below).
 // Accumulators are fp32 registers in a fixed point order: bitwise reproducible.
 #include "mcs_internal.cuh"
 
 namespace mcs {
 
-constexpr int kSweepThreads = 128;
-constexpr int kChunk = 256;  // scan points per shared-memory stage (12 KB)
+#ifndef MCS_SWEEP_THREADS
+#define MCS_SWEEP_THREADS 128
+#endif
+#ifndef MCS_SWEEP_CHUNK
+#define MCS_SWEEP_CHUNK 256
+#endif
+#ifndef MCS_SWEEP_MINBLOCKS
+#define MCS_SWEEP_MINBLOCKS 1
+#endif
+constexpr int kSweepThreads = MCS_SWEEP_THREADS;
+constexpr int kChunk = MCS_SWEEP_CHUNK;  // scan points per shared-memory stage (48 B each)
 
 struct Probe {
-  float4 s0, s1, s2;   // slot payload (first probe position, speculatively loaded)
+  float4 s0, s1, s2;   // slot payload at the first probe position (speculatively loaded)
   float qx, qy, qz;    // pinned fp32 transform of the point
-  unsigned int key;    // bbox-local key; kEmptyKey32 = out of the keyframe bbox
+  unsigned int key;    // bbox-local key; kEmptyKey32 = outside the keyframe bbox
   unsigned int h;      // slot index of the first probe
 };
 
@@ -35,7 +45,11 @@ __device__ __forceinline__ float rcp_approx(float x) {
   return r;
 }
 
-__global__ void __launch_bounds__(kSweepThreads)
+// floor(x) as the bits of x + 1.5*2^23 rounded toward -inf: exact for |x| < 2^22, and every
+// other finite x maps far outside any keyframe bbox after the offset.
+constexpr float kMagic = 12582912.0f;
+
+__global__ void __launch_bounds__(kSweepThreads, MCS_SWEEP_MINBLOCKS)
     sweep_kernel(const float4* __restrict__ items, const int32_t* __restrict__ order,
                  int n_items, const float4* __restrict__ scan, int S,
                  const KfMeta* __restrict__ kmeta, float inv_r, float* __restrict__ part) {
@@ -62,33 +76,35 @@ __global__ void __launch_bounds__(kSweepThreads)
     m.shift = 31;
     m.mask = 0;
   }
+  const unsigned int offx = (unsigned)__float_as_int(kMagic) + (unsigned)m.ox;
+  const unsigned int offy = (unsigned)__float_as_int(kMagic) + (unsigned)m.oy;
+  const unsigned int offz = (unsigned)__float_as_int(kMagic) + (unsigned)m.oz;
   const float R00 = r0.x, R01 = r0.y, R02 = r0.z, tx = r0.w;
   const float R10 = r1.x, R11 = r1.y, R12 = r1.z, ty = r1.w;
   const float R20 = r2.x, R21 = r2.y, R22 = r2.z, tz = r2.w;
 
-  // issue the first probe of point j (no wait on the loads)
+  // transform, cell, key and the (unconditional) first-probe loads of point j
   auto issue = [&](int j) {
     Probe p;
     const float4 A = s_pt[3 * j];
     p.qx = __fmaf_rn(R02, A.z, __fmaf_rn(R01, A.y, __fmaf_rn(R00, A.x, tx)));
     p.qy = __fmaf_rn(R12, A.z, __fmaf_rn(R11, A.y, __fmaf_rn(R10, A.x, ty)));
     p.qz = __fmaf_rn(R22, A.z, __fmaf_rn(R21, A.y, __fmaf_rn(R20, A.x, tz)));
-    // floor(q / r) (pinned: exact power-of-two scaling, R27), then bbox-local coordinates
-    const unsigned int dx = (unsigned)(__float2int_rd(__fmul_rn(p.qx, inv_r)) - m.ox);
-    const unsigned int dy = (unsigned)(__float2int_rd(__fmul_rn(p.qy, inv_r)) - m.oy);
-    const unsigned int dz = (unsigned)(__float2int_rd(__fmul_rn(p.qz, inv_r)) - m.oz);
+    // floor(q / r) (exact power-of-two scaling, R27) -> bbox-local cell coordinates
+    const unsigned int dx =
+        (unsigned)__float_as_int(__fadd_rd(__fmul_rn(p.qx, inv_r), kMagic)) - offx;
+    const unsigned int dy =
+        (unsigned)__float_as_int(__fadd_rd(__fmul_rn(p.qy, inv_r), kMagic)) - offy;
+    const unsigned int dz =
+        (unsigned)__float_as_int(__fadd_rd(__fmul_rn(p.qz, inv_r), kMagic)) - offz;
     const bool in = (dx < m.ex) & (dy < m.ey) & (dz < m.ez);
     p.key = in ? local_key(dx, dy, dz) : kEmptyKey32;
     p.h = slot_hash(p.key, m.shift) & m.mask;
-    if (in) {
-      const float4* s = m.slots + 4 * (size_t)p.h;
-      p.s0 = __ldg(s);
-      p.s1 = __ldg(s + 1);
-      p.s2 = __ldg(s + 2);
-    } else {
-      p.s0 = make_float4(0.f, 0.f, 0.f, __uint_as_float(kEmptyKey32));
-      p.s1 = p.s0;
-      p.s2 = p.s0;
+    const float4* sl = m.slots + 4 * (size_t)p.h;
+    if (active) {
+      p.s0 = __ldg(sl);
+      p.s1 = __ldg(sl + 1);
+      p.s2 = __ldg(sl + 2);
     }
     return p;
   };
@@ -102,12 +118,11 @@ __global__ void __launch_bounds__(kSweepThreads)
 #pragma unroll
   for (int k = 0; k < 6; ++k) bv[k] = 0.f;
 
-  // resolve a probe: first-probe hit, empty slot (miss), or continue linear probing
+  // first-probe hit, or an empty slot / out-of-bbox point (miss), else keep probing
   auto resolve = [&](Probe& p) -> bool {
-    if (p.key == kEmptyKey32) return false;
     const unsigned int k0 = __float_as_uint(p.s0.w);
-    if (k0 == p.key) return true;
-    if (k0 == kEmptyKey32) return false;
+    if (k0 == p.key) return p.key != kEmptyKey32;
+    if (k0 == kEmptyKey32 || p.key == kEmptyKey32) return false;
     unsigned int hh = p.h;
     while (true) {
       hh = (hh + 1) & m.mask;
@@ -126,30 +141,26 @@ __global__ void __launch_bounds__(kSweepThreads)
 
   // Eqs.3-4 and Eq.6 for one matched (item, point)
   auto accumulate = [&](int j, const Probe& p) {
-    const float4 A = s_pt[3 * j];
-    const float4 B = s_pt[3 * j + 1];
-    const float4 Cc = s_pt[3 * j + 2];
+    const float4 A = s_pt[3 * j];      // {mu, lambda3}
+    const float4 U = s_pt[3 * j + 1];  // {u, 0}
+    const float4 V = s_pt[3 * j + 2];  // {v, 0}   Sigma_j = lambda3 I + u u^T + v v^T
     const float4 P0 = p.s0, P1 = p.s1, P2 = p.s2;
     // e = mu' - kT mu   (Eq.4);  m = R mu = q - t
     const float ex = P0.x - p.qx, ey = P0.y - p.qy, ez = P0.z - p.qz;
     const float mx = p.qx - tx, my = p.qy - ty, mz = p.qz - tz;
-    // C = Sigma' + R Sigma R^T  (Eq.4)
-    const float s00 = A.w, s01 = B.x, s02 = B.y, s11 = B.z, s12 = B.w, s22 = Cc.x;
-    const float a00 = R00 * s00 + R01 * s01 + R02 * s02;
-    const float a01 = R00 * s01 + R01 * s11 + R02 * s12;
-    const float a02 = R00 * s02 + R01 * s12 + R02 * s22;
-    const float a10 = R10 * s00 + R11 * s01 + R12 * s02;
-    const float a11 = R10 * s01 + R11 * s11 + R12 * s12;
-    const float a12 = R10 * s02 + R11 * s12 + R12 * s22;
-    const float a20 = R20 * s00 + R21 * s01 + R22 * s02;
-    const float a21 = R20 * s01 + R21 * s11 + R22 * s12;
-    const float a22 = R20 * s02 + R21 * s12 + R22 * s22;
-    const float c00 = fmaf(a00, R00, fmaf(a01, R01, fmaf(a02, R02, P1.x)));
-    const float c01 = fmaf(a00, R10, fmaf(a01, R11, fmaf(a02, R12, P1.y)));
-    const float c02 = fmaf(a00, R20, fmaf(a01, R21, fmaf(a02, R22, P1.z)));
-    const float c11 = fmaf(a10, R10, fmaf(a11, R11, fmaf(a12, R12, P1.w)));
-    const float c12 = fmaf(a10, R20, fmaf(a11, R21, fmaf(a12, R22, P2.x)));
-    const float c22 = fmaf(a20, R20, fmaf(a21, R21, fmaf(a22, R22, P2.y)));
+    // C = Sigma' + R Sigma R^T = Sigma' + lambda3 I + (Ru)(Ru)^T + (Rv)(Rv)^T  (Eq.4)
+    const float ux = R00 * U.x + R01 * U.y + R02 * U.z;
+    const float uy = R10 * U.x + R11 * U.y + R12 * U.z;
+    const float uz = R20 * U.x + R21 * U.y + R22 * U.z;
+    const float vx = R00 * V.x + R01 * V.y + R02 * V.z;
+    const float vy = R10 * V.x + R11 * V.y + R12 * V.z;
+    const float vz = R20 * V.x + R21 * V.y + R22 * V.z;
+    const float c00 = fmaf(ux, ux, fmaf(vx, vx, P1.x + A.w));
+    const float c01 = fmaf(ux, uy, fmaf(vx, vy, P1.y));
+    const float c02 = fmaf(ux, uz, fmaf(vx, vz, P1.z));
+    const float c11 = fmaf(uy, uy, fmaf(vy, vy, P1.w + A.w));
+    const float c12 = fmaf(uy, uz, fmaf(vy, vz, P2.x));
+    const float c22 = fmaf(uz, uz, fmaf(vz, vz, P2.y + A.w));
     // Omega = C^-1 = adj(C) / det(C)
     const float k00 = c11 * c22 - c12 * c12;
     const float k01 = c02 * c12 - c01 * c22;
@@ -221,6 +232,66 @@ __global__ void __launch_bounds__(kSweepThreads)
   o[5] = make_float4(h[18], h[19], h[20], bv[0]);
   o[6] = make_float4(bv[1], bv[2], bv[3], bv[4]);
   o[7] = make_float4(bv[5], 0.f, 0.f, 0.f);
+}
+
+// Scan preparation (once per update): Sigma_j = lambda3 I + u u^T + v v^T with u, v the two
+// leading eigenvectors scaled by sqrt(lambda_k - lambda3) — the spectral decomposition,
+// exact up to rounding for any symmetric Sigma (fp64 cyclic Jacobi, then rounded).  The sweep
+// then forms R Sigma R^T as lambda3 I + (Ru)(Ru)^T + (Rv)(Rv)^T (33 FP32 ops instead of 45).
+__global__ void prepare_scan_kernel(const float* __restrict__ mean3,
+                                    const float* __restrict__ cov6, int S,
+                                    float4* __restrict__ out) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= S) return;
+  const float* c = cov6 + 6 * j;
+  double a[3][3] = {{c[0], c[1], c[2]}, {c[1], c[3], c[4]}, {c[2], c[4], c[5]}};
+  double v[3][3] = {{1, 0, 0}, {0, 1, 0}, {0, 0, 1}};
+  for (int sweep = 0; sweep < 12; ++sweep) {
+    const double off = a[0][1] * a[0][1] + a[0][2] * a[0][2] + a[1][2] * a[1][2];
+    const double dg = a[0][0] * a[0][0] + a[1][1] * a[1][1] + a[2][2] * a[2][2];
+    if (off <= 1e-36 * dg) break;
+    for (int pq = 0; pq < 3; ++pq) {
+      const int p = pq == 2 ? 1 : 0, q = pq == 0 ? 1 : 2;
+      if (a[p][q] == 0.0) continue;
+      const double theta = (a[q][q] - a[p][p]) / (2.0 * a[p][q]);
+      const double tt = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+      const double cs = 1.0 / sqrt(tt * tt + 1.0), sn = tt * cs;
+      for (int k = 0; k < 3; ++k) {  // A <- J^T A J
+        const double akp = a[k][p], akq = a[k][q];
+        a[k][p] = cs * akp - sn * akq;
+        a[k][q] = sn * akp + cs * akq;
+      }
+      for (int k = 0; k < 3; ++k) {
+        const double apk = a[p][k], aqk = a[q][k];
+        a[p][k] = cs * apk - sn * aqk;
+        a[q][k] = sn * apk + cs * aqk;
+      }
+      for (int k = 0; k < 3; ++k) {  // V <- V J
+        const double vkp = v[k][p], vkq = v[k][q];
+        v[k][p] = cs * vkp - sn * vkq;
+        v[k][q] = sn * vkp + cs * vkq;
+      }
+    }
+  }
+  // order eigenvalues: l0 >= l1 >= l2
+  int i0 = 0, i1 = 1, i2 = 2;
+  double lam[3] = {a[0][0], a[1][1], a[2][2]};
+  if (lam[i0] < lam[i1]) { int t = i0; i0 = i1; i1 = t; }
+  if (lam[i1] < lam[i2]) { int t = i1; i1 = i2; i2 = t; }
+  if (lam[i0] < lam[i1]) { int t = i0; i0 = i1; i1 = t; }
+  const double l3 = lam[i2];
+  const double su = sqrt(fmax(lam[i0] - l3, 0.0)), sv = sqrt(fmax(lam[i1] - l3, 0.0));
+  const float* m = mean3 + 3 * j;
+  out[3 * j + 0] = make_float4(m[0], m[1], m[2], (float)l3);
+  out[3 * j + 1] = make_float4((float)(su * v[0][i0]), (float)(su * v[1][i0]),
+                               (float)(su * v[2][i0]), 0.f);
+  out[3 * j + 2] = make_float4((float)(sv * v[0][i1]), (float)(sv * v[1][i1]),
+                               (float)(sv * v[2][i1]), 0.f);
+}
+
+void launch_prepare_scan(const float* mean3, const float* cov6, int S, float4* out,
+                         cudaStream_t st) {
+  prepare_scan_kernel<<<(S + 127) / 128, 128, 0, st>>>(mean3, cov6, S, out);
 }
 
 void launch_sweep(mcs_ctx* c, int S) {

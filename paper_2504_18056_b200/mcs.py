@@ -17,7 +17,7 @@ import re
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmcs.so")
+LIB_PATH = os.environ.get("MCS_LIB", os.path.join(_HERE, "libmcs.so"))
 HEADER = os.path.join(os.path.dirname(_HERE), "include", "mcs.h")
 
 ABI_VERSION = 1
