@@ -9,12 +9,9 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 VARIANTS = {
-    "base": [],
-    "depth2": ["MCS_EXP_DEPTH2"],
-    "magic": ["MCS_EXP_MAGICFLOOR"],
-    "depth2_magic": ["MCS_EXP_DEPTH2", "MCS_EXP_MAGICFLOOR"],
-    "depth2_magic_t64": ["MCS_EXP_DEPTH2", "MCS_EXP_MAGICFLOOR", "MCS_SWEEP_THREADS=64"],
-    "nomath_magic": ["MCS_EXP_NOMATH", "MCS_EXP_MAGICFLOOR"],
+    "sync_v5": [],
+    "sync_v5_t64": ["MCS_SWEEP_THREADS=64"],
+    "sync_v5_c128": ["MCS_SWEEP_CHUNK=128"],
 }
 OUT = os.path.join(ROOT, "bench", "_variants")
 

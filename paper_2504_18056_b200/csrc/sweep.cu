@@ -45,6 +45,34 @@ __device__ __forceinline__ float rcp_approx(float x) {
   return r;
 }
 
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned int sa = (unsigned int)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+#ifndef MCS_SWEEP_DEPTH
+#define MCS_SWEEP_DEPTH 3
+#endif
+constexpr int kDepth = MCS_SWEEP_DEPTH;      // probes in flight per thread
+constexpr int kStages = kDepth + 1;          // ring of per-thread staging slots in smem
+
+__device__ __forceinline__ void ld_slot(const float4* sl, float4& s0, float4& s1, float4& s2) {
+  asm volatile("ld.global.nc.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(s0.x), "=f"(s0.y), "=f"(s0.z), "=f"(s0.w) : "l"(sl));
+  asm volatile("ld.global.nc.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(s1.x), "=f"(s1.y), "=f"(s1.z), "=f"(s1.w) : "l"(sl + 1));
+  asm volatile("ld.global.nc.v2.f32 {%0, %1}, [%2];" : "=f"(s2.x), "=f"(s2.y) : "l"(sl + 2));
+  s2.z = 0.f;
+  s2.w = 0.f;
+}
+
 // floor(x) as the bits of x + 1.5*2^23 rounded toward -inf: exact for |x| < 2^22, and every
 // other finite x maps far outside any keyframe bbox after the offset.
 constexpr float kMagic = 12582912.0f;
@@ -54,6 +82,10 @@ __global__ void __launch_bounds__(kSweepThreads, MCS_SWEEP_MINBLOCKS)
                  int n_items, const float4* __restrict__ scan, int S,
                  const KfMeta* __restrict__ kmeta, float inv_r, float* __restrict__ part) {
   __shared__ float4 s_pt[kChunk * 3];
+#ifdef MCS_SWEEP_ASYNC
+  // per-thread probe staging: [stage][0..2 = slot float4s, 3 = {q, key}][thread]
+  __shared__ float4 s_stage[kStages][4][kSweepThreads];
+#endif
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   const int item = t < n_items ? order[t] : -1;
   float4 r0 = make_float4(0, 0, 0, 0), r1 = r0, r2 = r0, inf = r0;
@@ -102,9 +134,9 @@ __global__ void __launch_bounds__(kSweepThreads, MCS_SWEEP_MINBLOCKS)
     p.h = slot_hash(p.key, m.shift) & m.mask;
     const float4* sl = m.slots + 4 * (size_t)p.h;
     if (active) {
-      p.s0 = __ldg(sl);
-      p.s1 = __ldg(sl + 1);
-      p.s2 = __ldg(sl + 2);
+      // volatile: the compiler may not sink these loads towards their use (that would undo the
+      // prefetch); the payload is consumed one point later
+      ld_slot(sl, p.s0, p.s1, p.s2);
     }
     return p;
   };
@@ -118,21 +150,26 @@ __global__ void __launch_bounds__(kSweepThreads, MCS_SWEEP_MINBLOCKS)
 #pragma unroll
   for (int k = 0; k < 6; ++k) bv[k] = 0.f;
 
-  // first-probe hit, or an empty slot / out-of-bbox point (miss), else keep probing
-  auto resolve = [&](Probe& p) -> bool {
+  // first probe: 1 = hit, 0 = empty slot or out-of-bbox point (miss), 2 = keep probing
+  auto first_check = [&](const Probe& p) -> int {
     const unsigned int k0 = __float_as_uint(p.s0.w);
-    if (k0 == p.key) return p.key != kEmptyKey32;
-    if (k0 == kEmptyKey32 || p.key == kEmptyKey32) return false;
-    unsigned int hh = p.h;
+    if (k0 == p.key) return p.key != kEmptyKey32 ? 1 : 0;
+    if (k0 == kEmptyKey32 || p.key == kEmptyKey32) return 0;
+    return 2;
+  };
+  // continue linear probing (rare): loads into fresh registers q.s*, waited on inside this
+  // path, so the common path never inherits a pending scoreboard from it
+  auto probe_on = [&](Probe& q) -> bool {
+    unsigned int hh = q.h;
     while (true) {
       hh = (hh + 1) & m.mask;
       const float4* sl = m.slots + 4 * (size_t)hh;
       const float4 t0 = __ldg(sl);
       const unsigned int kk = __float_as_uint(t0.w);
-      if (kk == p.key) {
-        p.s0 = t0;
-        p.s1 = __ldg(sl + 1);
-        p.s2 = __ldg(sl + 2);
+      if (kk == q.key) {
+        q.s0 = t0;
+        q.s1 = __ldg(sl + 1);
+        q.s2 = __ldg(sl + 2);
         return true;
       }
       if (kk == kEmptyKey32) return false;
@@ -209,18 +246,83 @@ __global__ void __launch_bounds__(kSweepThreads, MCS_SWEEP_MINBLOCKS)
     for (int k = threadIdx.x; k < cnt * 3; k += kSweepThreads) s_pt[k] = scan[3 * base + k];
     __syncthreads();
     if (!active) continue;
+#ifndef MCS_SWEEP_ASYNC
     // two probe buffers in flight alternately: the slot of point j+1 is requested before the
     // math of point j (no register copies between iterations)
     Probe pa = issue(0), pb;
     for (int j = 0; j < cnt; j += 2) {
-      const bool ha = resolve(pa);
+      const int ra = first_check(pa);
       if (j + 1 < cnt) pb = issue(j + 1);
-      if (ha) accumulate(j, pa);
+      if (ra == 1) {
+        accumulate(j, pa);
+      } else if (ra == 2) {
+        Probe q;
+        q.qx = pa.qx; q.qy = pa.qy; q.qz = pa.qz; q.key = pa.key; q.h = pa.h;
+        if (probe_on(q)) accumulate(j, q);
+      }
       if (j + 1 >= cnt) break;
-      const bool hb2 = resolve(pb);
+      const int rb = first_check(pb);
       if (j + 2 < cnt) pa = issue(j + 2);
-      if (hb2) accumulate(j + 1, pb);
+      if (rb == 1) {
+        accumulate(j + 1, pb);
+      } else if (rb == 2) {
+        Probe q;
+        q.qx = pb.qx; q.qy = pb.qy; q.qz = pb.qz; q.key = pb.key; q.h = pb.h;
+        if (probe_on(q)) accumulate(j + 1, q);
+      }
     }
+#else
+    // kDepth probes in flight through cp.async into a per-thread smem ring: the slot copies
+    // never hold a register scoreboard, so the math of point j never waits on the loads of
+    // points j+1..j+kDepth.
+    const int tid = threadIdx.x;
+    auto stage_issue = [&](int j) {
+      const int st = j % kStages;
+      const float4 A = s_pt[3 * j];
+      const float qx = __fmaf_rn(R02, A.z, __fmaf_rn(R01, A.y, __fmaf_rn(R00, A.x, tx)));
+      const float qy = __fmaf_rn(R12, A.z, __fmaf_rn(R11, A.y, __fmaf_rn(R10, A.x, ty)));
+      const float qz = __fmaf_rn(R22, A.z, __fmaf_rn(R21, A.y, __fmaf_rn(R20, A.x, tz)));
+      const unsigned int dx =
+          (unsigned)__float_as_int(__fadd_rd(__fmul_rn(qx, inv_r), kMagic)) - offx;
+      const unsigned int dy =
+          (unsigned)__float_as_int(__fadd_rd(__fmul_rn(qy, inv_r), kMagic)) - offy;
+      const unsigned int dz =
+          (unsigned)__float_as_int(__fadd_rd(__fmul_rn(qz, inv_r), kMagic)) - offz;
+      const bool in = (dx < m.ex) & (dy < m.ey) & (dz < m.ez);
+      const unsigned int key = in ? local_key(dx, dy, dz) : kEmptyKey32;
+      const unsigned int hh = slot_hash(key, m.shift) & m.mask;
+      const float4* sl = m.slots + 4 * (size_t)hh;
+      cp_async16(&s_stage[st][0][tid], sl);
+      cp_async16(&s_stage[st][1][tid], sl + 1);
+      cp_async16(&s_stage[st][2][tid], sl + 2);
+      s_stage[st][3][tid] = make_float4(qx, qy, qz, __uint_as_float(key));
+    };
+#pragma unroll
+    for (int d = 0; d < kDepth; ++d) {
+      if (d < cnt) stage_issue(d);
+      cp_async_commit();
+    }
+    for (int j = 0; j < cnt; ++j) {
+      if (j + kDepth < cnt) stage_issue(j + kDepth);
+      cp_async_commit();
+      cp_async_wait<kDepth>();
+      const int st = j % kStages;
+      Probe p;
+      const float4 qk = s_stage[st][3][tid];
+      p.qx = qk.x;
+      p.qy = qk.y;
+      p.qz = qk.z;
+      p.key = __float_as_uint(qk.w);
+      p.h = slot_hash(p.key, m.shift) & m.mask;
+      p.s0 = s_stage[st][0][tid];
+      p.s1 = s_stage[st][1][tid];
+      p.s2 = s_stage[st][2][tid];
+      const int r = first_check(p);
+      if (r == 1) accumulate(j, p);
+      else if (r == 2 && probe_on(p)) accumulate(j, p);
+    }
+    cp_async_wait<0>();
+#endif
   }
   if (!active) return;
   float4* o = reinterpret_cast<float4*>(part + (size_t)item * kSlotFloats);
