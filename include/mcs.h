@@ -167,6 +167,20 @@ MCS_API mcs_status mcs_resample(mcs_ctx* ctx, const double* e, const uint8_t* de
 MCS_API mcs_status mcs_snapshot(mcs_ctx* ctx);
 MCS_API mcs_status mcs_restore(mcs_ctx* ctx);
 
+/* Multi-GPU respawn plan (host functions; pure functions of allgathered per-rank totals).
+ * mcs_plan_ladder: from every rank's survivor-ladder total Q_g (sum of floor(e_i 2^32) over its
+ * survivors, R18) and dead count D_g, in rank order: each rank's ladder and dead offsets, the
+ * number of clones its survivors make under the GLOBAL systematic count formula with uniform u,
+ * and the totals.  MCS_E_DEGENERATE if D > 0 and Q = 0.  Output pointers may be NULL.
+ * mcs_plan_migration: send_counts[src * world + dst] = clones made on rank src that land in dead
+ * slots of rank dst (the r-th global clone fills the r-th global dead slot, both ascending). */
+MCS_API mcs_status mcs_plan_ladder(int32_t world, const uint64_t* Q_per_rank,
+                                   const int64_t* D_per_rank, uint32_t u, uint64_t* q_offset,
+                                   int64_t* d_offset, int64_t* clones_per_rank, uint64_t* Q_total,
+                                   int64_t* D_total);
+MCS_API mcs_status mcs_plan_migration(int32_t world, const int64_t* clones_per_rank,
+                                      const int64_t* dead_per_rank, int64_t* send_counts);
+
 /* Per-particle state bytes with K keyframes: 48 (T_t) + 48 K (T_k) + 8 (L). */
 MCS_API size_t mcs_state_bytes_per_particle(int32_t n_keyframes);
 

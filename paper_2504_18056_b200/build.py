@@ -15,7 +15,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libmcs.so")
-SOURCES = ["api.cu", "kf_store.cu", "select.cu", "sweep.cu", "update.cu", "weights.cu"]
+SOURCES = ["api.cu", "kf_store.cu", "select.cu", "sweep.cu", "update.cu", "weights.cu", "dist.cu"]
 HEADERS = ["mcs_internal.cuh", "reduce.cuh"]
 
 NVCC_FLAGS = [

@@ -93,6 +93,8 @@ def load() -> C.CDLL:
         "mcs_state_bytes_per_particle": (C.c_size_t, [i32]),
         "mcs_set_profiling": (st, [vp, i32]),
         "mcs_get_phase_ms": (st, [vp, vp]),
+        "mcs_plan_ladder": (st, [i32, vp, vp, u32, vp, vp, vp, vp, vp]),
+        "mcs_plan_migration": (st, [i32, vp, vp, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -300,6 +302,35 @@ class Context:
         self._check(self._lib.mcs_get_phase_ms(self._ctx, ms))
         return {"select": ms[0], "sweep": ms[1], "update": ms[2], "weights": ms[3],
                 "total": ms[4]}
+
+
+def plan_ladder(Q_per_rank, D_per_rank, u: int):
+    """Host plan of the global respawn ladder (mcs_plan_ladder): per-rank offsets and clone counts."""
+    Q = np.ascontiguousarray(Q_per_rank, np.uint64)
+    D = np.ascontiguousarray(D_per_rank, np.int64)
+    G = len(Q)
+    qo = np.zeros(G, np.uint64)
+    do = np.zeros(G, np.int64)
+    cl = np.zeros(G, np.int64)
+    qt = np.zeros(1, np.uint64)
+    dt = np.zeros(1, np.int64)
+    st = load().mcs_plan_ladder(G, Q.ctypes.data, D.ctypes.data, int(u) & 0xFFFFFFFF,
+                                qo.ctypes.data, do.ctypes.data, cl.ctypes.data, qt.ctypes.data,
+                                dt.ctypes.data)
+    return {"status": int(st), "q_offset": qo, "d_offset": do, "clones": cl,
+            "Q": int(qt[0]), "D": int(dt[0])}
+
+
+def plan_migration(clones_per_rank, dead_per_rank):
+    """send[src, dst] = clones made on rank src that fill dead slots on rank dst."""
+    c = np.ascontiguousarray(clones_per_rank, np.int64)
+    d = np.ascontiguousarray(dead_per_rank, np.int64)
+    G = len(c)
+    out = np.zeros((G, G), np.int64)
+    st = load().mcs_plan_migration(G, c.ctypes.data, d.ctypes.data, out.ctypes.data)
+    if st:
+        raise MCSError(st, "invalid migration plan input")
+    return out
 
 
 def unpack_h21(h21):
