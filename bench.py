@@ -35,7 +35,7 @@ FLOPS_MATCHED = 236.0    # FP32 flops per matched (particle, point, slot) with H
 FLOPS_UNMATCHED = 21.0   # transform + key for an unmatched triple
 GATHER_MATCHED = 56.0    # bytes: 8-B key probe + 48-B payload
 GATHER_UNMATCHED = 8.0
-LAUNCHES_PER_UPDATE = 19  # see DESIGN.md §5 (verified against the ncu launch list)
+LAUNCHES_PER_UPDATE = 25  # kernels per mcs_update_async incl. CUB sort/scan (profiles/r01_launch_shares.txt)
 
 
 def dist_env():
@@ -219,11 +219,10 @@ def run_gpu(args):
             e1.record(stream)
         return e0, e1
 
-    for _ in range(args.warmup):
-        one_step()
-    torch.cuda.synchronize()
     step_ms, sweep_ms, phases = [], [], []
     with ClockSampler(local) as clocks:
+        for _ in range(args.warmup):
+            one_step()
         torch.cuda.synchronize()
         for _ in range(args.steps):
             e0, e1 = one_step()
@@ -298,7 +297,7 @@ def run_gpu(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--particles", type=int, default=100_000)
