@@ -179,15 +179,21 @@ def run_gpu(args):
 
     import paper_2504_18056_b200 as mcs
     rank, world, local = dist_env()
-    if world > 1:
-        raise SystemExit("multi-GPU bench requires the NCCL build of libmcs (not yet)")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    s = make_scene(args.particles)
+    dist = None
+    extra = {}
+    if world > 1:  # one process per GPU; the library owns its own NCCL communicator
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+        obj = [mcs.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        extra = dict(world_size=world, rank=rank, nccl_unique_id=obj[0])
+    s = make_scene(args.particles)  # every rank: the same keyframes and scan, its own shard
     N, S, K = s.N, s.S, s.K
     stream = torch.cuda.Stream(device=dev)
     ctx = mcs.Context(N, K, S, neighbor_count=3, loop_recency_gap=s.gap, voxel_resolution=s.r,
-                      device=local)
+                      device=local, **extra)
     ctx.set_stream(stream)
     t0 = time.perf_counter()
     for (m3, c6), d in zip(s.keyframes, s.D):
@@ -224,6 +230,9 @@ def run_gpu(args):
         for _ in range(args.warmup):
             one_step()
         torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
         for _ in range(args.steps):
             e0, e1 = one_step()
             e1.synchronize()
@@ -232,9 +241,16 @@ def run_gpu(args):
             phases.append(ph)
             sweep_ms.append(ph["sweep"])
         torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
     total_ms = float(np.sum(step_ms))
+    if dist:  # the job's time is the slowest rank's
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
     ms = total_ms / args.steps
-    value = N * S * args.steps / (total_ms * 1e-3)
+    value = world * N * S * args.steps / (total_ms * 1e-3)
 
     # e2e: the public synchronous call with pinned host buffers (H2D scan, D2H results)
     h_m = torch.from_numpy(s.scan_mean3).pin_memory()
@@ -248,7 +264,12 @@ def run_gpu(args):
         t2 = time.perf_counter()
         if k >= args.warmup:
             e2e_t.append(t2 - t1)
-    e2e_value = N * S / float(np.mean(e2e_t))
+    e2e_mean = float(np.mean(e2e_t))
+    if dist:
+        t = torch.tensor([e2e_mean], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_mean = float(t.item())
+    e2e_value = world * N * S / e2e_mean
 
     peaks, peak_src = measured_peaks()
     sm_mhz = peaks.get("sm_max_mhz", 1965.0)
@@ -264,7 +285,8 @@ def run_gpu(args):
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": "C2: 100k particles x 4096-pt LiDAR-like scan vs 20 keyframes "
                                "(loop corridor, r = 0.5 m, 3 neighbours, every particle loops)",
-                   "particles": N, "scan_points": S, "keyframes": K,
+                   "particles": N * world, "particles_per_gpu": N, "scan_points": S,
+                   "keyframes": K, "parallelism": f"particle shards x{world} (NCCL)",
                    "keyframe_cells": int(sum(len(k[0]) for k in s.keyframes)),
                    "l2": "particle state restored from a device snapshot and 256 MiB L2 flush "
                          "before every timed step (untimed)"},
@@ -276,7 +298,7 @@ def run_gpu(args):
                      "flops_per_launch": flops, "sweep_ms": sweep_avg,
                      "l2_gather_GBps": gather / (sweep_avg * 1e-3) / 1e9},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(36 * S),
-                "d2h_bytes_per_step": int(16 * N + 4 + 8), "ms_per_step": 1e3 * float(np.mean(e2e_t))},
+                "d2h_bytes_per_step": int(16 * N + 4 + 8), "ms_per_step": 1e3 * e2e_mean},
         "gpu_launches": LAUNCHES_PER_UPDATE * args.steps,
         "clocks": clocks.summary(),
         "ms_p10_p50_p90": [float(np.percentile(step_ms, q)) for q in (10, 50, 90)],
@@ -286,11 +308,14 @@ def run_gpu(args):
         "a0_ms_per_keyframe": a0_ms,
         "n_dead": int(out["n_dead"][0]),
     }
-    if rank == 0 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"], _ = cpu_baseline(s, args.cpu_budget_s)
     ctx.close()
     if rank == 0:
         print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
     return 0
 
 

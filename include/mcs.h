@@ -69,6 +69,20 @@ typedef enum { MCS_GN_OLD_SLOTS = 0, /* Fig.3: gradient w.r.t. non-recent 
                MCS_GN_ALL_SLOTS = 1  /* every neighbour slot                      */
 } mcs_gn_slots;
 
+/* Collective transport for world_size > 1 when NCCL is not used (e.g. torch.distributed gloo or
+ * the in-process transport below).  Buffers are HOST memory; every rank calls the same sequence
+ * of operations.  allreduce: in place over n values (dtype 0 = f64, 1 = i64; op 0 = sum,
+ * 1 = max), reduced in rank order.  allgather: `bytes` from every rank into recv[world][bytes].
+ * alltoallv: send[p] (send_bytes[p]) goes to rank p, recv[p] (recv_bytes[p]) comes from rank p.
+ * Each returns 0 on success. */
+typedef struct mcs_transport {
+  void* user;
+  int (*allreduce)(void* user, int32_t rank, void* buf, int32_t n, int32_t dtype, int32_t op);
+  int (*allgather)(void* user, int32_t rank, const void* send, void* recv, size_t bytes);
+  int (*alltoallv)(void* user, int32_t rank, const void* const* send, const size_t* send_bytes,
+                   void* const* recv, const size_t* recv_bytes);
+} mcs_transport;
+
 typedef struct mcs_config {
   uint32_t abi_version;          /* MCS_ABI_VERSION                                         */
   int32_t  capacity_particles;   /* particles on this device (its shard when world_size>1)  */
@@ -86,6 +100,7 @@ typedef struct mcs_config {
   int32_t  device;               /* CUDA ordinal                                            */
   int32_t  rank, world_size;     /* particle shards (one process per GPU)                   */
   const void* nccl_unique_id;    /* 128-byte ncclUniqueId when world_size > 1, else NULL    */
+  const mcs_transport* transport; /* host transport when world_size > 1 without NCCL        */
 } mcs_config;
 
 /* Fills *cfg with the defaults above (capacities 0: caller sets them). */
@@ -121,7 +136,8 @@ MCS_API mcs_status mcs_get_sizes(const mcs_ctx* ctx, int32_t* n_local, int32_t* 
  * MCS_GN_OLD_SLOTS); hess21 = undamped H over G; psi6 = applied update (0 if none);
  * weight = w_i after respawn; donor = -1 or the GLOBAL index cloned into slot i;
  * flags: bit0 loop, bit1 updated, bit2 singular, bit3 dead before respawn, bit4 clamped;
- * representative = GLOBAL argmax w (ties -> lowest); n_dead = global dead count. */
+ * representative = GLOBAL argmax w (ties -> lowest); n_dead = global dead count.
+ * Global index = sum of the local particle counts of lower ranks + local index. */
 typedef struct {
   double*  loglik;
   float*   grad6;
@@ -180,6 +196,15 @@ MCS_API mcs_status mcs_plan_ladder(int32_t world, const uint64_t* Q_per_rank,
                                    int64_t* D_total);
 MCS_API mcs_status mcs_plan_migration(int32_t world, const int64_t* clones_per_rank,
                                       const int64_t* dead_per_rank, int64_t* send_counts);
+
+/* NCCL unique id (128 bytes) for mcs_config.nccl_unique_id; rank 0 creates it and the caller
+ * broadcasts it (e.g. through torch.distributed).  MCS_E_NCCL if libnccl.so.2 is unavailable. */
+MCS_API mcs_status mcs_nccl_unique_id(void* out128);
+
+/* In-process transport joining `world` contexts of one process (one thread per rank); for tests
+ * of the multi-rank path on a single device.  Reductions run in rank order. */
+MCS_API mcs_transport* mcs_inproc_transport_create(int32_t world);
+MCS_API void mcs_inproc_transport_destroy(mcs_transport* t);
 
 /* Per-particle state bytes with K keyframes: 48 (T_t) + 48 K (T_k) + 8 (L). */
 MCS_API size_t mcs_state_bytes_per_particle(int32_t n_keyframes);

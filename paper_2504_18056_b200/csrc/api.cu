@@ -131,12 +131,11 @@ __global__ void gather_outputs_kernel(OutPtrs o, int N, int capN, const double* 
                                       const double* __restrict__ psi,
                                       const double* __restrict__ w,
                                       const int32_t* __restrict__ donor,
-                                      const uint8_t* __restrict__ flags, const Scalars* sc,
-                                      int base_index) {
+                                      const uint8_t* __restrict__ flags, const Scalars* sc) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i == 0) {
-    if (o.rep) *o.rep = sc->rep;
-    if (o.n_dead) *o.n_dead = sc->D;
+    if (o.rep) *o.rep = (int32_t)sc->rep;
+    if (o.n_dead) *o.n_dead = sc->D_tot;
   }
   if (i >= N) return;
   if (o.loglik) o.loglik[i] = l[i];
@@ -147,7 +146,7 @@ __global__ void gather_outputs_kernel(OutPtrs o, int N, int capN, const double* 
   if (o.psi6)
     for (int k = 0; k < 6; ++k) o.psi6[(size_t)i * 6 + k] = (float)psi[(size_t)k * capN + i];
   if (o.weight) o.weight[i] = w[i];
-  if (o.donor) o.donor[i] = donor[i] < 0 ? -1 : donor[i] + base_index;
+  if (o.donor) o.donor[i] = donor[i];
   if (o.flags) o.flags[i] = flags[i];
 }
 
@@ -172,10 +171,13 @@ static void free_all(mcs_ctx* c) {
                   c->d_grad,    c->d_hess,    c->d_flags,    c->d_e,        c->d_w,
                   c->d_ladder,  c->d_ladder_scan, c->d_ncum, c->d_donor,    c->d_partials,
                   c->d_ipartials, c->d_scal,  c->d_cub_temp, c->d_skeys, c->d_skeys_out,
-                  c->d_sids,    c->d_stage,   c->d_bad};
+                  c->d_sids,    c->d_stage,   c->d_bad,      c->d_dead_list, c->d_donor_g,
+                  c->d_plan,    c->d_pack_src, c->d_send,    c->d_recv};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->h_scal) cudaFreeHost(c->h_scal);
+  if (c->h_stage) cudaFreeHost(c->h_stage);
+  dist_destroy(c);
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
@@ -255,8 +257,12 @@ mcs_status mcs_create(const mcs_config* cfg, mcs_ctx** out) {
     g_create_error = "invalid numeric configuration";
     return MCS_E_INVALID_ARG;
   }
-  if (cfg->world_size != 1 || cfg->rank != 0) {
-    g_create_error = "world_size > 1 requires the NCCL build (not in this library version)";
+  if (cfg->world_size < 1 || cfg->rank < 0 || cfg->rank >= cfg->world_size) {
+    g_create_error = "need 0 <= rank < world_size";
+    return MCS_E_INVALID_ARG;
+  }
+  if (cfg->world_size > 1 && !cfg->transport && !cfg->nccl_unique_id) {
+    g_create_error = "world_size > 1 needs nccl_unique_id or a transport";
     return MCS_E_INVALID_ARG;
   }
   if ((long long)cfg->capacity_particles * cfg->neighbor_count > 0x7fffffffLL) {
@@ -292,6 +298,9 @@ mcs_status mcs_create(const mcs_config* cfg, mcs_ctx** out) {
   if (e == cudaSuccess) e = dalloc(&c->d_skeys_out, nb * N);
   if (e == cudaSuccess) e = dalloc(&c->d_sids, nb * N);
   if (e == cudaSuccess) e = dalloc(&c->d_bad, 1);
+  if (e == cudaSuccess) e = dalloc(&c->d_dead_list, N);
+  if (e == cudaSuccess) e = dalloc(&c->d_donor_g, N);
+  if (e == cudaSuccess) e = dalloc(&c->d_plan, 5 * (size_t)(cfg->world_size + 1));
   if (e == cudaSuccess) {
     c->stage_bytes = StageLayout(N).total;
     e = dalloc(&c->d_stage, c->stage_bytes);
@@ -328,6 +337,16 @@ mcs_status mcs_create(const mcs_config* cfg, mcs_ctx** out) {
   }
   for (int k = 0; k < 6 && e == cudaSuccess; ++k) e = cudaEventCreate(&c->ev[k]);
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e == cudaSuccess) {
+    std::string derr;
+    const mcs_status ds = dist_init(c, derr);
+    if (ds != MCS_OK) {
+      g_create_error = derr;
+      free_all(c);
+      delete c;
+      return ds;
+    }
+  }
   if (e != cudaSuccess) {
     g_create_error = std::string("CUDA: ") + cudaGetErrorString(e);
     free_all(c);
@@ -494,6 +513,16 @@ mcs_status mcs_set_particles(mcs_ctx* ctx, int32_t n, const float* pose12,
   cudaFreeAsync(bad, st);
   CUDA_TRY(ctx, cudaStreamSynchronize(st));
   ctx->N = n;
+  // global index base of this shard (collective over ranks)
+  ctx->n_per_rank.assign(ctx->world, 0);
+  const long long mine = n;
+  const mcs_status ds = dist_allgather_host(ctx, &mine, ctx->n_per_rank.data(), sizeof(long long));
+  if (ds != MCS_OK) {
+    ctx->sticky = ds;
+    FAIL(ctx, ds, "allgather of the shard sizes failed");
+  }
+  ctx->gbase = 0;
+  for (int g = 0; g < ctx->rank; ++g) ctx->gbase += ctx->n_per_rank[g];
   return MCS_OK;
 }
 
@@ -551,8 +580,8 @@ static void record(mcs_ctx* ctx, int k) {
   if (ctx->profiling) cudaEventRecord(ctx->ev[k], ctx->stream);
 }
 
-// the hot path a1..a7, stream-ordered; scan already packed in d_scan
-static void run_update(mcs_ctx* ctx, int n_pts, double D_now, uint32_t U) {
+// the hot path a1..a7, stream-ordered; scan already prepared in d_scan
+static mcs_status run_update(mcs_ctx* ctx, int n_pts, double D_now, uint32_t U) {
   record(ctx, 0);
   launch_select(ctx, false);                                            // a1
   record(ctx, 1);
@@ -561,8 +590,9 @@ static void run_update(mcs_ctx* ctx, int n_pts, double D_now, uint32_t U) {
   launch_combine(ctx, n_pts, false, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr);  // a3
   launch_propagate(ctx, D_now);                                         // a4
   record(ctx, 3);
-  launch_weights_resample(ctx, U);                                      // a5-a7
+  const mcs_status s = launch_weights_resample(ctx, U);                 // a5-a7 (+ exchanges)
   record(ctx, 4);
+  return s;
 }
 
 mcs_status mcs_update(mcs_ctx* ctx, const float* scan_mean3, const float* scan_cov6,
@@ -579,7 +609,11 @@ mcs_status mcs_update(mcs_ctx* ctx, const float* scan_mean3, const float* scan_c
   s = validate_scan(ctx, n_pts);
   if (s != MCS_OK) return s;
   launch_prepare_scan(raw_m, raw_c, n_pts, ctx->d_scan, st);
-  run_update(ctx, n_pts, D_now, resample_u);
+  s = run_update(ctx, n_pts, D_now, resample_u);
+  if (s != MCS_OK) {
+    ctx->sticky = s;
+    FAIL(ctx, s, "update failed in the weights/exchange phase (%d)", (int)s);
+  }
   CUDA_TRY(ctx, cudaGetLastError());
   const int N = ctx->N;
   if (out) {
@@ -595,8 +629,8 @@ mcs_status mcs_update(mcs_ctx* ctx, const float* scan_mean3, const float* scan_c
     if (out->donor) o.donor = (int32_t*)(stage + lay.d);
     if (out->flags) o.flags = (uint8_t*)(stage + lay.f);
     gather_outputs_kernel<<<(N + 255) / 256, 256, 0, st>>>(
-        o, N, ctx->capN, ctx->d_l, ctx->d_grad, ctx->d_hess, ctx->d_psi, ctx->d_w, ctx->d_donor,
-        ctx->d_flags, ctx->d_scal, 0);
+        o, N, ctx->capN, ctx->d_l, ctx->d_grad, ctx->d_hess, ctx->d_psi, ctx->d_w, ctx->d_donor_g,
+        ctx->d_flags, ctx->d_scal);
     if (out->loglik) CUDA_TRY(ctx, cudaMemcpyAsync(out->loglik, o.loglik, 8 * N, cudaMemcpyDefault, st));
     if (out->grad6) CUDA_TRY(ctx, cudaMemcpyAsync(out->grad6, o.grad6, 24 * N, cudaMemcpyDefault, st));
     if (out->hess21) CUDA_TRY(ctx, cudaMemcpyAsync(out->hess21, o.hess21, 84 * N, cudaMemcpyDefault, st));
@@ -608,8 +642,8 @@ mcs_status mcs_update(mcs_ctx* ctx, const float* scan_mean3, const float* scan_c
   CUDA_TRY(ctx, cudaMemcpyAsync(ctx->h_scal, ctx->d_scal, sizeof(Scalars), cudaMemcpyDeviceToHost,
                                 st));
   CUDA_TRY(ctx, cudaStreamSynchronize(st));
-  if (out && out->representative) *out->representative = ctx->h_scal->rep;
-  if (out && out->n_dead) *out->n_dead = ctx->h_scal->D;
+  if (out && out->representative) *out->representative = (int32_t)ctx->h_scal->rep;
+  if (out && out->n_dead) *out->n_dead = ctx->h_scal->D_tot;
   if (ctx->h_scal->status == MCS_E_DEGENERATE)
     FAIL(ctx, MCS_E_DEGENERATE, "every particle dead (S:381); respawn skipped");
   return MCS_OK;
@@ -624,13 +658,18 @@ mcs_status mcs_update_async(mcs_ctx* ctx, const float* d_scan_mean3, const float
   cudaStream_t saved = ctx->stream;
   if (cuda_stream) ctx->stream = (cudaStream_t)cuda_stream;
   launch_prepare_scan(d_scan_mean3, d_scan_cov6, n_pts, ctx->d_scan, ctx->stream);
-  run_update(ctx, n_pts, D_now, resample_u);
+  s = run_update(ctx, n_pts, D_now, resample_u);
+  if (s != MCS_OK) {
+    ctx->stream = saved;
+    ctx->sticky = s;
+    FAIL(ctx, s, "update failed in the weights/exchange phase (%d)", (int)s);
+  }
   if (d_out) {
     OutPtrs o{d_out->loglik, d_out->grad6,  d_out->hess21,         d_out->psi6,  d_out->weight,
               d_out->donor,  d_out->flags,  d_out->representative, d_out->n_dead};
     gather_outputs_kernel<<<(ctx->N + 255) / 256, 256, 0, ctx->stream>>>(
         o, ctx->N, ctx->capN, ctx->d_l, ctx->d_grad, ctx->d_hess, ctx->d_psi, ctx->d_w,
-        ctx->d_donor, ctx->d_flags, ctx->d_scal, 0);
+        ctx->d_donor_g, ctx->d_flags, ctx->d_scal);
   }
   cudaError_t e = cudaGetLastError();
   ctx->stream = saved;
@@ -693,7 +732,7 @@ mcs_status mcs_resample(mcs_ctx* ctx, const double* e, const uint8_t* dead, int3
   CUDA_TRY(ctx, to_device(de, e, 8 * (size_t)n, st));
   int32_t* ddon = nullptr;
   CUDA_TRY(ctx, cudaMallocAsync(&ddon, 4 * (size_t)n, st));
-  launch_resample_only(ctx, de, dd, n, u, ddon);
+  if (launch_resample_only(ctx, de, dd, n, u, ddon) != MCS_OK) CUDA_TRY(ctx, cudaGetLastError());
   CUDA_TRY(ctx, cudaGetLastError());
   CUDA_TRY(ctx, cudaMemcpyAsync(donor_out, ddon, 4 * (size_t)n, cudaMemcpyDefault, st));
   CUDA_TRY(ctx, cudaMemcpyAsync(ctx->h_scal, ctx->d_scal, sizeof(Scalars), cudaMemcpyDeviceToHost,

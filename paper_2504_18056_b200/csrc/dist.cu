@@ -86,3 +86,306 @@ mcs_status mcs_plan_migration(int32_t world, const int64_t* clones_per_rank,
 }
 
 }  // extern "C"
+
+// ======================================================================================
+// Exchange layer: NCCL (dlopen'ed libnccl.so.2, collectives on the context stream) or a host
+// transport (mcs_transport callbacks; small device buffers staged through pinned memory).
+// ======================================================================================
+#include <dlfcn.h>
+#include <string.h>
+
+#include <chrono>
+#include <condition_variable>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "mcs_internal.cuh"
+
+namespace {
+
+// minimal NCCL ABI (nccl.h 2.x), resolved at run time
+typedef struct { char internal[128]; } NcclId;
+typedef void* NcclComm;
+enum { kNcclInt8 = 0, kNcclUint8 = 1, kNcclFloat64 = 8 };
+enum { kNcclSum = 0, kNcclMax = 2 };
+struct NcclApi {
+  void* h = nullptr;
+  int (*GetUniqueId)(NcclId*) = nullptr;
+  int (*CommInitRank)(NcclComm*, int, NcclId, int) = nullptr;
+  int (*CommDestroy)(NcclComm) = nullptr;
+  int (*AllReduce)(const void*, void*, size_t, int, int, NcclComm, cudaStream_t) = nullptr;
+  int (*AllGather)(const void*, void*, size_t, int, NcclComm, cudaStream_t) = nullptr;
+  int (*Send)(const void*, size_t, int, int, NcclComm, cudaStream_t) = nullptr;
+  int (*Recv)(void*, size_t, int, int, NcclComm, cudaStream_t) = nullptr;
+  int (*GroupStart)() = nullptr;
+  int (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(int) = nullptr;
+};
+
+NcclApi* nccl() {
+  static NcclApi api;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return nullptr;
+    api.h = h;
+#define SYM(f, n) api.f = reinterpret_cast<decltype(api.f)>(dlsym(h, n))
+    SYM(GetUniqueId, "ncclGetUniqueId");
+    SYM(CommInitRank, "ncclCommInitRank");
+    SYM(CommDestroy, "ncclCommDestroy");
+    SYM(AllReduce, "ncclAllReduce");
+    SYM(AllGather, "ncclAllGather");
+    SYM(Send, "ncclSend");
+    SYM(Recv, "ncclRecv");
+    SYM(GroupStart, "ncclGroupStart");
+    SYM(GroupEnd, "ncclGroupEnd");
+    SYM(GetErrorString, "ncclGetErrorString");
+#undef SYM
+    if (!api.GetUniqueId || !api.CommInitRank || !api.AllReduce || !api.AllGather || !api.Send ||
+        !api.Recv || !api.GroupStart || !api.GroupEnd)
+      api.h = nullptr;
+  }
+  return api.h ? &api : nullptr;
+}
+
+// ---------------------------------------------------------------- in-process transport
+struct Inproc {
+  int world;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  long long gen = 0;
+  std::vector<const void*> in;        // per-rank input pointers of the current operation
+  std::vector<const size_t*> in_sizes;
+  mcs_transport t;
+
+  bool barrier() {
+    std::unique_lock<std::mutex> lk(mu);
+    const long long g = gen;
+    if (++arrived == world) {
+      arrived = 0;
+      ++gen;
+      cv.notify_all();
+      return true;
+    }
+    return cv.wait_for(lk, std::chrono::seconds(300), [&] { return gen != g; });
+  }
+};
+
+int ip_allreduce(void* user, int32_t rank, void* buf, int32_t n, int32_t dtype, int32_t op) {
+  Inproc* P = static_cast<Inproc*>(user);
+  const size_t esz = 8;
+  std::vector<char> mine((char*)buf, (char*)buf + esz * n);
+  P->in[rank] = mine.data();
+  if (!P->barrier()) return 1;
+  for (int32_t k = 0; k < n; ++k) {  // rank order: deterministic
+    if (dtype == 0) {
+      double acc = reinterpret_cast<const double*>(P->in[0])[k];
+      for (int g = 1; g < P->world; ++g) {
+        const double v = reinterpret_cast<const double*>(P->in[g])[k];
+        acc = op == 0 ? acc + v : (v > acc ? v : acc);
+      }
+      reinterpret_cast<double*>(buf)[k] = acc;
+    } else {
+      long long acc = reinterpret_cast<const long long*>(P->in[0])[k];
+      for (int g = 1; g < P->world; ++g) {
+        const long long v = reinterpret_cast<const long long*>(P->in[g])[k];
+        acc = op == 0 ? acc + v : (v > acc ? v : acc);
+      }
+      reinterpret_cast<long long*>(buf)[k] = acc;
+    }
+  }
+  return P->barrier() ? 0 : 1;
+}
+
+int ip_allgather(void* user, int32_t rank, const void* send, void* recv, size_t bytes) {
+  Inproc* P = static_cast<Inproc*>(user);
+  P->in[rank] = send;
+  if (!P->barrier()) return 1;
+  for (int g = 0; g < P->world; ++g) memcpy((char*)recv + g * bytes, P->in[g], bytes);
+  return P->barrier() ? 0 : 1;
+}
+
+int ip_alltoallv(void* user, int32_t rank, const void* const* send, const size_t* send_bytes,
+                 void* const* recv, const size_t* recv_bytes) {
+  Inproc* P = static_cast<Inproc*>(user);
+  P->in[rank] = send;
+  P->in_sizes[rank] = send_bytes;
+  if (!P->barrier()) return 1;
+  for (int g = 0; g < P->world; ++g) {
+    const void* const* theirs = reinterpret_cast<const void* const*>(P->in[g]);
+    const size_t nb = P->in_sizes[g][rank];
+    if (nb != recv_bytes[g]) return 2;
+    if (nb) memcpy(recv[g], theirs[rank], nb);
+  }
+  return P->barrier() ? 0 : 1;
+}
+
+}  // namespace
+
+extern "C" {
+
+mcs_status mcs_nccl_unique_id(void* out128) {
+  NcclApi* a = nccl();
+  if (!a || !out128) return MCS_E_NCCL;
+  NcclId id;
+  if (a->GetUniqueId(&id) != 0) return MCS_E_NCCL;
+  memcpy(out128, &id, sizeof(id));
+  return MCS_OK;
+}
+
+mcs_transport* mcs_inproc_transport_create(int32_t world) {
+  if (world < 1) return nullptr;
+  Inproc* P = new Inproc();
+  P->world = world;
+  P->in.assign(world, nullptr);
+  P->in_sizes.assign(world, nullptr);
+  P->t.user = P;
+  P->t.allreduce = ip_allreduce;
+  P->t.allgather = ip_allgather;
+  P->t.alltoallv = ip_alltoallv;
+  return &P->t;
+}
+
+void mcs_inproc_transport_destroy(mcs_transport* t) {
+  if (t) delete static_cast<Inproc*>(t->user);
+}
+
+}  // extern "C"
+
+namespace mcs {
+
+mcs_status dist_init(mcs_ctx* c, std::string& err) {
+  c->world = c->cfg.world_size;
+  c->rank = c->cfg.rank;
+  // world_size 1 with a transport or an NCCL id still runs the exchange path (tests of it)
+  if (c->world == 1 && !c->cfg.transport && !c->cfg.nccl_unique_id) return MCS_OK;
+  if (c->cfg.transport) {
+    c->tr = c->cfg.transport;
+    return MCS_OK;
+  }
+  NcclApi* a = nccl();
+  if (!a) {
+    err = "world_size > 1 needs libnccl.so.2 (dlopen failed) or a host transport";
+    return MCS_E_NCCL;
+  }
+  NcclId id;
+  memcpy(&id, c->cfg.nccl_unique_id, sizeof(id));
+  NcclComm comm = nullptr;
+  const int r = a->CommInitRank(&comm, c->world, id, c->rank);
+  if (r != 0) {
+    err = std::string("ncclCommInitRank: ") + (a->GetErrorString ? a->GetErrorString(r) : "?");
+    return MCS_E_NCCL;
+  }
+  c->nccl_comm = comm;
+  return MCS_OK;
+}
+
+void dist_destroy(mcs_ctx* c) {
+  if (c->nccl_comm) {
+    NcclApi* a = nccl();
+    if (a && a->CommDestroy) a->CommDestroy(c->nccl_comm);
+    c->nccl_comm = nullptr;
+  }
+}
+
+static mcs_status stage(mcs_ctx* c, size_t bytes) {
+  if (c->h_stage_bytes >= bytes) return MCS_OK;
+  if (c->h_stage) cudaFreeHost(c->h_stage);
+  c->h_stage = nullptr;
+  c->h_stage_bytes = 0;
+  if (cudaMallocHost(&c->h_stage, bytes) != cudaSuccess) return MCS_E_OUT_OF_MEMORY;
+  c->h_stage_bytes = bytes;
+  return MCS_OK;
+}
+
+bool dist_active(const mcs_ctx* c) { return c->world > 1 || c->tr || c->nccl_comm; }
+
+mcs_status dist_allreduce_f64(mcs_ctx* c, double* d_buf, int n, int op) {
+  if (!dist_active(c)) return MCS_OK;
+  if (c->nccl_comm) {
+    NcclApi* a = nccl();
+    return a->AllReduce(d_buf, d_buf, n, kNcclFloat64, op ? kNcclMax : kNcclSum, c->nccl_comm,
+                        c->stream) == 0 ? MCS_OK : MCS_E_NCCL;
+  }
+  if (stage(c, 8 * n) != MCS_OK) return MCS_E_OUT_OF_MEMORY;
+  if (cudaMemcpyAsync(c->h_stage, d_buf, 8 * n, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess ||
+      cudaStreamSynchronize(c->stream) != cudaSuccess)
+    return MCS_E_CUDA;
+  if (c->tr->allreduce(c->tr->user, c->rank, c->h_stage, n, 0, op)) return MCS_E_NCCL;
+  if (cudaMemcpyAsync(d_buf, c->h_stage, 8 * n, cudaMemcpyHostToDevice, c->stream) != cudaSuccess ||
+      cudaStreamSynchronize(c->stream) != cudaSuccess)
+    return MCS_E_CUDA;
+  return MCS_OK;
+}
+
+mcs_status dist_allgather_host(mcs_ctx* c, const void* send, void* recv, size_t bytes) {
+  if (!dist_active(c)) {
+    memcpy(recv, send, bytes);
+    return MCS_OK;
+  }
+  if (c->nccl_comm) {
+    NcclApi* a = nccl();
+    char* d = nullptr;
+    if (cudaMalloc(&d, bytes * (c->world + 1)) != cudaSuccess) return MCS_E_OUT_OF_MEMORY;
+    mcs_status st = MCS_OK;
+    if (cudaMemcpyAsync(d, send, bytes, cudaMemcpyHostToDevice, c->stream) != cudaSuccess)
+      st = MCS_E_CUDA;
+    if (st == MCS_OK &&
+        a->AllGather(d, d + bytes, bytes, kNcclUint8, c->nccl_comm, c->stream) != 0)
+      st = MCS_E_NCCL;
+    if (st == MCS_OK && (cudaMemcpyAsync(recv, d + bytes, bytes * c->world, cudaMemcpyDeviceToHost,
+                                         c->stream) != cudaSuccess ||
+                         cudaStreamSynchronize(c->stream) != cudaSuccess))
+      st = MCS_E_CUDA;
+    cudaFree(d);
+    return st;
+  }
+  return c->tr->allgather(c->tr->user, c->rank, send, recv, bytes) ? MCS_E_NCCL : MCS_OK;
+}
+
+mcs_status dist_alltoallv(mcs_ctx* c, const float* d_send, const size_t* send_bytes,
+                          const size_t* send_off, float* d_recv, const size_t* recv_bytes,
+                          const size_t* recv_off) {
+  if (!dist_active(c)) return MCS_OK;
+  const int G = c->world;
+  if (c->nccl_comm) {
+    NcclApi* a = nccl();
+    if (a->GroupStart() != 0) return MCS_E_NCCL;
+    for (int p = 0; p < G; ++p) {
+      if (p == c->rank) continue;
+      if (send_bytes[p] &&
+          a->Send((const char*)d_send + send_off[p], send_bytes[p], kNcclUint8, p, c->nccl_comm,
+                  c->stream) != 0)
+        return MCS_E_NCCL;
+      if (recv_bytes[p] &&
+          a->Recv((char*)d_recv + recv_off[p], recv_bytes[p], kNcclUint8, p, c->nccl_comm,
+                  c->stream) != 0)
+        return MCS_E_NCCL;
+    }
+    return a->GroupEnd() == 0 ? MCS_OK : MCS_E_NCCL;
+  }
+  size_t ts = send_off[G], tr = recv_off[G];
+  if (stage(c, ts + tr + 16) != MCS_OK) return MCS_E_OUT_OF_MEMORY;
+  char* hs = (char*)c->h_stage;
+  char* hr = hs + ts;
+  if ((ts && cudaMemcpyAsync(hs, d_send, ts, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess) ||
+      cudaStreamSynchronize(c->stream) != cudaSuccess)
+    return MCS_E_CUDA;
+  std::vector<const void*> sp(G);
+  std::vector<void*> rp(G);
+  for (int p = 0; p < G; ++p) {
+    sp[p] = hs + send_off[p];
+    rp[p] = hr + recv_off[p];
+  }
+  if (c->tr->alltoallv(c->tr->user, c->rank, sp.data(), send_bytes, rp.data(), recv_bytes))
+    return MCS_E_NCCL;
+  if ((tr && cudaMemcpyAsync(d_recv, hr, tr, cudaMemcpyHostToDevice, c->stream) != cudaSuccess) ||
+      cudaStreamSynchronize(c->stream) != cudaSuccess)
+    return MCS_E_CUDA;
+  return MCS_OK;
+}
+
+}  // namespace mcs

@@ -63,15 +63,22 @@ struct KfHost {
 };
 
 struct Scalars {                // device-side reduction results of one update
-  double m;                     // max_i L_i (after L += l)
-  double lstar;                 // max_i l_i
-  double S;                     // sum_i exp(L_i - m)
-  unsigned long long Q;         // survivor ladder total
-  long long D;                  // dead count
-  double m2, S2;                // after respawn
-  int32_t rep;                  // representative (global index)
+  double m;                     // max_i L_i (after L += l)            } exchanged together
+  double lstar;                 // max_i l_i                           } (allreduce MAX)
+  double S;                     // sum_i exp(L_i - m)                    (allreduce SUM)
+  double m2;                    // after respawn                         (allreduce MAX)
+  double S2;                    //                                       (allreduce SUM)
+  unsigned long long Q;         // local survivor ladder total
+  long long D;                  // local dead count
+  unsigned long long Q_tot;     // global ladder total
+  long long D_tot;              // global dead count
+  unsigned long long q_off;     // ladder offset of this rank
+  long long d_off;              // dead-slot offset of this rank
+  long long clone_off;          // first global draw made by this rank's survivors
+  long long clones;             // number of draws made by this rank's survivors
+  double wbest;                 // best local weight, then global
+  long long rep;                // representative (global index)
   int32_t status;               // 0 ok, MCS_E_DEGENERATE
-  double wbest;
   unsigned int counter[8];      // last-block counters (reset by the last block)
 };
 
@@ -135,6 +142,22 @@ struct mcs_ctx {
   void* d_cub_temp = nullptr;
   size_t cub_temp_bytes = 0;
   int32_t capN = 0, capK = 0, capS = 0, nbcap = 0;
+
+  // multi-rank (world > 1): particle shards with global index = gbase + local index
+  int world = 1, rank = 0;
+  long long gbase = 0;
+  std::vector<long long> n_per_rank;
+  const mcs_transport* tr = nullptr;  // host transport, or
+  void* nccl_comm = nullptr;          // NCCL communicator (dlopen'ed libnccl)
+  int32_t* d_dead_list = nullptr;     // [Ncap] local dead slots, ascending
+  int32_t* d_donor_g = nullptr;       // [Ncap] global donor index or -1
+  long long* d_plan = nullptr;        // [5][world+1] d_offs, send_off, recv_off, kstart, sfirst
+  int32_t* d_pack_src = nullptr;      // [xfer_cap_items] local donors to pack, send order
+  float* d_send = nullptr;            // packed particle states to send / received
+  float* d_recv = nullptr;
+  size_t xfer_cap_items = 0;
+  void* h_stage = nullptr;            // pinned host staging for the host transport
+  size_t h_stage_bytes = 0;
 };
 
 namespace mcs {
@@ -158,12 +181,25 @@ void launch_combine(mcs_ctx* c, int S, bool eval_mode, double* slot_l, float* sl
                     float* slot_b6, int32_t* slot_n, int32_t* slot_kf, uint8_t* loop_out);
 // a4
 void launch_propagate(mcs_ctx* c, double D_now);
-// a5-a7; returns nothing, status in d_scal
-void launch_weights_resample(mcs_ctx* c, uint32_t U);
-// isolated respawn on caller arrays
-void launch_resample_only(mcs_ctx* c, const double* d_e, const uint8_t* d_dead, int n,
-                          uint32_t U, int32_t* d_donor);
+// a5-a7 (+ the exchange steps when world > 1); degenerate status in d_scal
+mcs_status launch_weights_resample(mcs_ctx* c, uint32_t U);
+// isolated respawn on caller arrays (single device)
+mcs_status launch_resample_only(mcs_ctx* c, const double* d_e, const uint8_t* d_dead, int n,
+                                uint32_t U, int32_t* d_donor);
 size_t cub_temp_needed(int n);
+
+// ---- multi-rank exchange (dist.cu); world == 1 => no-ops returning MCS_OK ----
+mcs_status dist_init(mcs_ctx* c, std::string& err);
+bool dist_active(const mcs_ctx* c);  // exchange path in use (world > 1, or a transport/NCCL)
+void dist_destroy(mcs_ctx* c);
+// in place on device doubles; op 0 = sum, 1 = max (stream-ordered; host transport syncs)
+mcs_status dist_allreduce_f64(mcs_ctx* c, double* d_buf, int n, int op);
+// host values gathered to host (small, synchronous)
+mcs_status dist_allgather_host(mcs_ctx* c, const void* send, void* recv, size_t bytes);
+// device buffers; byte counts per peer on the host
+mcs_status dist_alltoallv(mcs_ctx* c, const float* d_send, const size_t* send_bytes,
+                          const size_t* send_off, float* d_recv, const size_t* recv_bytes,
+                          const size_t* recv_off);
 size_t sort_temp_needed(int n, int capK);
 
 }  // namespace mcs

@@ -1,14 +1,20 @@
 // weights.cu — a5: importance weights (Eq.11) as a max-subtracted log-sum-exp in
 // fp64 (R22); a6: dead-particle pruning + respawn (R17-R21); a7: representative
-// (P:206).
+// (P:206).  Single device or one shard of a multi-GPU run.
 //
 //   m = max L (from a3), e_i = exp(L_i - m), S = sum e (fixed tree), w_i = e_i / S
 //   dead_i = (l_i - max l < rel_floor) or (w_i < posterior_floor)            (R17)
 //   survivors' rungs q_i = floor(e_i 2^32), dead rungs 0; C = inclusive scan (exact uint64)
 //   n(c) = clamp(ceil((c D 2^32 - U Q) / (Q 2^32)), 0, D)  in signed 128-bit  (R18)
-//   the r-th dead slot (ascending) takes donor min{j : n(C_j) > r}
+//   draw r is made by the survivor j with n(C_{j-1}) <= r < n(C_j) and fills the r-th dead slot
 //   clone T_t, every T_k and L (R19, R20); re-normalise; representative = argmax w, ties low.
+// Across ranks every quantity above is global: m, l*, S are all-reduced, the ladder offsets and
+// totals come from an allgather of (Q_g, D_g), and clones whose dead slot lives on another rank
+// travel as packed particle states.
 #include <cub/cub.cuh>
+
+#include <algorithm>
+#include <vector>
 
 #include "mcs_internal.cuh"
 #include "reduce.cuh"
@@ -84,11 +90,21 @@ __global__ void rung_from_inputs_kernel(const double* __restrict__ e,
   rung[i] = r;
 }
 
-__global__ void totals_kernel(const Rung* __restrict__ scan, int N, Scalars* sc) {
+// local totals; on a single device also the (trivial) global plan
+__global__ void totals_kernel(const Rung* __restrict__ scan, int N, int single, Scalars* sc) {
   const Rung last = scan[N - 1];
   sc->Q = last.C;
   sc->D = (long long)last.d;
-  sc->status = (last.d > 0 && last.C == 0ull) ? (int)MCS_E_DEGENERATE : 0;
+  if (single) {
+    const bool degenerate = last.d > 0 && last.C == 0ull;
+    sc->Q_tot = last.C;
+    sc->D_tot = (long long)last.d;
+    sc->q_off = 0;
+    sc->d_off = 0;
+    sc->clone_off = 0;
+    sc->clones = degenerate ? 0 : (long long)last.d;
+    sc->status = degenerate ? (int)MCS_E_DEGENERATE : 0;
+  }
 }
 
 __device__ __forceinline__ long long draws_below(unsigned long long c, long long D,
@@ -102,30 +118,60 @@ __device__ __forceinline__ long long draws_below(unsigned long long c, long long
   return (long long)q;
 }
 
-__global__ void ncum_kernel(const Rung* __restrict__ scan, int N, const Scalars* __restrict__ sc,
-                            unsigned int U, long long* __restrict__ ncum) {
+// n(C_i) on the GLOBAL ladder for every local particle; compacted list of local dead slots
+__global__ void ncum_dead_kernel(const Rung* __restrict__ scan, int N,
+                                 const Scalars* __restrict__ sc, unsigned int U,
+                                 long long* __restrict__ ncum, int32_t* __restrict__ dead_list,
+                                 int32_t* __restrict__ donor_local, int32_t* __restrict__ donor_g) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= N) return;
-  if (sc->D == 0 || sc->Q == 0) return;
-  ncum[i] = draws_below(scan[i].C, sc->D, sc->Q, U);
+  const Rung s = scan[i];
+  const Rung prev = i > 0 ? scan[i - 1] : Rung{0ull, 0u, 0u};
+  if (s.d != prev.d) dead_list[s.d - 1] = i;  // this particle is dead
+  donor_local[i] = -1;
+  if (donor_g) donor_g[i] = -1;
+  if (sc->D_tot == 0 || sc->Q_tot == 0) return;
+  ncum[i] = draws_below(sc->q_off + s.C, sc->D_tot, sc->Q_tot, U);
 }
 
-__global__ void assign_kernel(const Rung* __restrict__ rung, const Rung* __restrict__ scan, int N,
-                              const Scalars* __restrict__ sc,
-                              const long long* __restrict__ ncum, int32_t* __restrict__ donor) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= N) return;
-  if (!rung[i].d || sc->D == 0 || sc->Q == 0) {
-    donor[i] = -1;
-    return;
-  }
-  const long long r = (long long)scan[i].d - 1;  // rank among dead slots (ascending)
-  int lo = 0, hi = N - 1;                        // first j with ncum[j] > r
+// one thread per draw made by this rank's survivors: find the donor (binary search on the
+// monotone n(C)), then either record a local clone or queue the donor for a remote rank.
+// plan (world > 1): [0..G] dead offsets, [G+1..2G+1] send item offsets, [4(G+1)..] first draw
+// sent to each peer.
+__global__ void draws_kernel(const long long* __restrict__ ncum, int N,
+                             const Scalars* __restrict__ sc, int world, int me, long long gbase,
+                             const long long* __restrict__ plan,
+                             const int32_t* __restrict__ dead_list,
+                             int32_t* __restrict__ donor_local, int32_t* __restrict__ donor_g,
+                             int32_t* __restrict__ pack_src) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= sc->clones) return;
+  const long long R = sc->clone_off + t;
+  int lo = 0, hi = N - 1;  // first j with ncum[j] > R
   while (lo < hi) {
     const int mid = (lo + hi) >> 1;
-    if (ncum[mid] > r) hi = mid; else lo = mid + 1;
+    if (ncum[mid] > R) hi = mid; else lo = mid + 1;
   }
-  donor[i] = lo;
+  const int j = lo;
+  int dst = me;
+  if (world > 1) {
+    const long long* doffs = plan;
+    int a = 0, b = world - 1;  // last rank with doffs[rank] <= R
+    while (a < b) {
+      const int mid = (a + b + 1) >> 1;
+      if (doffs[mid] <= R) a = mid; else b = mid - 1;
+    }
+    dst = a;
+  }
+  if (dst == me) {
+    const int slot = dead_list[R - sc->d_off];
+    donor_local[slot] = j;
+    if (donor_g) donor_g[slot] = (int32_t)(gbase + j);
+  } else {
+    const long long* send_off = plan + (world + 1);
+    const long long* sfirst = plan + 4 * (world + 1);
+    pack_src[send_off[dst] + (R - sfirst[dst])] = j;
+  }
 }
 
 __global__ void clone_kernel(const int32_t* __restrict__ donor, int N, int K, int capK, int capN,
@@ -147,6 +193,62 @@ __global__ void clone_kernel(const int32_t* __restrict__ donor, int N, int K, in
     dst[0] = src[0];
     dst[1] = src[1];
     dst[2] = src[2];
+  }
+}
+
+// packed particle state: [pose 12][K keyframe poses x 12][L (2 words)][global donor (2 words)]
+__host__ __device__ inline int state_floats(int K) { return 12 + 12 * K + 4; }
+
+__global__ void pack_kernel(const int32_t* __restrict__ pack_src, long long n_items, int K,
+                            int capK, int capN, long long gbase, const float* __restrict__ pose,
+                            const float* __restrict__ kfpose, const double* __restrict__ L,
+                            float* __restrict__ out) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const int KK = K + 1;
+  if (t >= n_items * KK) return;
+  const long long it = t / KK;
+  const int k = (int)(t - it * KK);
+  const int j = pack_src[it];
+  float* o = out + it * state_floats(K);
+  if (k == K) {
+    for (int e = 0; e < 12; ++e) o[e] = pose[(size_t)e * capN + j];
+    double* od = reinterpret_cast<double*>(o + 12 + 12 * K);
+    od[0] = L[j];
+    long long* og = reinterpret_cast<long long*>(o + 12 + 12 * K + 2);
+    og[0] = gbase + j;
+  } else {
+    const float* src = kfpose + ((size_t)j * capK + k) * 12;
+    for (int e = 0; e < 12; ++e) o[12 + 12 * k + e] = src[e];
+  }
+}
+
+// plan: [2(G+1)..3(G+1)) recv item offsets, [3(G+1)..4(G+1)) first local dead index per source
+__global__ void unpack_kernel(const float* __restrict__ in, long long n_items, int K, int capK,
+                              int capN, int world, const long long* __restrict__ plan,
+                              const int32_t* __restrict__ dead_list, float* __restrict__ pose,
+                              float* __restrict__ kfpose, double* __restrict__ L,
+                              int32_t* __restrict__ donor_g) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const int KK = K + 1;
+  if (t >= n_items * KK) return;
+  const long long it = t / KK;
+  const int k = (int)(t - it * KK);
+  const long long* roff = plan + 2 * (world + 1);
+  const long long* kstart = plan + 3 * (world + 1);
+  int a = 0, b = world - 1;  // source rank: last with roff[src] <= it
+  while (a < b) {
+    const int mid = (a + b + 1) >> 1;
+    if (roff[mid] <= it) a = mid; else b = mid - 1;
+  }
+  const int slot = dead_list[kstart[a] + (it - roff[a])];
+  const float* s = in + it * state_floats(K);
+  if (k == K) {
+    for (int e = 0; e < 12; ++e) pose[(size_t)e * capN + slot] = s[e];
+    L[slot] = reinterpret_cast<const double*>(s + 12 + 12 * K)[0];
+    donor_g[slot] = (int32_t)reinterpret_cast<const long long*>(s + 12 + 12 * K + 2)[0];
+  } else {
+    float* dst = kfpose + ((size_t)slot * capK + k) * 12;
+    for (int e = 0; e < 12; ++e) dst[e] = s[12 + 12 * k + e];
   }
 }
 
@@ -200,7 +302,7 @@ __global__ void __launch_bounds__(kWT) weight_argmax_kernel(const double* __rest
                                                             double* __restrict__ w,
                                                             double* __restrict__ pw,
                                                             int32_t* __restrict__ pi,
-                                                            Scalars* sc, int base_index,
+                                                            Scalars* sc, long long gbase,
                                                             unsigned int* counter) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   double wi = -INFINITY;
@@ -218,7 +320,7 @@ __global__ void __launch_bounds__(kWT) weight_argmax_kernel(const double* __rest
     for (int k = threadIdx.x; k < (int)gridDim.x; k += blockDim.x) better(bw, bi, pw[k], pi[k]);
     block_argmax(bw, bi);
     if (threadIdx.x == 0) {
-      sc->rep = base_index + bi;
+      sc->rep = gbase + bi;
       sc->wbest = bw;
     }
   }
@@ -230,45 +332,205 @@ size_t cub_temp_needed(int n) {
   return b;
 }
 
-static void ladder_and_assign(mcs_ctx* c, Rung* rung, int N, uint32_t U, int32_t* donor) {
-  cudaStream_t st = c->stream;
-  Rung* scan = reinterpret_cast<Rung*>(c->d_ladder_scan);
-  size_t tb = c->cub_temp_bytes;
-  cub::DeviceScan::InclusiveScan(c->d_cub_temp, tb, rung, scan, RungSum(), N, st);
-  const int g = (N + kWT - 1) / kWT;
-  totals_kernel<<<1, 1, 0, st>>>(scan, N, c->d_scal);
-  ncum_kernel<<<g, kWT, 0, st>>>(scan, N, c->d_scal, U, c->d_ncum);
-  assign_kernel<<<g, kWT, 0, st>>>(rung, scan, N, c->d_scal, c->d_ncum, donor);
+#define MCS_TRY(x)                    \
+  do {                                \
+    const mcs_status _s = (x);        \
+    if (_s != MCS_OK) return _s;      \
+  } while (0)
+#define MCS_CUDA(x)                                  \
+  do {                                               \
+    if ((x) != cudaSuccess) return MCS_E_CUDA;       \
+  } while (0)
+
+// Global respawn plan for world > 1: allgather (Q_g, D_g), plan on the host, upload.
+static mcs_status plan_global(mcs_ctx* c, uint32_t U, long long* n_send_items,
+                              long long* n_recv_items, std::vector<size_t>& sb,
+                              std::vector<size_t>& so, std::vector<size_t>& rb,
+                              std::vector<size_t>& ro) {
+  const int G = c->world, me = c->rank;
+  long long mine[2];
+  MCS_CUDA(cudaMemcpyAsync(mine, &c->d_scal->Q, 16, cudaMemcpyDeviceToHost, c->stream));
+  MCS_CUDA(cudaStreamSynchronize(c->stream));
+  std::vector<long long> all(2 * G);
+  MCS_TRY(dist_allgather_host(c, mine, all.data(), 16));
+  std::vector<uint64_t> Q(G);
+  std::vector<int64_t> D(G), qoff(G), clones(G), send((size_t)G * G);
+  std::vector<uint64_t> qo(G);
+  for (int g = 0; g < G; ++g) {
+    Q[g] = (uint64_t)all[2 * g];
+    D[g] = all[2 * g + 1];
+  }
+  uint64_t Qt = 0;
+  int64_t Dt = 0;
+  std::vector<int64_t> doff(G);
+  const mcs_status st = mcs_plan_ladder(G, Q.data(), D.data(), U, qo.data(), doff.data(),
+                                        clones.data(), &Qt, &Dt);
+  if (st != MCS_OK && st != MCS_E_DEGENERATE) return st;
+  if (st == MCS_E_DEGENERATE)
+    for (auto& x : clones) x = 0;
+  if (st == MCS_OK || st == MCS_E_DEGENERATE) {
+    if (st == MCS_OK) MCS_TRY(mcs_plan_migration(G, clones.data(), D.data(), send.data()));
+  }
+  std::vector<long long> coff(G + 1, 0), doffs(G + 1, 0);
+  for (int g = 0; g < G; ++g) {
+    coff[g + 1] = coff[g] + clones[g];
+    doffs[g + 1] = doffs[g] + D[g];
+  }
+  // plan table: [0] dead offsets, [1] send item offsets, [2] recv item offsets,
+  //             [3] first local dead index per source, [4] first draw sent per destination
+  std::vector<long long> plan(5 * (G + 1), 0);
+  for (int g = 0; g <= G; ++g) plan[g] = doffs[g];
+  long long s = 0, r = 0;
+  sb.assign(G, 0);
+  rb.assign(G, 0);
+  so.assign(G + 1, 0);
+  ro.assign(G + 1, 0);
+  const size_t SB = sizeof(float) * 12 * (1 + c->K) + 16;
+  for (int p = 0; p < G; ++p) {
+    plan[(G + 1) + p] = s;
+    plan[2 * (G + 1) + p] = r;
+    const long long ns = (p == me || st != MCS_OK) ? 0 : send[(size_t)me * G + p];
+    const long long nr = (p == me || st != MCS_OK) ? 0 : send[(size_t)p * G + me];
+    plan[3 * (G + 1) + p] = std::max(coff[p], doffs[me]) - doffs[me];
+    plan[4 * (G + 1) + p] = std::max(coff[me], doffs[p]);
+    sb[p] = (size_t)ns * SB;
+    rb[p] = (size_t)nr * SB;
+    so[p] = (size_t)s * SB;
+    ro[p] = (size_t)r * SB;
+    s += ns;
+    r += nr;
+  }
+  plan[(G + 1) + G] = s;
+  plan[2 * (G + 1) + G] = r;
+  so[G] = (size_t)s * SB;
+  ro[G] = (size_t)r * SB;
+  *n_send_items = s;
+  *n_recv_items = r;
+  // scalars Q_tot .. clones are contiguous in Scalars
+  const long long host_sc[6] = {(long long)Qt, (long long)Dt, (long long)qo[me], (long long)doff[me],
+                                coff[me], st == MCS_OK ? (long long)clones[me] : 0};
+  MCS_CUDA(cudaMemcpyAsync(&c->d_scal->Q_tot, host_sc, sizeof(host_sc), cudaMemcpyHostToDevice,
+                           c->stream));
+  const int status = st == MCS_E_DEGENERATE ? (int)MCS_E_DEGENERATE : 0;
+  MCS_CUDA(cudaMemcpyAsync(&c->d_scal->status, &status, sizeof(int), cudaMemcpyHostToDevice,
+                           c->stream));
+  MCS_CUDA(cudaMemcpyAsync(c->d_plan, plan.data(), sizeof(long long) * plan.size(),
+                           cudaMemcpyHostToDevice, c->stream));
+  MCS_CUDA(cudaStreamSynchronize(c->stream));  // host arrays above go out of scope
+  return MCS_OK;
 }
 
-void launch_weights_resample(mcs_ctx* c, uint32_t U) {
+static mcs_status ensure_xfer(mcs_ctx* c, long long items) {
+  if ((size_t)items <= c->xfer_cap_items) return MCS_OK;
+  cudaFree(c->d_send);
+  cudaFree(c->d_recv);
+  cudaFree(c->d_pack_src);
+  c->d_send = c->d_recv = nullptr;
+  c->d_pack_src = nullptr;
+  const size_t cap = (size_t)items + (items >> 2) + 1024;
+  const size_t bytes = cap * (sizeof(float) * 12 * (1 + c->capK) + 16);
+  if (cudaMalloc(&c->d_send, bytes) != cudaSuccess || cudaMalloc(&c->d_recv, bytes) != cudaSuccess ||
+      cudaMalloc(&c->d_pack_src, sizeof(int32_t) * cap) != cudaSuccess)
+    return MCS_E_OUT_OF_MEMORY;
+  c->xfer_cap_items = cap;
+  return MCS_OK;
+}
+
+mcs_status launch_weights_resample(mcs_ctx* c, uint32_t U) {
   cudaStream_t st = c->stream;
   const int N = c->N;
   const int g = (N + kWT - 1) / kWT;
+  const bool single = !dist_active(c);
   Scalars* sc = c->d_scal;
   double* p0 = c->d_partials;
-  // a5: e = exp(L - m), S   (m, l* reduced by a3)
+  // a5: m and l* (reduced locally by a3) are global maxima across ranks
+  MCS_TRY(dist_allreduce_f64(c, &sc->m, 2, 1));
   exp_sum_kernel<<<g, kWT, 0, st>>>(c->d_L, N, &sc->m, c->d_e, p0, &sc->S, &sc->counter[1]);
-  // a6: dead set, ladder, counts, donors, clones
+  MCS_TRY(dist_allreduce_f64(c, &sc->S, 1, 0));
+  // a6: dead set and the survivor ladder
   Rung* rung = reinterpret_cast<Rung*>(c->d_ladder);
+  Rung* scan = reinterpret_cast<Rung*>(c->d_ladder_scan);
   dead_kernel<<<g, kWT, 0, st>>>(c->d_e, c->d_l, N, sc, c->cfg.loglik_rel_floor,
                                  c->cfg.posterior_floor, c->d_w, c->d_flags, rung);
-  ladder_and_assign(c, rung, N, U, c->d_donor);
+  size_t tb = c->cub_temp_bytes;
+  MCS_CUDA(cub::DeviceScan::InclusiveScan(c->d_cub_temp, tb, rung, scan, RungSum(), N, st));
+  totals_kernel<<<1, 1, 0, st>>>(scan, N, single ? 1 : 0, sc);
+  long long n_send = 0, n_recv = 0, n_draws_bound = N;
+  std::vector<size_t> sb, so, rb, ro;
+  if (!single) {
+    MCS_TRY(plan_global(c, U, &n_send, &n_recv, sb, so, rb, ro));
+    long long h_clones = 0;
+    MCS_CUDA(cudaMemcpy(&h_clones, &sc->clones, sizeof(long long), cudaMemcpyDeviceToHost));
+    n_draws_bound = h_clones;
+    MCS_TRY(ensure_xfer(c, std::max(n_send, n_recv)));
+  }
+  ncum_dead_kernel<<<g, kWT, 0, st>>>(scan, N, sc, U, c->d_ncum, c->d_dead_list, c->d_donor,
+                                      c->d_donor_g);
+  if (n_draws_bound > 0)
+    draws_kernel<<<(int)((n_draws_bound + kWT - 1) / kWT), kWT, 0, st>>>(
+        c->d_ncum, N, sc, c->world, c->rank, c->gbase, c->d_plan, c->d_dead_list, c->d_donor,
+        c->d_donor_g, c->d_pack_src);
+  if (!single && n_send > 0) {
+    const long long tot = n_send * (c->K + 1);
+    pack_kernel<<<(int)((tot + 255) / 256), 256, 0, st>>>(c->d_pack_src, n_send, c->K, c->capK,
+                                                          c->capN, c->gbase, c->d_pose,
+                                                          c->d_kfpose, c->d_L, c->d_send);
+  }
   const long long tot = (long long)N * (c->K + 1);
   clone_kernel<<<(int)((tot + 255) / 256), 256, 0, st>>>(c->d_donor, N, c->K, c->capK, c->capN,
                                                          c->d_pose, c->d_kfpose, c->d_L);
-  // re-normalise on the new L, then a7
+  if (!single) {
+    MCS_TRY(dist_alltoallv(c, c->d_send, sb.data(), so.data(), c->d_recv, rb.data(), ro.data()));
+    if (n_recv > 0) {
+      const long long tr = n_recv * (c->K + 1);
+      unpack_kernel<<<(int)((tr + 255) / 256), 256, 0, st>>>(
+          c->d_recv, n_recv, c->K, c->capK, c->capN, c->world, c->d_plan, c->d_dead_list,
+          c->d_pose, c->d_kfpose, c->d_L, c->d_donor_g);
+    }
+  }
+  // re-normalise on the new L (global max and sum), then a7
   max_kernel<<<g, kWT, 0, st>>>(c->d_L, N, p0, &sc->m2, &sc->counter[2]);
+  MCS_TRY(dist_allreduce_f64(c, &sc->m2, 1, 1));
   exp_sum_kernel<<<g, kWT, 0, st>>>(c->d_L, N, &sc->m2, c->d_e, p0, &sc->S2, &sc->counter[3]);
+  MCS_TRY(dist_allreduce_f64(c, &sc->S2, 1, 0));
   weight_argmax_kernel<<<g, kWT, 0, st>>>(c->d_e, N, &sc->S2, c->d_w, p0, c->d_ipartials, sc,
-                                          c->cfg.rank * 0, &sc->counter[4]);
+                                          c->gbase, &sc->counter[4]);
+  if (!single) {  // representative: best (w, global index) over ranks, ties -> lowest index
+    double mine[2];
+    MCS_CUDA(cudaMemcpyAsync(&mine[0], &sc->wbest, 8, cudaMemcpyDeviceToHost, st));
+    MCS_CUDA(cudaMemcpyAsync(&mine[1], &sc->rep, 8, cudaMemcpyDeviceToHost, st));
+    MCS_CUDA(cudaStreamSynchronize(st));
+    std::vector<double> all(2 * c->world);
+    MCS_TRY(dist_allgather_host(c, mine, all.data(), 16));
+    double bw = -INFINITY;
+    long long bi = 0x7fffffffffffffffLL;
+    for (int r = 0; r < c->world; ++r) {
+      long long ri;
+      memcpy(&ri, &all[2 * r + 1], 8);
+      if (all[2 * r] > bw || (all[2 * r] == bw && ri < bi)) { bw = all[2 * r]; bi = ri; }
+    }
+    MCS_CUDA(cudaMemcpyAsync(&sc->rep, &bi, 8, cudaMemcpyHostToDevice, st));
+    MCS_CUDA(cudaMemcpyAsync(&sc->wbest, &bw, 8, cudaMemcpyHostToDevice, st));
+    MCS_CUDA(cudaStreamSynchronize(st));
+  }
+  return cudaGetLastError() == cudaSuccess ? MCS_OK : MCS_E_CUDA;
 }
 
-void launch_resample_only(mcs_ctx* c, const double* d_e, const uint8_t* d_dead, int n,
-                          uint32_t U, int32_t* d_donor) {
+mcs_status launch_resample_only(mcs_ctx* c, const double* d_e, const uint8_t* d_dead, int n,
+                                uint32_t U, int32_t* d_donor) {
+  cudaStream_t st = c->stream;
   Rung* rung = reinterpret_cast<Rung*>(c->d_ladder);
-  rung_from_inputs_kernel<<<(n + kWT - 1) / kWT, kWT, 0, c->stream>>>(d_e, d_dead, n, rung);
-  ladder_and_assign(c, rung, n, U, d_donor);
+  Rung* scan = reinterpret_cast<Rung*>(c->d_ladder_scan);
+  const int g = (n + kWT - 1) / kWT;
+  rung_from_inputs_kernel<<<g, kWT, 0, st>>>(d_e, d_dead, n, rung);
+  size_t tb = c->cub_temp_bytes;
+  MCS_CUDA(cub::DeviceScan::InclusiveScan(c->d_cub_temp, tb, rung, scan, RungSum(), n, st));
+  totals_kernel<<<1, 1, 0, st>>>(scan, n, 1, c->d_scal);
+  ncum_dead_kernel<<<g, kWT, 0, st>>>(scan, n, c->d_scal, U, c->d_ncum, c->d_dead_list, d_donor,
+                                      nullptr);
+  draws_kernel<<<g, kWT, 0, st>>>(c->d_ncum, n, c->d_scal, 1, 0, 0, nullptr, c->d_dead_list,
+                                  d_donor, nullptr, nullptr);
+  return cudaGetLastError() == cudaSuccess ? MCS_OK : MCS_E_CUDA;
 }
 
 }  // namespace mcs

@@ -52,6 +52,7 @@ class Config(C.Structure):
         ("rank", C.c_int32),
         ("world_size", C.c_int32),
         ("nccl_unique_id", C.c_void_p),
+        ("transport", C.c_void_p),
     ]
 
 
@@ -94,6 +95,9 @@ def load() -> C.CDLL:
         "mcs_set_profiling": (st, [vp, i32]),
         "mcs_get_phase_ms": (st, [vp, vp]),
         "mcs_plan_ladder": (st, [i32, vp, vp, u32, vp, vp, vp, vp, vp]),
+        "mcs_nccl_unique_id": (st, [vp]),
+        "mcs_inproc_transport_create": (vp, [i32]),
+        "mcs_inproc_transport_destroy": (None, [vp]),
         "mcs_plan_migration": (st, [i32, vp, vp, vp]),
     }
     for name, (res, args) in sig.items():
@@ -149,6 +153,16 @@ class Context:
     def __init__(self, capacity_particles: int, capacity_keyframes: int,
                  capacity_scan_points: int, **cfg_kw):
         self._lib = load()
+        self._keep = []
+        tr = cfg_kw.pop("transport", None)
+        nid = cfg_kw.pop("nccl_unique_id", None)
+        if tr is not None:
+            cfg_kw["transport"] = tr.ptr if isinstance(tr, InprocTransport) else tr
+            self._keep.append(tr)
+        if nid is not None:
+            idbuf = C.create_string_buffer(bytes(nid), 128)
+            self._keep.append(idbuf)
+            cfg_kw["nccl_unique_id"] = C.cast(idbuf, C.c_void_p)
         self.cfg = default_config(capacity_particles=capacity_particles,
                                   capacity_keyframes=capacity_keyframes,
                                   capacity_scan_points=capacity_scan_points, **cfg_kw)
@@ -302,6 +316,34 @@ class Context:
         self._check(self._lib.mcs_get_phase_ms(self._ctx, ms))
         return {"select": ms[0], "sweep": ms[1], "update": ms[2], "weights": ms[3],
                 "total": ms[4]}
+
+
+def nccl_unique_id() -> bytes:
+    """A fresh 128-byte ncclUniqueId (rank 0 creates it; broadcast it to the other ranks)."""
+    buf = C.create_string_buffer(128)
+    st = load().mcs_nccl_unique_id(buf)
+    if st:
+        raise MCSError(st, "libnccl.so.2 unavailable")
+    return buf.raw
+
+
+class InprocTransport:
+    """In-process transport joining `world` contexts (one thread per rank) on one device."""
+
+    def __init__(self, world: int):
+        self.world = world
+        self.ptr = load().mcs_inproc_transport_create(int(world))
+
+    def close(self):
+        if self.ptr:
+            load().mcs_inproc_transport_destroy(self.ptr)
+            self.ptr = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def plan_ladder(Q_per_rank, D_per_rank, u: int):
