@@ -9,9 +9,10 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 VARIANTS = {
-    "sync_v5": [],
-    "sync_v5_t64": ["MCS_SWEEP_THREADS=64"],
-    "sync_v5_c128": ["MCS_SWEEP_CHUNK=128"],
+    "base": [],
+    "masked": ["MCS_SWEEP_MASKED"],
+    "masked_t64": ["MCS_SWEEP_MASKED", "MCS_SWEEP_THREADS=64"],
+    "masked_mb5": ["MCS_SWEEP_MASKED", "MCS_SWEEP_MINBLOCKS=5"],
 }
 OUT = os.path.join(ROOT, "bench", "_variants")
 

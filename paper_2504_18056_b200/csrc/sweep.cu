@@ -45,24 +45,6 @@ __device__ __forceinline__ float rcp_approx(float x) {
   return r;
 }
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  const unsigned int sa = (unsigned int)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() {
-  asm volatile("cp.async.commit_group;\n" ::: "memory");
-}
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
-}
-
-#ifndef MCS_SWEEP_DEPTH
-#define MCS_SWEEP_DEPTH 3
-#endif
-constexpr int kDepth = MCS_SWEEP_DEPTH;      // probes in flight per thread
-constexpr int kStages = kDepth + 1;          // ring of per-thread staging slots in smem
-
 __device__ __forceinline__ void ld_slot(const float4* sl, float4& s0, float4& s1, float4& s2) {
   asm volatile("ld.global.nc.v4.f32 {%0, %1, %2, %3}, [%4];"
                : "=f"(s0.x), "=f"(s0.y), "=f"(s0.z), "=f"(s0.w) : "l"(sl));
@@ -82,10 +64,6 @@ __global__ void __launch_bounds__(kSweepThreads, MCS_SWEEP_MINBLOCKS)
                  int n_items, const float4* __restrict__ scan, int S,
                  const KfMeta* __restrict__ kmeta, float inv_r, float* __restrict__ part) {
   __shared__ float4 s_pt[kChunk * 3];
-#ifdef MCS_SWEEP_ASYNC
-  // per-thread probe staging: [stage][0..2 = slot float4s, 3 = {q, key}][thread]
-  __shared__ float4 s_stage[kStages][4][kSweepThreads];
-#endif
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   const int item = t < n_items ? order[t] : -1;
   float4 r0 = make_float4(0, 0, 0, 0), r1 = r0, r2 = r0, inf = r0;
@@ -246,7 +224,6 @@ __global__ void __launch_bounds__(kSweepThreads, MCS_SWEEP_MINBLOCKS)
     for (int k = threadIdx.x; k < cnt * 3; k += kSweepThreads) s_pt[k] = scan[3 * base + k];
     __syncthreads();
     if (!active) continue;
-#ifndef MCS_SWEEP_ASYNC
     // two probe buffers in flight alternately: the slot of point j+1 is requested before the
     // math of point j (no register copies between iterations)
     Probe pa = issue(0), pb;
@@ -271,58 +248,6 @@ __global__ void __launch_bounds__(kSweepThreads, MCS_SWEEP_MINBLOCKS)
         if (probe_on(q)) accumulate(j + 1, q);
       }
     }
-#else
-    // kDepth probes in flight through cp.async into a per-thread smem ring: the slot copies
-    // never hold a register scoreboard, so the math of point j never waits on the loads of
-    // points j+1..j+kDepth.
-    const int tid = threadIdx.x;
-    auto stage_issue = [&](int j) {
-      const int st = j % kStages;
-      const float4 A = s_pt[3 * j];
-      const float qx = __fmaf_rn(R02, A.z, __fmaf_rn(R01, A.y, __fmaf_rn(R00, A.x, tx)));
-      const float qy = __fmaf_rn(R12, A.z, __fmaf_rn(R11, A.y, __fmaf_rn(R10, A.x, ty)));
-      const float qz = __fmaf_rn(R22, A.z, __fmaf_rn(R21, A.y, __fmaf_rn(R20, A.x, tz)));
-      const unsigned int dx =
-          (unsigned)__float_as_int(__fadd_rd(__fmul_rn(qx, inv_r), kMagic)) - offx;
-      const unsigned int dy =
-          (unsigned)__float_as_int(__fadd_rd(__fmul_rn(qy, inv_r), kMagic)) - offy;
-      const unsigned int dz =
-          (unsigned)__float_as_int(__fadd_rd(__fmul_rn(qz, inv_r), kMagic)) - offz;
-      const bool in = (dx < m.ex) & (dy < m.ey) & (dz < m.ez);
-      const unsigned int key = in ? local_key(dx, dy, dz) : kEmptyKey32;
-      const unsigned int hh = slot_hash(key, m.shift) & m.mask;
-      const float4* sl = m.slots + 4 * (size_t)hh;
-      cp_async16(&s_stage[st][0][tid], sl);
-      cp_async16(&s_stage[st][1][tid], sl + 1);
-      cp_async16(&s_stage[st][2][tid], sl + 2);
-      s_stage[st][3][tid] = make_float4(qx, qy, qz, __uint_as_float(key));
-    };
-#pragma unroll
-    for (int d = 0; d < kDepth; ++d) {
-      if (d < cnt) stage_issue(d);
-      cp_async_commit();
-    }
-    for (int j = 0; j < cnt; ++j) {
-      if (j + kDepth < cnt) stage_issue(j + kDepth);
-      cp_async_commit();
-      cp_async_wait<kDepth>();
-      const int st = j % kStages;
-      Probe p;
-      const float4 qk = s_stage[st][3][tid];
-      p.qx = qk.x;
-      p.qy = qk.y;
-      p.qz = qk.z;
-      p.key = __float_as_uint(qk.w);
-      p.h = slot_hash(p.key, m.shift) & m.mask;
-      p.s0 = s_stage[st][0][tid];
-      p.s1 = s_stage[st][1][tid];
-      p.s2 = s_stage[st][2][tid];
-      const int r = first_check(p);
-      if (r == 1) accumulate(j, p);
-      else if (r == 2 && probe_on(p)) accumulate(j, p);
-    }
-    cp_async_wait<0>();
-#endif
   }
   if (!active) return;
   float4* o = reinterpret_cast<float4*>(part + (size_t)item * kSlotFloats);
