@@ -101,6 +101,8 @@ typedef struct mcs_config {
   int32_t  rank, world_size;     /* particle shards (one process per GPU)                   */
   const void* nccl_unique_id;    /* 128-byte ncclUniqueId when world_size > 1, else NULL    */
   const mcs_transport* transport; /* host transport when world_size > 1 without NCCL        */
+  int32_t  gn_iterations;        /* GN steps per update, each a full a1-a4 pass (R12); 1        */
+  int32_t  weight_after_update;  /* 0: weight with the pre-update l (R13); 1: re-evaluate l   */
 } mcs_config;
 
 /* Fills *cfg with the defaults above (capacities 0: caller sets them). */
@@ -196,6 +198,23 @@ MCS_API mcs_status mcs_plan_ladder(int32_t world, const uint64_t* Q_per_rank,
                                    int64_t* D_total);
 MCS_API mcs_status mcs_plan_migration(int32_t world, const int64_t* clones_per_rank,
                                       const int64_t* dead_per_rank, int64_t* send_counts);
+
+/* Prediction step (Eq.1): for every local particle i (global index g),
+ *   T_t^i = T_{t-1}^i dT exp(delta_i),  delta_i = chol(cov) z,  z ~ N(0, I)
+ * with z from Philox4x32-10 keyed by seed, counter (block, g, frame), and fp64 Box-Muller
+ * (R31).  dT12: odometry relative motion (pose12, host or device); cov36: 6x6 row-major SPD
+ * covariance of the twist (rho, phi) or all zeros.  vertical_sigma > 0 adds the elevator
+ * heuristic's world-frame vertical random walk t_z += vertical_sigma z_6.
+ * MCS_E_INVALID_ARG if cov is neither SPD nor zero. */
+MCS_API mcs_status mcs_predict(mcs_ctx* ctx, const float* dT12, const double* cov36,
+                               uint64_t seed, uint64_t frame, double vertical_sigma);
+
+/* Keyframe-insertion test: the fraction of scan points (mean3[n_pts][3]) whose
+ * cell, after the transform rel12 (T_kf^-1 T_now from odometry), is occupied in keyframe kf's
+ * voxel map (same pinned key path as the likelihood, R27).  Insert a keyframe when it falls
+ * below 0.7. */
+MCS_API mcs_status mcs_overlap(mcs_ctx* ctx, const float* scan_mean3, int32_t n_pts,
+                               const float* rel12, int32_t kf, double* out_rate);
 
 /* NCCL unique id (128 bytes) for mcs_config.nccl_unique_id; rank 0 creates it and the caller
  * broadcasts it (e.g. through torch.distributed).  MCS_E_NCCL if libnccl.so.2 is unavailable. */

@@ -49,14 +49,18 @@ class Config(C.Structure):
         ("unmatched_penalty", C.c_double),
         ("loglik_rel_floor", C.c_double),
         ("posterior_floor", C.c_double),
+        ("gn_iterations", C.c_int32),
+        ("weight_after_update", C.c_int32),
     ]
 
 
 def make_config(voxel_resolution=0.5, neighbor_count=3, loop_recency_gap=10, gn_slots=0,
                 damping_rel=1e-6, step_clamp=1.0, unmatched_penalty=0.0,
-                loglik_rel_floor=LN_1E16, posterior_floor=1e-8) -> Config:
+                loglik_rel_floor=LN_1E16, posterior_floor=1e-8, gn_iterations=1,
+                weight_after_update=0) -> Config:
     return Config(neighbor_count, loop_recency_gap, voxel_resolution, gn_slots, damping_rel,
-                  step_clamp, unmatched_penalty, loglik_rel_floor, posterior_floor)
+                  step_clamp, unmatched_penalty, loglik_rel_floor, posterior_floor,
+                  gn_iterations, weight_after_update)
 
 
 class ParticleOut(C.Structure):
@@ -116,6 +120,12 @@ def lib():
         L.orc_update.argtypes = [vp, i32, vp, vp, f64, i32, vp, vp, i32, vp, vp, vp, i32, u32, vp]
         L.orc_update.restype = C.c_int
         L.orc_num_threads.restype = C.c_int
+        L.orc_philox4x32_10.argtypes = [vp, vp, vp]
+        L.orc_normals8.argtypes = [C.c_uint64, C.c_uint64, C.c_int64, vp]
+        L.orc_predict.argtypes = [i32, vp, vp, vp, C.c_uint64, C.c_uint64, C.c_int64, f64]
+        L.orc_predict.restype = C.c_int
+        L.orc_overlap.argtypes = [vp, vp, i32, vp]
+        L.orc_overlap.restype = f64
     return _lib
 
 
@@ -293,6 +303,37 @@ def resample(e, dead_mask, U: int):
 def representative(w) -> int:
     w = _c(w, np.float64)
     return int(lib().orc_representative(len(w), _p(w)))
+
+
+def philox4x32_10(ctr, key):
+    c = _c(ctr, np.uint32)
+    k = _c(key, np.uint32)
+    out = np.zeros(4, np.uint32)
+    lib().orc_philox4x32_10(_p(c), _p(k), _p(out))
+    return out
+
+
+def normals8(seed: int, frame: int, gi: int):
+    z = np.zeros(8)
+    lib().orc_normals8(int(seed), int(frame), int(gi), _p(z))
+    return z
+
+
+def predict(pose12, dT12, cov36, seed: int, frame: int, gbase: int = 0, vertical_sigma=0.0):
+    """Eq.1 prediction, in place on pose12 (N, 12) fp32."""
+    assert pose12.dtype == np.float32 and pose12.flags.c_contiguous
+    dT = _c(np.asarray(dT12).reshape(12), np.float32)
+    cv = _c(np.asarray(cov36).reshape(36), np.float64)
+    rc = lib().orc_predict(len(pose12), _p(pose12), _p(dT), _p(cv), int(seed), int(frame),
+                           int(gbase), float(vertical_sigma))
+    if rc:
+        raise ValueError("covariance neither SPD nor zero")
+
+
+def overlap(m: "Map", mean3, rel32) -> float:
+    mean3 = _c(mean3, np.float32).reshape(-1, 3)
+    r = _c(np.asarray(rel32).reshape(12), np.float32)
+    return float(lib().orc_overlap(m.ptr, _p(mean3), len(mean3), _p(r)))
 
 
 class Keyframes:

@@ -762,9 +762,37 @@ int orc_update(const orc_config* cfg, int32_t K, orc_map* const* maps, const dou
   po.hess36 = out->hess36;
   po.psi6 = out->psi6;
   po.flags = out->flags;
-  int rc = orc_particles(cfg, K, maps, D, D_now, N, pose12, kf_pose12, kf_stride, scan_mean3,
-                         scan_cov6, S, NULL, N, 1, &po);
-  if (rc) return rc;
+  double* lw = (double*)malloc(sizeof(double) * (N > 0 ? N : 1));
+  /* steps 2-7, repeated gn_iterations times (R12); the weighting l is the pre-update l of the
+   * first iteration (R13) unless weight_after_update asks for a re-evaluation */
+  const int32_t iters = cfg->gn_iterations > 0 ? cfg->gn_iterations : 1;
+  int rc = 0;
+  for (int32_t it = 0; it < iters && rc == 0; ++it) {
+    rc = orc_particles(cfg, K, maps, D, D_now, N, pose12, kf_pose12, kf_stride, scan_mean3,
+                       scan_cov6, S, NULL, N, 1, &po);
+    if (it == 0) memcpy(lw, out->loglik, sizeof(double) * N);
+  }
+  if (rc == 0 && cfg->weight_after_update) {
+    orc_particle_out pe;
+    memset(&pe, 0, sizeof(pe));
+    pe.loglik = lw;
+    pe.grad6 = (double*)malloc(sizeof(double) * 6 * (size_t)N);
+    pe.hess36 = (double*)malloc(sizeof(double) * 36 * (size_t)N);
+    pe.psi6 = (double*)malloc(sizeof(double) * 6 * (size_t)N);
+    pe.flags = (uint8_t*)malloc(N);
+    rc = orc_particles(cfg, K, maps, D, D_now, N, pose12, kf_pose12, kf_stride, scan_mean3,
+                       scan_cov6, S, NULL, N, 0, &pe);
+    free(pe.grad6);
+    free(pe.hess36);
+    free(pe.psi6);
+    free(pe.flags);
+  }
+  if (rc) {
+    free(lw);
+    return rc;
+  }
+  memcpy(out->loglik, lw, sizeof(double) * N);
+  free(lw);
   double* e = (double*)malloc(sizeof(double) * N);
   uint8_t* dead = (uint8_t*)malloc(N);
   /* step 8: Eq.11 */
@@ -793,4 +821,106 @@ int orc_update(const orc_config* cfg, int32_t K, orc_map* const* maps, const dou
   free(e);
   free(dead);
   return rc;
+}
+
+/* ------------------------------------------------------------------------- */
+/* Philox4x32-10 (Salmon, Moraes, Dror, Shaw: "Parallel random numbers: as    */
+/* easy as 1, 2, 3", SC'11): 10 rounds of two 32x32->64 multiplies + Weyl key */
+/* ------------------------------------------------------------------------- */
+
+void orc_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]) {
+  uint32_t c0 = ctr[0], c1 = ctr[1], c2 = ctr[2], c3 = ctr[3];
+  uint32_t k0 = key[0], k1 = key[1];
+  for (int r = 0; r < 10; ++r) {
+    const uint64_t p0 = (uint64_t)0xD2511F53u * c0;
+    const uint64_t p1 = (uint64_t)0xCD9E8D57u * c2;
+    const uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
+    const uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+    const uint32_t n0 = hi1 ^ c1 ^ k0, n1 = lo1, n2 = hi0 ^ c3 ^ k1, n3 = lo0;
+    c0 = n0; c1 = n1; c2 = n2; c3 = n3;
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+  out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
+}
+
+/* 8 standard normals for particle gi: two Philox blocks -> 8 uniforms in (0, 1] -> 4 Box-Muller
+ * pairs, fp64 (R31) */
+void orc_normals8(uint64_t seed, uint64_t frame, int64_t gi, double z[8]) {
+  const uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+  uint32_t x[8];
+  for (uint32_t b = 0; b < 2; ++b) {
+    const uint32_t ctr[4] = {b, (uint32_t)gi, (uint32_t)frame, (uint32_t)(frame >> 32)};
+    orc_philox4x32_10(ctr, key, x + 4 * b);
+  }
+  for (int k = 0; k < 4; ++k) {
+    const double u1 = ((double)x[2 * k] + 1.0) * 0x1.0p-32;
+    const double u2 = ((double)x[2 * k + 1] + 1.0) * 0x1.0p-32;
+    const double rr = sqrt(-2.0 * log(u1));
+    const double th = 2.0 * M_PI * u2;
+    z[2 * k] = rr * cos(th);
+    z[2 * k + 1] = rr * sin(th);
+  }
+}
+
+int orc_predict(int32_t N, float* pose12, const float dT12[12], const double cov36[36],
+                uint64_t seed, uint64_t frame, int64_t gbase, double vertical_sigma) {
+  /* delta ~ N(0, cov) as L z with cov = L L^T (Eq.1: "random noise in the tangent space") */
+  double Lc[36];
+  int zero = 1;
+  for (int k = 0; k < 36; ++k) zero &= (cov36[k] == 0.0);
+  if (zero) {
+    memset(Lc, 0, sizeof(Lc));
+  } else if (cholesky(6, cov36, Lc)) {
+    return 1;
+  }
+  double dT[12];
+  for (int k = 0; k < 12; ++k) dT[k] = (double)dT12[k];
+#pragma omp parallel for schedule(static)
+  for (int32_t i = 0; i < N; ++i) {
+    double z[8], delta[6], T[12], TdT[12];
+    orc_normals8(seed, frame, gbase + i, z);
+    for (int a = 0; a < 6; ++a) {
+      double s = 0.0;
+      for (int b = 0; b <= a; ++b) s += Lc[6 * a + b] * z[b];
+      delta[a] = s;
+    }
+    float* P = pose12 + 12 * (size_t)i;
+    for (int k = 0; k < 12; ++k) T[k] = (double)P[k];
+    orc_compose(T, dT, TdT);
+    /* T_{t-1} dT in fp64, then the right-applied exp with re-orthonormalisation (R30) */
+    float tmp[12];
+    for (int k = 0; k < 12; ++k) tmp[k] = 0.f;
+    {
+      double E[12], TE[12];
+      orc_se3_exp(delta, E);
+      orc_compose(TdT, E, TE);
+      double R[9], RtR[9], M[9], Rn[9];
+      for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b) R[3 * a + b] = TE[4 * a + b];
+      for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b) {
+          double s = 0.0;
+          for (int c = 0; c < 3; ++c) s += R[3 * c + a] * R[3 * c + b];
+          RtR[3 * a + b] = s;
+        }
+      for (int k = 0; k < 9; ++k) M[k] = ((k % 4 == 0) ? 3.0 : 0.0) - RtR[k];
+      mat3_mul(R, M, Rn);
+      for (int a = 0; a < 3; ++a) {
+        for (int b = 0; b < 3; ++b) tmp[4 * a + b] = (float)(0.5 * Rn[3 * a + b]);
+        double ta = TE[4 * a + 3];
+        if (a == 2) ta += vertical_sigma * z[6]; /* elevator: world-frame vertical walk */
+        tmp[4 * a + 3] = (float)ta;
+      }
+    }
+    memcpy(P, tmp, sizeof(tmp));
+  }
+  return 0;
+}
+
+double orc_overlap(const orc_map* m, const float* mean3, int32_t S, const float rel32[12]) {
+  if (S <= 0) return 0.0;
+  int64_t hit = 0;
+  for (int32_t j = 0; j < S; ++j) hit += (correspond(m, rel32, mean3 + 3 * j) >= 0);
+  return (double)hit / (double)S;
 }

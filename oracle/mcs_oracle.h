@@ -41,6 +41,8 @@ typedef struct {
   double  unmatched_penalty;   /* kappa (R8), 0 default                        */
   double  loglik_rel_floor;    /* ln(1e-16) (R17)                       */
   double  posterior_floor;     /* 1e-8                                 */
+  int32_t gn_iterations;       /* GN steps per update (R12), 1 default         */
+  int32_t weight_after_update; /* 0: weight with the pre-update l (R13); 1: re-evaluate */
 } orc_config;
 
 /* ---- SE(3) (right-applied exp) ---- */
@@ -141,6 +143,24 @@ int orc_update(const orc_config* cfg,
                int32_t N, float* pose12, float* kf_pose12, int32_t kf_stride, double* L,
                const float* scan_mean3, const float* scan_cov6, int32_t S, uint32_t U,
                orc_update_out* out);
+
+/* ---- Philox4x32-10 (counter-based generator; Salmon et al., SC'11) ---- */
+void orc_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]);
+
+/* ---- prediction (Eq.1; R31): for particle i (global index gbase + i)
+ * T_t^i = T_{t-1}^i dT exp(delta_i), delta_i = chol(cov) z, z ~ N(0, I) from Philox keyed by
+ * seed with counter (block, gbase + i, frame) and fp64 Box-Muller; vertical_sigma > 0 adds the
+ * elevator heuristic's world-frame vertical random walk t_z += vertical_sigma * z_6.
+ * cov36 row-major 6x6 SPD, or all zero (deterministic prediction).  returns 0, or 1 if cov is
+ * neither. ---- */
+int orc_predict(int32_t N, float* pose12, const float dT12[12], const double cov36[36],
+                uint64_t seed, uint64_t frame, int64_t gbase, double vertical_sigma);
+/* the 8 standard normals of particle gi (exposed for the statistical pins) */
+void orc_normals8(uint64_t seed, uint64_t frame, int64_t gi, double z[8]);
+
+/* ---- keyframe-insertion overlap: fraction of scan points whose pinned fp32 cell
+ * under rel32 is occupied in the map ---- */
+double orc_overlap(const orc_map* m, const float* mean3, int32_t S, const float rel32[12]);
 
 int orc_num_threads(void);
 

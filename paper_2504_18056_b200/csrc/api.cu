@@ -217,6 +217,8 @@ void mcs_config_default(mcs_config* cfg) {
   cfg->loglik_rel_floor = std::log(1e-16);
   cfg->posterior_floor = 1e-8;
   cfg->device = 0;
+  cfg->gn_iterations = 1;
+  cfg->weight_after_update = 0;
   cfg->rank = 0;
   cfg->world_size = 1;
   cfg->nccl_unique_id = nullptr;
@@ -255,6 +257,11 @@ mcs_status mcs_create(const mcs_config* cfg, mcs_ctx** out) {
       !(cfg->damping_rel >= 0) || !(cfg->step_clamp > 0) || !(cfg->unmatched_penalty >= 0) ||
       std::isnan(cfg->loglik_rel_floor) || std::isnan(cfg->posterior_floor)) {
     g_create_error = "invalid numeric configuration";
+    return MCS_E_INVALID_ARG;
+  }
+  if (cfg->gn_iterations < 1 || cfg->gn_iterations > 64 ||
+      (cfg->weight_after_update != 0 && cfg->weight_after_update != 1)) {
+    g_create_error = "gn_iterations must be in [1, 64], weight_after_update 0 or 1";
     return MCS_E_INVALID_ARG;
   }
   if (cfg->world_size < 1 || cfg->rank < 0 || cfg->rank >= cfg->world_size) {
@@ -582,13 +589,24 @@ static void record(mcs_ctx* ctx, int k) {
 
 // the hot path a1..a7, stream-ordered; scan already prepared in d_scan
 static mcs_status run_update(mcs_ctx* ctx, int n_pts, double D_now, uint32_t U) {
+  const int iters = ctx->cfg.gn_iterations > 0 ? ctx->cfg.gn_iterations : 1;
+  const bool post = ctx->cfg.weight_after_update != 0;
   record(ctx, 0);
-  launch_select(ctx, false);                                            // a1
-  record(ctx, 1);
-  launch_sweep(ctx, n_pts);                                             // a2
-  record(ctx, 2);
-  launch_combine(ctx, n_pts, false, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr);  // a3
-  launch_propagate(ctx, D_now);                                         // a4
+  for (int it = 0; it < iters; ++it) {  // R12: each iteration is a full a1-a4 pass
+    launch_select(ctx, kSelectUpdate);                                  // a1
+    if (it == 0) record(ctx, 1);
+    launch_sweep(ctx, n_pts);                                           // a2
+    if (it == 0) record(ctx, 2);
+    launch_combine(ctx, n_pts, (it == 0 && !post) ? kCombineUpdateWeight : kCombineUpdate,
+                   nullptr, nullptr, nullptr, nullptr, nullptr, nullptr);  // a3 (+ L += l)
+    launch_propagate(ctx, D_now);                                       // a4
+  }
+  if (post) {  // R13 variant: weight with l re-evaluated at the updated poses
+    launch_select(ctx, kSelectWeight);
+    launch_sweep(ctx, n_pts);
+    launch_combine(ctx, n_pts, kCombineWeight, nullptr, nullptr, nullptr, nullptr, nullptr,
+                   nullptr);
+  }
   record(ctx, 3);
   const mcs_status s = launch_weights_resample(ctx, U);                 // a5-a7 (+ exchanges)
   record(ctx, 4);
@@ -702,9 +720,9 @@ mcs_status mcs_eval(mcs_ctx* ctx, const float* scan_mean3, const float* scan_cov
   CUDA_TRY(ctx, cudaMallocAsync(&dn, 4 * NS, st));
   CUDA_TRY(ctx, cudaMallocAsync(&dk, 4 * NS, st));
   CUDA_TRY(ctx, cudaMallocAsync(&dloop, ctx->N, st));
-  launch_select(ctx, true);
+  launch_select(ctx, kSelectEval);
   launch_sweep(ctx, n_pts);
-  launch_combine(ctx, n_pts, true, dl, dH, db, dn, dk, dloop);
+  launch_combine(ctx, n_pts, kCombineEval, dl, dH, db, dn, dk, dloop);
   CUDA_TRY(ctx, cudaGetLastError());
   if (slot_loglik) CUDA_TRY(ctx, cudaMemcpyAsync(slot_loglik, dl, 8 * NS, cudaMemcpyDefault, st));
   if (slot_H21) CUDA_TRY(ctx, cudaMemcpyAsync(slot_H21, dH, 84 * NS, cudaMemcpyDefault, st));
@@ -742,6 +760,58 @@ mcs_status mcs_resample(mcs_ctx* ctx, const double* e, const uint8_t* dead, int3
   if (ctx->h_scal->status == MCS_E_DEGENERATE)
     FAIL(ctx, MCS_E_DEGENERATE, "every particle dead (S:381)");
   return MCS_OK;
+}
+
+mcs_status mcs_predict(mcs_ctx* ctx, const float* dT12, const double* cov36, uint64_t seed,
+                       uint64_t frame, double vertical_sigma) {
+  CHECK_CTX(ctx);
+  if (!dT12 || !cov36) FAIL(ctx, MCS_E_INVALID_ARG, "mcs_predict: null dT or covariance");
+  if (!std::isfinite(vertical_sigma) || vertical_sigma < 0)
+    FAIL(ctx, MCS_E_INVALID_ARG, "vertical_sigma must be finite and >= 0");
+  float hdT[12];
+  double hbuf[48];
+  CUDA_TRY(ctx, cudaMemcpy(hdT, dT12, sizeof(hdT), cudaMemcpyDefault));
+  CUDA_TRY(ctx, cudaMemcpy(hbuf + 12, cov36, sizeof(double) * 36, cudaMemcpyDefault));
+  for (int k = 0; k < 12; ++k) {
+    if (!std::isfinite(hdT[k])) FAIL(ctx, MCS_E_INVALID_ARG, "dT not finite");
+    hbuf[k] = (double)hdT[k];
+  }
+  for (int a = 0; a < 6; ++a)
+    for (int b = 0; b < 6; ++b)
+      if (!std::isfinite(hbuf[12 + 6 * a + b]) || hbuf[12 + 6 * a + b] != hbuf[12 + 6 * b + a])
+        FAIL(ctx, MCS_E_INVALID_ARG, "covariance not finite/symmetric");
+  cudaStream_t st = ctx->stream;
+  double* d = nullptr;
+  CUDA_TRY(ctx, cudaMallocAsync(&d, sizeof(double) * 84, st));
+  CUDA_TRY(ctx, cudaMemcpyAsync(d, hbuf, sizeof(double) * 48, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(ctx, cudaMemsetAsync(ctx->d_bad, 0, sizeof(int), st));
+  const mcs_status s = launch_predict(ctx, d, ctx->d_bad, seed, frame, vertical_sigma);
+  cudaFreeAsync(d, st);
+  CUDA_TRY(ctx, cudaStreamSynchronize(st));
+  if (s == MCS_E_INVALID_ARG) FAIL(ctx, s, "covariance neither SPD nor zero");
+  if (s != MCS_OK) CUDA_TRY(ctx, cudaGetLastError());
+  return s;
+}
+
+mcs_status mcs_overlap(mcs_ctx* ctx, const float* scan_mean3, int32_t n_pts, const float* rel12,
+                       int32_t kf, double* out_rate) {
+  CHECK_CTX(ctx);
+  if (!scan_mean3 || !rel12 || !out_rate || n_pts < 1)
+    FAIL(ctx, MCS_E_INVALID_ARG, "mcs_overlap: bad arguments");
+  if (kf < 0 || kf >= ctx->K) FAIL(ctx, MCS_E_INVALID_ARG, "mcs_overlap: no keyframe %d", kf);
+  cudaStream_t st = ctx->stream;
+  char* d = nullptr;
+  const size_t bm = (sizeof(float) * 3 * (size_t)n_pts + 255) & ~(size_t)255;  // keep alignment
+  CUDA_TRY(ctx, cudaMallocAsync(&d, bm + 64 + 8, st));
+  CUDA_TRY(ctx, to_device(d, scan_mean3, bm, st));
+  CUDA_TRY(ctx, to_device(d + bm, rel12, 48, st));
+  unsigned long long cnt = 0;
+  const mcs_status s = launch_overlap(ctx, (const float*)d, n_pts, (const float*)(d + bm), kf,
+                                      (unsigned long long*)(d + bm + 64), &cnt);
+  cudaFreeAsync(d, st);
+  if (s != MCS_OK) CUDA_TRY(ctx, cudaGetLastError());
+  *out_rate = (double)cnt / (double)n_pts;
+  return s;
 }
 
 mcs_status mcs_snapshot(mcs_ctx* ctx) {

@@ -172,12 +172,14 @@ cudaError_t kf_build(mcs_ctx* c, const float* d_mean3, const float* d_cov6, int 
 // (spectral form Sigma = lambda3 I + u u^T + v v^T, fp64 Jacobi)
 void launch_prepare_scan(const float* mean3, const float* cov6, int S, float4* out,
                          cudaStream_t st);
-// a1
-void launch_select(mcs_ctx* c, bool eval_mode);
+// a1; mode: kSelectUpdate (H~, b~ for slots in G), kSelectEval (all slots), kSelectWeight (none)
+enum { kSelectUpdate = 0, kSelectEval = 1, kSelectWeight = 2 };
+void launch_select(mcs_ctx* c, int mode);
 // a2
 void launch_sweep(mcs_ctx* c, int S);
-// a3 (+ L += l and max partials when !eval_mode)
-void launch_combine(mcs_ctx* c, int S, bool eval_mode, double* slot_l, float* slot_H21,
+// a3; modes: per-slot eval outputs; GN update and/or L += l with the first a5 reduction
+enum { kCombineEval = 0, kCombineUpdateWeight = 1, kCombineUpdate = 2, kCombineWeight = 3 };
+void launch_combine(mcs_ctx* c, int S, int mode, double* slot_l, float* slot_H21,
                     float* slot_b6, int32_t* slot_n, int32_t* slot_kf, uint8_t* loop_out);
 // a4
 void launch_propagate(mcs_ctx* c, double D_now);
@@ -201,5 +203,10 @@ mcs_status dist_alltoallv(mcs_ctx* c, const float* d_send, const size_t* send_by
                           const size_t* send_off, float* d_recv, const size_t* recv_bytes,
                           const size_t* recv_off);
 size_t sort_temp_needed(int n, int capK);
+// NEXT rows (predict.cu): Eq.1 prediction; keyframe-insertion overlap
+mcs_status launch_predict(mcs_ctx* c, double* d_buf, int* d_bad, unsigned long long seed,
+                          unsigned long long frame, double vsig);
+mcs_status launch_overlap(mcs_ctx* c, const float* d_mean3, int S, const float* d_rel, int kf,
+                          unsigned long long* d_count, unsigned long long* h_count);
 
 }  // namespace mcs

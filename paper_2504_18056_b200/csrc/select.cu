@@ -113,7 +113,7 @@ __global__ void select_kernel(const float* __restrict__ pose, int capN, int N,
           __fmaf_rn(Rk[6 + a], d[2], __fmaf_rn(Rk[3 + a], d[1], __fmul_rn(Rk[a], d[0])));
     }
     const int in_G = gn_all ? 1 : (k <= latest - gap);
-    const int flags = (eval_mode || in_G) ? 1 : 0;
+    const int flags = eval_mode == kSelectEval ? 1 : (eval_mode == kSelectWeight ? 0 : (in_G ? 1 : 0));
     it[0] = make_float4(rel[0], rel[1], rel[2], rel[3]);
     it[1] = make_float4(rel[4], rel[5], rel[6], rel[7]);
     it[2] = make_float4(rel[8], rel[9], rel[10], rel[11]);
@@ -136,14 +136,14 @@ size_t sort_temp_needed(int n, int capK) {
   return b;
 }
 
-void launch_select(mcs_ctx* c, bool eval_mode) {
+void launch_select(mcs_ctx* c, int mode) {
   const int N = c->N;
   const int nb_max = c->cfg.neighbor_count;
   const int end_bit = sort_end_bit(c->capK);
   const unsigned long long inactive = (end_bit >= 64) ? ~0ull : ((1ull << end_bit) - 1ull);
   select_kernel<<<(N + 127) / 128, 128, 0, c->stream>>>(
       c->d_pose, c->capN, N, c->d_kfpose, c->capK, c->K, nb_max, c->cfg.loop_recency_gap,
-      c->cfg.gn_slots == MCS_GN_ALL_SLOTS, eval_mode ? 1 : 0, c->d_items, c->d_meta, c->d_to,
+      c->cfg.gn_slots == MCS_GN_ALL_SLOTS, mode, c->d_items, c->d_meta, c->d_to,
       c->d_skeys, c->d_sids, inactive);
   size_t tb = c->cub_temp_bytes;
   cub::DeviceRadixSort::SortPairs(c->d_cub_temp, tb, c->d_skeys, c->d_skeys_out, c->d_sids,

@@ -13,81 +13,9 @@
 //   r_k = (D_k - D_{t_o}) / (D_now - D_{t_o}) (R14, R15); T_k <- T_k exp(r_k psi) (Eq.10, R16).
 #include "mcs_internal.cuh"
 #include "reduce.cuh"
+#include "se3.cuh"
 
 namespace mcs {
-
-__device__ void se3_exp_d(const double xi[6], double T[12]) {
-  const double px = xi[3], py = xi[4], pz = xi[5];
-  const double th2 = px * px + py * py + pz * pz;
-  const double th = sqrt(th2);
-  double A, B, C;
-  if (th < 1e-4) {
-    A = 1.0 - th2 / 6.0 + th2 * th2 / 120.0;
-    B = 0.5 - th2 / 24.0 + th2 * th2 / 720.0;
-    C = 1.0 / 6.0 - th2 / 120.0 + th2 * th2 / 5040.0;
-  } else {
-    double s, c;
-    sincos(th, &s, &c);
-    A = s / th;
-    B = (1.0 - c) / th2;
-    C = (th - s) / (th2 * th);
-  }
-  const double W[9] = {0.0, -pz, py, pz, 0.0, -px, -py, px, 0.0};
-  double W2[9];
-#pragma unroll
-  for (int a = 0; a < 3; ++a)
-#pragma unroll
-    for (int b = 0; b < 3; ++b)
-      W2[3 * a + b] = W[3 * a] * W[b] + W[3 * a + 1] * W[3 + b] + W[3 * a + 2] * W[6 + b];
-#pragma unroll
-  for (int a = 0; a < 3; ++a) {
-    double v[3];
-#pragma unroll
-    for (int b = 0; b < 3; ++b) {
-      const double I = (a == b) ? 1.0 : 0.0;
-      T[4 * a + b] = I + A * W[3 * a + b] + B * W2[3 * a + b];
-      v[b] = I + B * W[3 * a + b] + C * W2[3 * a + b];
-    }
-    T[4 * a + 3] = v[0] * xi[0] + v[1] * xi[1] + v[2] * xi[2];
-  }
-}
-
-// T32 <- round_fp32( Newton( T32 * exp(xi) ) )   (Eq.7 / Eq.10, R23, R30)
-__device__ void pose_right_update(float T32[12], const double xi[6]) {
-  double E[12], TE[12];
-  se3_exp_d(xi, E);
-#pragma unroll
-  for (int a = 0; a < 3; ++a) {
-#pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      double s = (b == 3) ? (double)T32[4 * a + 3] : 0.0;
-#pragma unroll
-      for (int c = 0; c < 3; ++c) s += (double)T32[4 * a + c] * E[4 * c + b];
-      TE[4 * a + b] = s;
-    }
-  }
-  double RtR[9];
-#pragma unroll
-  for (int a = 0; a < 3; ++a)
-#pragma unroll
-    for (int b = 0; b < 3; ++b) {
-      double s = 0.0;
-#pragma unroll
-      for (int c = 0; c < 3; ++c) s += TE[4 * c + a] * TE[4 * c + b];
-      RtR[3 * a + b] = s;
-    }
-#pragma unroll
-  for (int a = 0; a < 3; ++a) {
-#pragma unroll
-    for (int b = 0; b < 3; ++b) {
-      double s = 0.0;
-#pragma unroll
-      for (int c = 0; c < 3; ++c) s += TE[4 * a + c] * (((c == b) ? 3.0 : 0.0) - RtR[3 * c + b]);
-      T32[4 * a + b] = (float)(0.5 * s);
-    }
-    T32[4 * a + 3] = (float)TE[4 * a + 3];
-  }
-}
 
 __device__ __forceinline__ int up_idx(int r, int c) {  // r <= c
   return r * 6 - (r * (r - 1)) / 2 + (c - r);
@@ -107,6 +35,7 @@ struct CombineArgs {
   double* partials;  // [2][grid]
   Scalars* scal;
   int capN, N, K, nb_max, S, gap, gn_all, eval_mode;
+  int do_gn, do_weight;  // update mode: GN step (a3) and/or L += l with the a5 reduction
   double kappa, damping, clamp;
   // eval outputs (device, may be null)
   double* slot_l;
@@ -153,6 +82,7 @@ __global__ void __launch_bounds__(128) combine_kernel(CombineArgs a) {
       const bool in_G = a.gn_all ? true : (kf <= latest - a.gap);
       lsum += ls;
       unmatched += a.S - ns;
+      if (!a.eval_mode && !a.do_gn) continue;  // weighting-only pass: l is all it needs
       if (!(in_G || a.eval_mode)) continue;
       // full symmetric H~ in the rotated frame
       double Ht[36];
@@ -219,7 +149,7 @@ __global__ void __launch_bounds__(128) combine_kernel(CombineArgs a) {
     const uint8_t loop = a.meta[i] & 1;
     if (a.eval_mode) {
       if (a.loop_out) a.loop_out[i] = loop;
-    } else {
+    } else if (a.do_gn) {
       uint8_t flags = loop;
       double psi[6] = {0, 0, 0, 0, 0, 0};
       if (loop) {
@@ -285,7 +215,6 @@ __global__ void __launch_bounds__(128) combine_kernel(CombineArgs a) {
           }
         }
       }
-      a.l_out[i] = l;
 #pragma unroll
       for (int k = 0; k < 6; ++k) {
         a.psi[(size_t)k * a.capN + i] = psi[k];
@@ -294,11 +223,14 @@ __global__ void __launch_bounds__(128) combine_kernel(CombineArgs a) {
 #pragma unroll
       for (int k = 0; k < 21; ++k) a.hess[(size_t)k * a.capN + i] = (float)H[k];
       a.flags[i] = flags;
+    }
+    if (!a.eval_mode && a.do_weight) {
+      a.l_out[i] = l;
       Lnew = a.L[i] + l;  // Eq.11 in log space (R22)
       a.L[i] = Lnew;
     }
   }
-  if (a.eval_mode) return;
+  if (a.eval_mode || !a.do_weight) return;
   // first weight reduction: max L, max l  (a5)
   const double bm = block_reduce(Lnew, MaxOp(), -INFINITY);
   const double bl = block_reduce(l, MaxOp(), -INFINITY);
@@ -321,8 +253,9 @@ __global__ void __launch_bounds__(128) combine_kernel(CombineArgs a) {
   }
 }
 
-void launch_combine(mcs_ctx* c, int S, bool eval_mode, double* slot_l, float* slot_H21,
+void launch_combine(mcs_ctx* c, int S, int mode, double* slot_l, float* slot_H21,
                     float* slot_b6, int32_t* slot_n, int32_t* slot_kf, uint8_t* loop_out) {
+  const bool eval_mode = mode == kCombineEval;
   CombineArgs a;
   a.items = c->d_items;
   a.part = c->d_part;
@@ -344,6 +277,8 @@ void launch_combine(mcs_ctx* c, int S, bool eval_mode, double* slot_l, float* sl
   a.gap = c->cfg.loop_recency_gap;
   a.gn_all = c->cfg.gn_slots == MCS_GN_ALL_SLOTS;
   a.eval_mode = eval_mode ? 1 : 0;
+  a.do_gn = (mode == kCombineUpdateWeight || mode == kCombineUpdate) ? 1 : 0;
+  a.do_weight = (mode == kCombineUpdateWeight || mode == kCombineWeight) ? 1 : 0;
   a.kappa = c->cfg.unmatched_penalty;
   a.damping = c->cfg.damping_rel;
   a.clamp = c->cfg.step_clamp;

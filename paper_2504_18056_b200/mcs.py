@@ -53,6 +53,8 @@ class Config(C.Structure):
         ("world_size", C.c_int32),
         ("nccl_unique_id", C.c_void_p),
         ("transport", C.c_void_p),
+        ("gn_iterations", C.c_int32),
+        ("weight_after_update", C.c_int32),
     ]
 
 
@@ -96,6 +98,8 @@ def load() -> C.CDLL:
         "mcs_get_phase_ms": (st, [vp, vp]),
         "mcs_plan_ladder": (st, [i32, vp, vp, u32, vp, vp, vp, vp, vp]),
         "mcs_nccl_unique_id": (st, [vp]),
+        "mcs_predict": (st, [vp, vp, vp, C.c_uint64, C.c_uint64, f64]),
+        "mcs_overlap": (st, [vp, vp, i32, vp, i32, vp]),
         "mcs_inproc_transport_create": (vp, [i32]),
         "mcs_inproc_transport_destroy": (None, [vp]),
         "mcs_plan_migration": (st, [i32, vp, vp, vp]),
@@ -307,6 +311,22 @@ class Context:
         self._check(self._lib.mcs_resample(self._ctx, pe, pd, n, int(U) & 0xFFFFFFFF,
                                            donor.ctypes.data))
         return donor
+
+    def predict(self, dT12, cov36, seed: int, frame: int, vertical_sigma: float = 0.0):
+        """Eq.1 prediction of every local particle (mcs_predict)."""
+        pd, kd = _ptr(np.asarray(dT12, np.float32).reshape(12), np.float32)
+        pc, kc = _ptr(np.asarray(cov36, np.float64).reshape(36), np.float64)
+        self._check(self._lib.mcs_predict(self._ctx, pd, pc, int(seed), int(frame),
+                                          float(vertical_sigma)))
+
+    def overlap(self, scan_mean3, rel12, kf: int) -> float:
+        """Keyframe-insertion overlap rate of a scan against keyframe kf (mcs_overlap)."""
+        pm, km = _ptr(scan_mean3, np.float32)
+        pr, kr = _ptr(np.asarray(rel12, np.float32).reshape(12), np.float32)
+        out = C.c_double()
+        self._check(self._lib.mcs_overlap(self._ctx, pm, int(np.prod(km.shape)) // 3, pr,
+                                          int(kf), C.byref(out)))
+        return out.value
 
     def set_profiling(self, on: bool = True):
         self._check(self._lib.mcs_set_profiling(self._ctx, int(on)))

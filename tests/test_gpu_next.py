@@ -1,0 +1,84 @@
+"""GPU parity of the NEXT rows against the oracle: prediction (Eq.1) with the
+elevator vertical walk, the keyframe-insertion overlap test, and the multi-iteration /
+post-update weighting variants of the update."""
+import numpy as np
+import pytest
+
+import oracle
+import paper_2504_18056_b200 as mcs
+import synth
+
+pytestmark = pytest.mark.gpu
+
+
+def _ctx(s, **kw):
+    cfg = dict(neighbor_count=3, loop_recency_gap=s.gap, voxel_resolution=s.r)
+    cfg.update(kw)
+    ctx = mcs.Context(s.N, s.K, s.S, **cfg)
+    for (m3, c6), d in zip(s.keyframes, s.D):
+        ctx.add_keyframe(m3, c6, d)
+    ctx.set_particles(s.pose12, s.kf_pose12)
+    return ctx
+
+
+def test_predict_parity():
+    s = synth.c1()
+    A = np.random.default_rng(3).normal(size=(6, 6)) * 0.02
+    cov = A @ A.T + 1e-5 * np.eye(6)
+    dT = synth.to12(synth.pose((0.01, 0.0, 0.05), (0.4, 0.1, 0.0)))
+    for vs in (0.0, 0.7):
+        with _ctx(s) as ctx:
+            ctx.predict(dT, cov, seed=1234, frame=9, vertical_sigma=vs)
+            got = ctx.get_particles()["pose12"]
+        ref = s.pose12.copy()
+        oracle.predict(ref, dT, cov, seed=1234, frame=9, gbase=0, vertical_sigma=vs)
+        assert np.abs(got - ref).max() <= 2e-6, np.abs(got - ref).max()
+        assert np.abs(got - s.pose12).max() > 1e-3
+
+
+def test_predict_zero_covariance_and_errors():
+    s = synth.c1()
+    dT = synth.to12(synth.pose((0.0, 0.0, 0.1), (1.0, 0.0, 0.0)))
+    with _ctx(s) as ctx:
+        ctx.predict(dT, np.zeros((6, 6)), seed=1, frame=1)
+        got = ctx.get_particles()["pose12"]
+        with pytest.raises(mcs.MCSError):
+            ctx.predict(dT, -np.eye(6), seed=1, frame=1)
+        assert np.array_equal(ctx.get_particles()["pose12"], got)  # no state change
+    ref = s.pose12.copy()
+    oracle.predict(ref, dT, np.zeros((6, 6)), 1, 1)
+    assert np.abs(got - ref).max() <= 2e-6
+
+
+def test_overlap_parity_exact():
+    s = synth.c2(N=1000)
+    g = np.random.default_rng(5)
+    with mcs.Context(10, s.K, s.S, voxel_resolution=s.r) as ctx:
+        for (m3, c6), d in zip(s.keyframes, s.D):
+            ctx.add_keyframe(m3, c6, d)
+        maps = [oracle.Map(m3, c6, s.r) for m3, c6 in s.keyframes[:4]]
+        for k in range(4):
+            for _ in range(5):
+                rel = synth.to12(synth.pose(g.normal(0, 0.05, 3), g.normal(0, 1.0, 3)))
+                # the scan re-expressed in keyframe k's frame by a random odometry guess
+                assert ctx.overlap(s.scan_mean3, rel, k) == oracle.overlap(maps[k],
+                                                                           s.scan_mean3, rel)
+        m3, _ = s.keyframes[0]
+        assert ctx.overlap(m3, synth.to12(np.eye(4)), 0) == 1.0
+
+
+@pytest.mark.parametrize("iters,post", [(2, 0), (3, 1), (1, 1)])
+def test_iterations_and_post_update_parity(iters, post):
+    s = synth.c1()
+    kw = dict(posterior_floor=0.0, loglik_rel_floor=-np.inf)
+    with _ctx(s, gn_iterations=iters, weight_after_update=post, **kw) as ctx:
+        g = ctx.update(s.scan_mean3, s.scan_cov6, s.D_now, s.U)
+        st = ctx.get_particles()
+    pose, kp, L = s.pose12.copy(), s.kf_pose12.copy(), np.zeros(s.N)
+    o = oracle.update(oracle.make_config(voxel_resolution=s.r, loop_recency_gap=s.gap,
+                                         gn_iterations=iters, weight_after_update=post, **kw),
+                      oracle.Keyframes(s.keyframes, s.D, s.r), s.D_now, pose, kp, L,
+                      s.scan_mean3, s.scan_cov6, s.U)
+    assert np.all(np.abs(g["loglik"] - o["loglik"]) <= 1e-4 * np.abs(o["loglik"]) + 1e-6)
+    assert np.abs(st["pose12"] - pose).max() <= 2e-5
+    np.testing.assert_array_equal(g["flags"], o["flags"])
