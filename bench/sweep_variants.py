@@ -9,10 +9,9 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 VARIANTS = {
-    "base": [],
-    "masked": ["MCS_SWEEP_MASKED"],
-    "masked_t64": ["MCS_SWEEP_MASKED", "MCS_SWEEP_THREADS=64"],
-    "masked_mb5": ["MCS_SWEEP_MASKED", "MCS_SWEEP_MINBLOCKS=5"],
+    "acc64": [],
+    "acc64_mb4": ["MCS_SWEEP_MINBLOCKS=4"],
+    "acc64_c256_mb4": ["MCS_SWEEP_MINBLOCKS=4", "MCS_SWEEP_CHUNK=256"],
 }
 OUT = os.path.join(ROOT, "bench", "_variants")
 

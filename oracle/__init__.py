@@ -95,6 +95,8 @@ def lib():
         L.orc_map_size.restype = i32
         L.orc_map_lookup.argtypes = [vp, i32, i32, i32, vp, vp]
         L.orc_map_lookup.restype = i32
+        L.orc_map_cell.argtypes = [vp, i32, vp, vp]
+        L.orc_map_cell.restype = i32
         L.orc_cell_of.argtypes = [f32, f32, f32, f32, vp]
         L.orc_cell_of.restype = C.c_int
         L.orc_relpose.argtypes = [vp, vp, vp, vp]
@@ -183,6 +185,15 @@ class Map:
         c = np.zeros(6, np.float64)
         cnt = lib().orc_map_lookup(self.ptr, int(cell[0]), int(cell[1]), int(cell[2]), _p(m), _p(c))
         return (cnt, m, c) if cnt else (0, None, None)
+
+    def cells(self, idx):
+        """(mean (n,3), cov6 (n,6)) fp64 of the cells at sorted-list indices idx."""
+        idx = np.asarray(idx)
+        mean = np.zeros((len(idx), 3))
+        cov = np.zeros((len(idx), 6))
+        for j, k in enumerate(idx):
+            lib().orc_map_cell(self.ptr, int(k), mean[j].ctypes.data, cov[j].ctypes.data)
+        return mean, cov
 
     def __del__(self):
         try:

@@ -305,6 +305,13 @@ void orc_map_free(orc_map* m) {
 
 int32_t orc_map_size(const orc_map* m) { return m->n; }
 
+int32_t orc_map_cell(const orc_map* m, int32_t k, double mean[3], double cov6[6]) {
+  if (k < 0 || k >= m->n) return 0;
+  memcpy(mean, m->cells[k].mean, sizeof(double) * 3);
+  memcpy(cov6, m->cells[k].cov, sizeof(double) * 6);
+  return m->cells[k].count;
+}
+
 static int32_t map_find(const orc_map* m, const int32_t c[3]) {
   int32_t lo = 0, hi = m->n - 1;
   while (lo <= hi) {

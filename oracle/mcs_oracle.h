@@ -55,6 +55,8 @@ typedef struct orc_map orc_map;
 orc_map* orc_map_build(const float* mean3, const float* cov6, int32_t n, float r);
 void     orc_map_free(orc_map* m);
 int32_t  orc_map_size(const orc_map* m);
+/* the k-th cell of the sorted cell list (the index orc_pair_linearize's corr[] reports) */
+int32_t  orc_map_cell(const orc_map* m, int32_t k, double mean[3], double cov6[6]);
 /* returns member count (0 = empty cell); writes fp64 mean-of-means / mean-of-covs */
 int32_t  orc_map_lookup(const orc_map* m, int32_t cx, int32_t cy, int32_t cz,
                         double mean[3], double cov6[6]);

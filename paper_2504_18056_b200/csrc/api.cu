@@ -319,7 +319,7 @@ mcs_status mcs_create(const mcs_config* cfg, mcs_ctx** out) {
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     }
   }
-  if (e == cudaSuccess) e = dalloc(&c->d_part, (size_t)kSlotFloats * nb * N);
+  if (e == cudaSuccess) e = dalloc(&c->d_part, (size_t)kSlotWords * nb * N);
   if (e == cudaSuccess) e = dalloc(&c->d_meta, N);
   if (e == cudaSuccess) e = dalloc(&c->d_to, N);
   if (e == cudaSuccess) e = dalloc(&c->d_l, N);

@@ -7,7 +7,7 @@
 //   cumulative log-lik L   : fp64 [Ncap]                    (R22)
 //   keyframe hash tables   : per keyframe, keys u64 [cap] + payload float4 [cap][3]
 //   work items (a1 -> a2)  : float4 [3*Ncap][4]  = (kR|kt rows, {kf, particle, flags, 0})
-//   sweep partials (a2->a3): float [3*Ncap][32] = {l, n, H~21, b~6, pad}
+//   sweep partials (a2->a3): fp64 [3*Ncap][32] = {l, n, H~21, b~6, pad}
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -21,7 +21,7 @@ namespace mcs {
 
 constexpr int kCellMin = -1048576;               // 21-bit signed cell coordinates (R27)
 constexpr int kCellMax = 1048575;
-constexpr int kSlotFloats = 32;                   // sweep partial record per (particle, slot)
+constexpr int kSlotWords = 32;                    // sweep partial record per (particle, slot), fp64
 constexpr int kMaxNb = MCS_MAX_NEIGHBORS;
 
 // Per-keyframe open-addressing table in the keyframe's own cell grid.  Keys are 32-bit
@@ -118,7 +118,7 @@ struct mcs_ctx {
   unsigned long long* d_skeys = nullptr;      // [nb*Ncap] coherence keys (a1)
   unsigned long long* d_skeys_out = nullptr;  // [nb*Ncap]
   int32_t* d_sids = nullptr;                  // [nb*Ncap] item ids before sorting
-  float* d_part = nullptr;      // [nb*Ncap][32]
+  double* d_part = nullptr;     // [nb*Ncap][32] fp64 {l, n, H~21, b~6, pad}
   uint8_t* d_meta = nullptr;    // [Ncap] bit0 loop
   int32_t* d_to = nullptr;      // [Ncap] oldest neighbour keyframe t_o
   double* d_l = nullptr;        // [Ncap] l_i

@@ -27,7 +27,7 @@ namespace mcs {
 #define MCS_SWEEP_CHUNK 256
 #endif
 #ifndef MCS_SWEEP_MINBLOCKS
-#define MCS_SWEEP_MINBLOCKS 1
+#define MCS_SWEEP_MINBLOCKS 4
 #endif
 constexpr int kSweepThreads = MCS_SWEEP_THREADS;
 constexpr int kChunk = MCS_SWEEP_CHUNK;  // scan points per shared-memory stage (48 B each)
@@ -62,8 +62,12 @@ constexpr float kMagic = 12582912.0f;
 __global__ void __launch_bounds__(kSweepThreads, MCS_SWEEP_MINBLOCKS)
     sweep_kernel(const float4* __restrict__ items, const int32_t* __restrict__ order,
                  int n_items, const float4* __restrict__ scan, int S,
-                 const KfMeta* __restrict__ kmeta, float inv_r, float* __restrict__ part) {
+                 const KfMeta* __restrict__ kmeta, float inv_r, double* __restrict__ part) {
   __shared__ float4 s_pt[kChunk * 3];
+  // two-level accumulation: fp32 registers within a stage, fp64 totals per thread in shared
+  // memory across stages (the fp32 running sums over a whole 4,096-point scan lose ~1e-5
+  // relative, which an ill-conditioned H turns into >1e-5 m of pose error)
+  __shared__ double s_acc[28][kSweepThreads];
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   const int item = t < n_items ? order[t] : -1;
   float4 r0 = make_float4(0, 0, 0, 0), r1 = r0, r2 = r0, inf = r0;
@@ -218,6 +222,23 @@ __global__ void __launch_bounds__(kSweepThreads, MCS_SWEEP_MINBLOCKS)
     }
   };
 
+#pragma unroll
+  for (int k = 0; k < 28; ++k) s_acc[k][threadIdx.x] = 0.0;
+  auto flush = [&]() {
+    s_acc[0][threadIdx.x] += (double)l;
+    l = 0.f;
+#pragma unroll
+    for (int k = 0; k < 21; ++k) {
+      s_acc[1 + k][threadIdx.x] += (double)h[k];
+      h[k] = 0.f;
+    }
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+      s_acc[22 + k][threadIdx.x] += (double)bv[k];
+      bv[k] = 0.f;
+    }
+  };
+
   for (int base = 0; base < S; base += kChunk) {
     const int cnt = min(kChunk, S - base);
     __syncthreads();
@@ -248,17 +269,16 @@ __global__ void __launch_bounds__(kSweepThreads, MCS_SWEEP_MINBLOCKS)
         if (probe_on(q)) accumulate(j + 1, q);
       }
     }
+    flush();
   }
   if (!active) return;
-  float4* o = reinterpret_cast<float4*>(part + (size_t)item * kSlotFloats);
-  o[0] = make_float4(l, __int_as_float(n), h[0], h[1]);
-  o[1] = make_float4(h[2], h[3], h[4], h[5]);
-  o[2] = make_float4(h[6], h[7], h[8], h[9]);
-  o[3] = make_float4(h[10], h[11], h[12], h[13]);
-  o[4] = make_float4(h[14], h[15], h[16], h[17]);
-  o[5] = make_float4(h[18], h[19], h[20], bv[0]);
-  o[6] = make_float4(bv[1], bv[2], bv[3], bv[4]);
-  o[7] = make_float4(bv[5], 0.f, 0.f, 0.f);
+  double* o = part + (size_t)item * kSlotWords;
+  o[0] = s_acc[0][threadIdx.x];
+  o[1] = (double)n;
+#pragma unroll
+  for (int k = 0; k < 21; ++k) o[2 + k] = s_acc[1 + k][threadIdx.x];
+#pragma unroll
+  for (int k = 0; k < 6; ++k) o[23 + k] = s_acc[22 + k][threadIdx.x];
 }
 
 // Scan preparation (once per update): Sigma_j = lambda3 I + u u^T + v v^T with u, v the two

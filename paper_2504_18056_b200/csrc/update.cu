@@ -23,7 +23,7 @@ __device__ __forceinline__ int up_idx(int r, int c) {  // r <= c
 
 struct CombineArgs {
   const float4* items;
-  const float* part;
+  const double* part;
   const uint8_t* meta;
   float* pose;
   double* L;
@@ -76,9 +76,9 @@ __global__ void __launch_bounds__(128) combine_kernel(CombineArgs a) {
                    r2 = a.items[4 * item + 2], inf = a.items[4 * item + 3];
       const int kf = __float_as_int(inf.x);
       const double R[9] = {r0.x, r0.y, r0.z, r1.x, r1.y, r1.z, r2.x, r2.y, r2.z};
-      const float* o = a.part + item * kSlotFloats;
-      const double ls = (double)o[0];
-      const int ns = __float_as_int(o[1]);
+      const double* o = a.part + item * kSlotWords;
+      const double ls = o[0];
+      const int ns = (int)o[1];
       const bool in_G = a.gn_all ? true : (kf <= latest - a.gap);
       lsum += ls;
       unmatched += a.S - ns;
@@ -90,13 +90,13 @@ __global__ void __launch_bounds__(128) combine_kernel(CombineArgs a) {
       for (int r = 0; r < 6; ++r)
 #pragma unroll
         for (int c = r; c < 6; ++c) {
-          const double v = (double)o[2 + up_idx(r, c)];
+          const double v = o[2 + up_idx(r, c)];
           Ht[6 * r + c] = v;
           Ht[6 * c + r] = v;
         }
       double bt[6];
 #pragma unroll
-      for (int k = 0; k < 6; ++k) bt[k] = (double)o[23 + k];
+      for (int k = 0; k < 6; ++k) bt[k] = o[23 + k];
       // H_s = B^T H~ B, b_s = B^T b~ with B = blockdiag(R, R)
       double Hs[36], bs[6];
 #pragma unroll

@@ -87,19 +87,31 @@ def _ray_boxes(o, d, boxes, tbest, chunk=32768):
     return out.numpy()
 
 
-def _ray_cylinders(o, d, cyl, tbest):
-    for cx, cy, rad, z0, z1 in cyl:
-        ox, oy = o[0] - cx, o[1] - cy
-        a = d[:, 0] ** 2 + d[:, 1] ** 2
-        b = 2 * (ox * d[:, 0] + oy * d[:, 1])
-        c = ox * ox + oy * oy - rad * rad
+def _ray_cylinders(o, d, cyl, tbest, chunk=32768):
+    """Vertical cylinders (x, y, radius, z0, z1): nearest entry of every ray (torch CPU)."""
+    if len(cyl) == 0:
+        return tbest
+    import torch
+    cx = torch.from_numpy(np.ascontiguousarray(cyl[:, 0] - o[0], np.float64))[None]
+    cy = torch.from_numpy(np.ascontiguousarray(cyl[:, 1] - o[1], np.float64))[None]
+    rad = torch.from_numpy(np.ascontiguousarray(cyl[:, 2], np.float64))[None]
+    z0 = torch.from_numpy(np.ascontiguousarray(cyl[:, 3], np.float64))[None]
+    z1 = torch.from_numpy(np.ascontiguousarray(cyl[:, 4], np.float64))[None]
+    out = torch.from_numpy(tbest)
+    for s in range(0, len(d), chunk):
+        dd = torch.from_numpy(np.ascontiguousarray(d[s:s + chunk], np.float64))
+        dx, dy, dz = dd[:, 0:1], dd[:, 1:2], dd[:, 2:3]
+        a = dx * dx + dy * dy
+        b = -2 * (cx * dx + cy * dy)            # origin at 0, cylinder centre at (cx, cy)
+        c = cx * cx + cy * cy - rad * rad
         disc = b * b - 4 * a * c
         ok = (disc > 0) & (a > 1e-12)
-        t = (-b - np.sqrt(np.where(ok, disc, 0))) / (2 * np.where(ok, a, 1))
-        z = o[2] + t * d[:, 2]
+        t = (-b - torch.sqrt(torch.clamp(disc, min=0))) / (2 * torch.clamp(a, min=1e-12))
+        z = o[2] + t * dz
         hit = ok & (t > 1e-6) & (z >= z0) & (z <= z1)
-        tbest = np.where(hit & (t < tbest), t, tbest)
-    return tbest
+        t = torch.where(hit, t, torch.full_like(t, np.inf))
+        out[s:s + chunk] = torch.minimum(out[s:s + chunk], t.amin(dim=1))
+    return out.numpy()
 
 
 def raycast(world: World, T_sensor: np.ndarray, n_az: int, n_el: int, g: np.random.Generator,
@@ -150,11 +162,14 @@ def covariances(p: np.ndarray, k: int = 10, eps: float = EPS_PLANE) -> np.ndarra
 
 
 def sensor_cloud(world: World, T_sensor: np.ndarray, r: float, count: int | None,
-                 g: np.random.Generator, n_az: int, n_el: int):
-    """Ray cast -> sensor frame -> downsample at r -> (subsample to count) -> covariances."""
+                 g: np.random.Generator, n_az: int, n_el: int, crop_backward: bool = False):
+    """Ray cast -> sensor frame -> (backward crop) -> downsample at r -> (subsample to
+    count) -> covariances."""
     pw = raycast(world, T_sensor, n_az, n_el, g)
     Ti = np.linalg.inv(T_sensor)
     ps = (pw @ Ti[:3, :3].T + Ti[:3, 3]).astype(np.float32)
+    if crop_backward:
+        ps = ps[ps[:, 0] > 0]
     ds = downsample(ps, r, g)
     cov_all = covariances(ds)
     if count is not None:
@@ -323,6 +338,124 @@ def c2(seed: int = 0, N: int = 100_000, S: int = 4096, K: int = 20, gap: int = 1
         Tk[:, k] = np.einsum("ij,njk->nik", kf_gt[k], drift)
     return Scene("C2", r, gap, kfs, D, float(P + D[1] + 0.4), scan[0], scan[1], to12(Tt),
                  to12(Tk), int(rng(seed, "c2/U").integers(0, 2**32)), T_gt, kf_gt)
+
+
+def forest(seed: int, rows: int = 10, pitch: float = 5.0) -> World:
+    """Forest-like grid: rows x rows trees at `pitch`, radius 0.3 +- 0.05 m, 8 m
+    tall, on a ground plane — repeated geometry with one-pitch ambiguity."""
+    g = rng(seed, "forest")
+    xs = np.arange(rows) * pitch
+    X, Y = np.meshgrid(xs, xs, indexing="ij")
+    n = rows * rows
+    cyl = np.stack([X.ravel() + g.normal(0, 0.1, n), Y.ravel() + g.normal(0, 0.1, n),
+                    0.3 + g.uniform(-0.05, 0.05, n), np.zeros(n), np.full(n, 8.0)], 1)
+    return World(cylinders=cyl, ground_z=0.0)
+
+
+def forest_path(arc: float, lo=2.5, hi=42.5, z=1.5) -> np.ndarray:
+    """Counter-clockwise rectangular lap in the gaps between tree rows."""
+    L = hi - lo
+    s = arc % (4 * L)
+    if s < L:
+        p, yaw = (lo + s, lo), 0.0
+    elif s < 2 * L:
+        p, yaw = (hi, lo + s - L), np.pi / 2
+    elif s < 3 * L:
+        p, yaw = (hi - (s - 2 * L), hi), np.pi
+    else:
+        p, yaw = (lo, hi - (s - 3 * L)), 1.5 * np.pi
+    return pose((0, 0, yaw), (p[0], p[1], z))
+
+
+def _kf_poses_drift(kf_gt, N, g, drift_t, drift_r):
+    """(N, K, 12) fp32: GT keyframe poses composed with a per-particle random-walk drift."""
+    K = len(kf_gt)
+    out = np.empty((N, K, 12), np.float32)
+    drift = np.tile(np.eye(4), (N, 1, 1))
+    for k in range(K):
+        if k > 0:
+            drift = perturb(drift, drift_t, drift_r, g, N)
+        out[:, k] = to12(np.einsum("ij,njk->nik", kf_gt[k], drift))
+    return out
+
+
+@functools.lru_cache(maxsize=2)
+def c3(seed: int = 0, N: int = 100_000, S: int = 4096, K: int = 200, gap: int = 10,
+       modes=((0.0, 0.0), (5.0, 0.0), (-5.0, 0.0), (0.0, 5.0))) -> Scene:
+    """C3: forest-like grid, r = 1 m, K keyframes from a prior lap (backward-cropped scans,
+    P:168), the current scan back near the start; particles in lattice-shifted modes one tree
+    pitch apart (the multimodal loop-closure ambiguity of P:168-170)."""
+    world = forest(seed)
+    r = 1.0
+    L = 4 * 40.0
+    D = np.arange(K) * (L / K)
+    kf_gt = np.stack([forest_path(d) for d in D])
+    kfs = [sensor_cloud(world, kf_gt[k], r, None, rng(seed, f"c3/kf{k}"), 512, 84,
+                        crop_backward=True) for k in range(K)]
+    T_gt = forest_path(L + D[2] + 0.3) @ pose((0.0, 0.0, 0.02), (0.0, 0.2, 0.0))
+    scan = sensor_cloud(world, T_gt, r / 4, S, rng(seed, "c3/scan"), 1024, 168,
+                        crop_backward=True)
+    g = rng(seed, "c3/particles")
+    per = -(-N // len(modes))
+    Tt = np.concatenate([perturb(pose(t=(dx, dy, 0.0)) @ T_gt, 0.2, 0.02, g, per)
+                         for dx, dy in modes])[:N]
+    Tk = _kf_poses_drift(kf_gt, N, g, 0.005, 0.0005)
+    return Scene("C3", r, gap, kfs, D, float(L + D[2] + 0.3), scan[0], scan[1], to12(Tt), Tk,
+                 int(rng(seed, "c3/U").integers(0, 2**32)), T_gt, kf_gt)
+
+
+def multi_floor(seed: int, floors: int = 2, height: float = 3.5) -> World:
+    """Near-identical floors: one layout of walls and furniture repeated every
+    `height` metres, plus one distinguishing box per floor."""
+    base = loop_corridor(seed, outer=(30.0, 20.0), width=6.0, height=3.0, n_clutter=60)
+    boxes = []
+    for f in range(floors):
+        off = np.array([0.0, 0.0, f * height])
+        boxes.extend(list(base.boxes + off))
+        c = rng(seed, f"floor{f}").uniform([2, 2, 0], [28, 4, 0]) + off
+        boxes.append(np.array([c, c + [1.5, 1.5, 2.0]]))
+    return World(boxes=np.array(boxes))
+
+
+@functools.lru_cache(maxsize=2)
+def c5(seed: int = 0, N: int = 100_000, S: int = 4096, K_floor: int = 20, gap: int = 10,
+       height: float = 3.5) -> Scene:
+    """C5: kidnapping across two floors.  Keyframes 0..K-1 from a lap of floor 1,
+    K..2K-1 from the same lap on floor 2; the scan is on floor 2 after the elevator; particles
+    spread vertically over both floors (the elevator's vertical random walk)."""
+    world = multi_floor(seed, 2, height)
+    r = 0.5
+    P = 2 * ((30.0 - 6.0) + (20.0 - 6.0))
+    path = lambda arc, f: loop_path(arc, outer=(30.0, 20.0), width=6.0, z=1.5 + f * height)
+    D1 = np.arange(K_floor) * (P / K_floor)
+    kf_gt = np.stack([path(d, 0) for d in D1] + [path(d, 1) for d in D1])
+    D = np.concatenate([D1, P + 10.0 + D1])
+    kfs = [sensor_cloud(world, kf_gt[k], r, None, rng(seed, f"c5/kf{k}"), 600, 100)
+           for k in range(2 * K_floor)]
+    T_gt = path(D1[1] + 0.3, 1)
+    scan = sensor_cloud(world, T_gt, r / 2, S, rng(seed, "c5/scan"), 900, 150)
+    g = rng(seed, "c5/particles")
+    Tt = perturb(T_gt, 0.2, 0.02, g, N)
+    Tt[:, 2, 3] += np.where(g.random(N) < 0.5, -height, 0.0) + g.normal(0, 0.3, N)
+    Tk = _kf_poses_drift(kf_gt, N, g, 0.01, 0.001)
+    D_now = float(2 * P + 20.0 + D1[1] + 0.3)
+    return Scene("C5", r, gap, kfs, D, D_now, scan[0], scan[1], to12(Tt), Tk,
+                 int(rng(seed, "c5/U").integers(0, 2**32)), T_gt, kf_gt)
+
+
+@functools.lru_cache(maxsize=1)
+def c4(seed: int = 0, N: int = 1_000_000, S: int = 8192) -> Scene:
+    """C4: the C2 scene with an 8,192-point scan and 1M particles (sharded over 2/4/8 GPUs)."""
+    base = c2(seed, N=1000)
+    world = loop_corridor(seed)
+    scan = sensor_cloud(world, base.T_gt, base.r / 2, S, rng(seed, "c4/scan"), 1200, 200)
+    g = rng(seed, "c4/particles")
+    Tt = perturb(base.T_gt, 0.1, 0.01, g, N)
+    Tk = _kf_poses_drift(base.kf_gt, N, g, 0.01, 0.001)
+    import dataclasses
+    return dataclasses.replace(base, name="C4", scan_mean3=scan[0], scan_cov6=scan[1],
+                               pose12=to12(Tt), kf_pose12=Tk,
+                               U=int(rng(seed, "c4/U").integers(0, 2**32)))
 
 
 def subset(scene: Scene, N: int) -> Scene:
