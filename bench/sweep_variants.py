@@ -9,9 +9,9 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 VARIANTS = {
-    "acc64": [],
-    "acc64_mb4": ["MCS_SWEEP_MINBLOCKS=4"],
-    "acc64_c256_mb4": ["MCS_SWEEP_MINBLOCKS=4", "MCS_SWEEP_CHUNK=256"],
+    "base": [],
+    "mb3": ["MCS_SWEEP_MINBLOCKS=3"],
+    "chunk128": ["MCS_SWEEP_CHUNK=128"],
 }
 OUT = os.path.join(ROOT, "bench", "_variants")
 

@@ -72,21 +72,23 @@ __global__ void aggregate_insert_kernel(const unsigned long long* __restrict__ s
   unsigned int h = slot_hash(lk, m.shift);
   unsigned int* kw;
   while (true) {
-    kw = reinterpret_cast<unsigned int*>(&slots[4 * h].w);
+    kw = reinterpret_cast<unsigned int*>(&slots[4 * h].x);
     unsigned int prev = atomicCAS(kw, kEmptyKey32, lk);
     if (prev == kEmptyKey32) break;
     h = (h + 1) & m.mask;
   }
-  slots[4 * h + 0] = make_float4((float)mu[0], (float)mu[1], (float)mu[2], __uint_as_float(lk));
-  slots[4 * h + 1] = make_float4((float)s[0], (float)s[1], (float)s[2], (float)s[3]);
-  slots[4 * h + 2] = make_float4((float)s[4], (float)s[5], __int_as_float(cnt), 0.f);
+  // layout (mcs_internal.cuh): the (y, z) pairs sit in aligned register pairs for the sweep's
+  // packed FFMA2 math; s[] = (xx, xy, xz, yy, yz, zz)
+  slots[4 * h + 0] = make_float4(__uint_as_float(lk), (float)mu[0], (float)mu[1], (float)mu[2]);
+  slots[4 * h + 1] = make_float4((float)s[3], (float)s[5], (float)s[1], (float)s[2]);
+  slots[4 * h + 2] = make_float4((float)s[0], (float)s[4], __int_as_float(cnt), 0.f);
 }
 
 __global__ void init_slots_kernel(float4* __restrict__ slots, int cap) {
   int h = blockIdx.x * blockDim.x + threadIdx.x;
   if (h >= cap) return;
   const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-  slots[4 * h + 0] = make_float4(0.f, 0.f, 0.f, __uint_as_float(kEmptyKey32));
+  slots[4 * h + 0] = make_float4(__uint_as_float(kEmptyKey32), 0.f, 0.f, 0.f);
   slots[4 * h + 1] = z;
   slots[4 * h + 2] = z;
   slots[4 * h + 3] = z;

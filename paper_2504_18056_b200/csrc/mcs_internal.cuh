@@ -27,9 +27,10 @@ constexpr int kMaxNb = MCS_MAX_NEIGHBORS;
 // Per-keyframe open-addressing table in the keyframe's own cell grid.  Keys are 32-bit
 // bbox-local cell coordinates (dx << 21 | dy << 10 | dz), so a query outside the keyframe's
 // occupied bounding box is a miss without a probe, and a probe is one 64-byte slot:
-//   float4 {mu'x, mu'y, mu'z, key}  {S'xx, S'xy, S'xz, S'yy}  {S'yz, S'zz, count, 0}  {0,0,0,0}
+//   float4 {key, mu'x, mu'y, mu'z}  {S'yy, S'zz, S'xy, S'xz}  {S'xx, S'yz, count, 0}  {0,0,0,0}
 // (the key shares the first 16 bytes with the mean, so the first-probe payload loads are
-// issued together with the key).  Load factor <= 1/4.
+// issued together with the key; the (y, z) pairs (mu'y, mu'z), (S'yy, S'zz), (S'xy, S'xz) land
+// in aligned register pairs, the operands of the sweep's packed FFMA2 math).  Load factor <= 1/4.
 constexpr unsigned int kEmptyKey32 = 0xFFFFFFFFu;  // dx = 2047 never occurs (ex <= 2047)
 constexpr int kMaxEx = 2047, kMaxEy = 2048, kMaxEz = 1024;
 constexpr unsigned int kHashMul32 = 0x9E3779B1u;

@@ -163,7 +163,7 @@ __global__ void overlap_kernel(const float* __restrict__ mean3, int S, const flo
       const unsigned int key = local_key(dx, dy, dz);
       unsigned int h = slot_hash(key, m.shift) & m.mask;
       while (true) {
-        const unsigned int k = __float_as_uint(m.slots[4 * (size_t)h].w);
+        const unsigned int k = __float_as_uint(m.slots[4 * (size_t)h].x);
         if (k == key) { hit = 1; break; }
         if (k == kEmptyKey32) break;
         h = (h + 1) & m.mask;

@@ -34,7 +34,8 @@ constexpr int kChunk = MCS_SWEEP_CHUNK;  // scan points per shared-memory stage 
 
 struct Probe {
   float4 s0, s1, s2;   // slot payload at the first probe position (speculatively loaded)
-  float qx, qy, qz;    // pinned fp32 transform of the point
+  float qx;            // pinned fp32 transform of the point: x, and (y, z) as one register pair
+  float2 qyz;
   unsigned int key;    // bbox-local key; kEmptyKey32 = outside the keyframe bbox
   unsigned int h;      // slot index of the first probe
 };
@@ -44,6 +45,15 @@ __device__ __forceinline__ float rcp_approx(float x) {
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
   return r;
 }
+
+// packed-pair helpers: one FFMA2/FMUL2/FADD2 does the (y, z) halves of two scalar ops; each
+// lane is the same IEEE fp32 operation as the scalar form (so the R27 key path stays pinned)
+__device__ __forceinline__ float2 bc(float a) { return make_float2(a, a); }
+__device__ __forceinline__ float2 sw(float2 a) { return make_float2(a.y, a.x); }
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ float2 add2(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 neg2(float2 a) { return make_float2(-a.x, -a.y); }
 
 __device__ __forceinline__ void ld_slot(const float4* sl, float4& s0, float4& s1, float4& s2) {
   asm volatile("ld.global.nc.v4.f32 {%0, %1, %2, %3}, [%4];"
@@ -93,24 +103,25 @@ __global__ void __launch_bounds__(kSweepThreads, MCS_SWEEP_MINBLOCKS)
   const unsigned int offx = (unsigned)__float_as_int(kMagic) + (unsigned)m.ox;
   const unsigned int offy = (unsigned)__float_as_int(kMagic) + (unsigned)m.oy;
   const unsigned int offz = (unsigned)__float_as_int(kMagic) + (unsigned)m.oz;
+  // row 0 of kT as scalars, rows 1 and 2 as (y, z) column pairs
   const float R00 = r0.x, R01 = r0.y, R02 = r0.z, tx = r0.w;
-  const float R10 = r1.x, R11 = r1.y, R12 = r1.z, ty = r1.w;
-  const float R20 = r2.x, R21 = r2.y, R22 = r2.z, tz = r2.w;
+  const float2 Ryz0 = make_float2(r1.x, r2.x), Ryz1 = make_float2(r1.y, r2.y);
+  const float2 Ryz2 = make_float2(r1.z, r2.z), tyz = make_float2(r1.w, r2.w);
+  const float2 ntyz = neg2(tyz);
 
   // transform, cell, key and the (unconditional) first-probe loads of point j
   auto issue = [&](int j) {
     Probe p;
     const float4 A = s_pt[3 * j];
+    // q = kR mu + kt with the pinned chain fma(R2, z, fma(R1, y, fma(R0, x, t))) per lane (R27)
     p.qx = __fmaf_rn(R02, A.z, __fmaf_rn(R01, A.y, __fmaf_rn(R00, A.x, tx)));
-    p.qy = __fmaf_rn(R12, A.z, __fmaf_rn(R11, A.y, __fmaf_rn(R10, A.x, ty)));
-    p.qz = __fmaf_rn(R22, A.z, __fmaf_rn(R21, A.y, __fmaf_rn(R20, A.x, tz)));
+    p.qyz = fma2(Ryz2, bc(A.z), fma2(Ryz1, bc(A.y), fma2(Ryz0, bc(A.x), tyz)));
     // floor(q / r) (exact power-of-two scaling, R27) -> bbox-local cell coordinates
     const unsigned int dx =
         (unsigned)__float_as_int(__fadd_rd(__fmul_rn(p.qx, inv_r), kMagic)) - offx;
-    const unsigned int dy =
-        (unsigned)__float_as_int(__fadd_rd(__fmul_rn(p.qy, inv_r), kMagic)) - offy;
-    const unsigned int dz =
-        (unsigned)__float_as_int(__fadd_rd(__fmul_rn(p.qz, inv_r), kMagic)) - offz;
+    const float2 fyz = __fadd2_rd(mul2(p.qyz, bc(inv_r)), bc(kMagic));
+    const unsigned int dy = (unsigned)__float_as_int(fyz.x) - offy;
+    const unsigned int dz = (unsigned)__float_as_int(fyz.y) - offz;
     const bool in = (dx < m.ex) & (dy < m.ey) & (dz < m.ez);
     p.key = in ? local_key(dx, dy, dz) : kEmptyKey32;
     p.h = slot_hash(p.key, m.shift) & m.mask;
@@ -134,7 +145,7 @@ __global__ void __launch_bounds__(kSweepThreads, MCS_SWEEP_MINBLOCKS)
 
   // first probe: 1 = hit, 0 = empty slot or out-of-bbox point (miss), 2 = keep probing
   auto first_check = [&](const Probe& p) -> int {
-    const unsigned int k0 = __float_as_uint(p.s0.w);
+    const unsigned int k0 = __float_as_uint(p.s0.x);
     if (k0 == p.key) return p.key != kEmptyKey32 ? 1 : 0;
     if (k0 == kEmptyKey32 || p.key == kEmptyKey32) return 0;
     return 2;
@@ -147,7 +158,7 @@ __global__ void __launch_bounds__(kSweepThreads, MCS_SWEEP_MINBLOCKS)
       hh = (hh + 1) & m.mask;
       const float4* sl = m.slots + 4 * (size_t)hh;
       const float4 t0 = __ldg(sl);
-      const unsigned int kk = __float_as_uint(t0.w);
+      const unsigned int kk = __float_as_uint(t0.x);
       if (kk == q.key) {
         q.s0 = t0;
         q.s1 = __ldg(sl + 1);
@@ -158,42 +169,46 @@ __global__ void __launch_bounds__(kSweepThreads, MCS_SWEEP_MINBLOCKS)
     }
   };
 
-  // Eqs.3-4 and Eq.6 for one matched (item, point)
+  // Eqs.3-4 and Eq.6 for one matched (item, point); the (y, z) halves of the 3-vectors and of
+  // the symmetric 3x3 matrices travel as register pairs (packed FFMA2/FMUL2/FADD2)
   auto accumulate = [&](int j, const Probe& p) {
     const float4 A = s_pt[3 * j];      // {mu, lambda3}
     const float4 U = s_pt[3 * j + 1];  // {u, 0}
     const float4 V = s_pt[3 * j + 2];  // {v, 0}   Sigma_j = lambda3 I + u u^T + v v^T
+    // payload {key, mu'} {S'yy, S'zz, S'xy, S'xz} {S'xx, S'yz}
     const float4 P0 = p.s0, P1 = p.s1, P2 = p.s2;
     // e = mu' - kT mu   (Eq.4);  m = R mu = q - t
-    const float ex = P0.x - p.qx, ey = P0.y - p.qy, ez = P0.z - p.qz;
-    const float mx = p.qx - tx, my = p.qy - ty, mz = p.qz - tz;
+    const float ex = P0.y - p.qx;
+    const float2 eyz = fma2(p.qyz, bc(-1.f), make_float2(P0.z, P0.w));
+    const float mx = p.qx - tx;
+    const float2 myz = add2(p.qyz, ntyz);
+    const float my = myz.x, mz = myz.y;
     // C = Sigma' + R Sigma R^T = Sigma' + lambda3 I + (Ru)(Ru)^T + (Rv)(Rv)^T  (Eq.4)
-    const float ux = R00 * U.x + R01 * U.y + R02 * U.z;
-    const float uy = R10 * U.x + R11 * U.y + R12 * U.z;
-    const float uz = R20 * U.x + R21 * U.y + R22 * U.z;
-    const float vx = R00 * V.x + R01 * V.y + R02 * V.z;
-    const float vy = R10 * V.x + R11 * V.y + R12 * V.z;
-    const float vz = R20 * V.x + R21 * V.y + R22 * V.z;
-    const float c00 = fmaf(ux, ux, fmaf(vx, vx, P1.x + A.w));
-    const float c01 = fmaf(ux, uy, fmaf(vx, vy, P1.y));
-    const float c02 = fmaf(ux, uz, fmaf(vx, vz, P1.z));
-    const float c11 = fmaf(uy, uy, fmaf(vy, vy, P1.w + A.w));
-    const float c12 = fmaf(uy, uz, fmaf(vy, vz, P2.x));
-    const float c22 = fmaf(uz, uz, fmaf(vz, vz, P2.y + A.w));
-    // Omega = C^-1 = adj(C) / det(C)
-    const float k00 = c11 * c22 - c12 * c12;
-    const float k01 = c02 * c12 - c01 * c22;
-    const float k02 = c01 * c12 - c02 * c11;
-    const float k11 = c00 * c22 - c02 * c02;
-    const float k12 = c01 * c02 - c00 * c12;
-    const float k22 = c00 * c11 - c01 * c01;
-    const float id = rcp_approx(fmaf(c00, k00, fmaf(c01, k01, c02 * k02)));
-    const float o00 = k00 * id, o01 = k01 * id, o02 = k02 * id;
-    const float o11 = k11 * id, o12 = k12 * id, o22 = k22 * id;
-    // w = Omega e ; l -= e^T Omega e  (Eq.3)
-    const float w0 = o00 * ex + o01 * ey + o02 * ez;
-    const float w1 = o01 * ex + o11 * ey + o12 * ez;
-    const float w2 = o02 * ex + o12 * ey + o22 * ez;
+    const float ux = fmaf(R02, U.z, fmaf(R01, U.y, R00 * U.x));
+    const float2 uyz = fma2(Ryz2, bc(U.z), fma2(Ryz1, bc(U.y), mul2(Ryz0, bc(U.x))));
+    const float vx = fmaf(R02, V.z, fmaf(R01, V.y, R00 * V.x));
+    const float2 vyz = fma2(Ryz2, bc(V.z), fma2(Ryz1, bc(V.y), mul2(Ryz0, bc(V.x))));
+    const float c00 = fmaf(ux, ux, fmaf(vx, vx, P2.x + A.w));
+    const float2 c1122 = fma2(uyz, uyz, fma2(vyz, vyz, add2(make_float2(P1.x, P1.y), bc(A.w))));
+    const float2 c0102 = fma2(bc(ux), uyz, fma2(bc(vx), vyz, make_float2(P1.z, P1.w)));
+    const float c12 = fmaf(uyz.x, uyz.y, fmaf(vyz.x, vyz.y, P2.y));
+    // Omega = C^-1 = adj(C) / det(C):  (k11, k22) = c00 (c22, c11) - (c02, c01)^2,
+    // (k01, k02) = c12 (c02, c01) - (c01 c22, c02 c11)
+    const float k00 = fmaf(c1122.x, c1122.y, -c12 * c12);
+    const float2 c0201 = sw(c0102);
+    const float2 k1122 = fma2(bc(c00), sw(c1122), mul2(c0201, neg2(c0201)));
+    const float2 k0102 = fma2(bc(c12), c0201, mul2(c0102, neg2(sw(c1122))));
+    const float k12 = fmaf(c0102.x, c0102.y, -c00 * c12);
+    const float id = rcp_approx(fmaf(c00, k00, fmaf(c0102.x, k0102.x, c0102.y * k0102.y)));
+    const float o00 = k00 * id, o12 = k12 * id;
+    const float2 o1122 = mul2(k1122, bc(id)), o0102 = mul2(k0102, bc(id));
+    const float o01 = o0102.x, o02 = o0102.y, o11 = o1122.x, o22 = o1122.y;
+    const float ey = eyz.x, ez = eyz.y;
+    // w = Omega e: w0 = o00 ex + o01 ey + o02 ez; (w1, w2) = ex (o01, o02) + (o11 ey, o22 ez)
+    // + o12 (ez, ey);  l -= e^T Omega e  (Eq.3)
+    const float w0 = fmaf(o00, ex, fmaf(o01, ey, o02 * ez));
+    const float2 w12 = fma2(bc(ex), o0102, fma2(o1122, eyz, mul2(bc(o12), sw(eyz))));
+    const float w1 = w12.x, w2 = w12.y;
     l = fmaf(-ex, w0, fmaf(-ey, w1, fmaf(-ez, w2, l)));
     ++n;
     if (hb) {
@@ -255,7 +270,7 @@ __global__ void __launch_bounds__(kSweepThreads, MCS_SWEEP_MINBLOCKS)
         accumulate(j, pa);
       } else if (ra == 2) {
         Probe q;
-        q.qx = pa.qx; q.qy = pa.qy; q.qz = pa.qz; q.key = pa.key; q.h = pa.h;
+        q.qx = pa.qx; q.qyz = pa.qyz; q.key = pa.key; q.h = pa.h;
         if (probe_on(q)) accumulate(j, q);
       }
       if (j + 1 >= cnt) break;
@@ -265,7 +280,7 @@ __global__ void __launch_bounds__(kSweepThreads, MCS_SWEEP_MINBLOCKS)
         accumulate(j + 1, pb);
       } else if (rb == 2) {
         Probe q;
-        q.qx = pb.qx; q.qy = pb.qy; q.qz = pb.qz; q.key = pb.key; q.h = pb.h;
+        q.qx = pb.qx; q.qyz = pb.qyz; q.key = pb.key; q.h = pb.h;
         if (probe_on(q)) accumulate(j + 1, q);
       }
     }
