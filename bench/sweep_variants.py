@@ -9,9 +9,10 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 VARIANTS = {
-    "base": [],
-    "mb3": ["MCS_SWEEP_MINBLOCKS=3"],
-    "chunk128": ["MCS_SWEEP_CHUNK=128"],
+    "a1": [],
+    "a2": ["MCS_SWEEP_AHEAD=2"],
+    "pf": ["MCS_SWEEP_AHEAD=3"],
+    "pf2": ["MCS_SWEEP_AHEAD=3", "MCS_SWEEP_PF2=1"],
 }
 OUT = os.path.join(ROOT, "bench", "_variants")
 

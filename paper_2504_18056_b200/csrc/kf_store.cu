@@ -163,10 +163,11 @@ cudaError_t kf_build(mcs_ctx* c, const float* d_mean3, const float* d_cov6, int 
     out.cap = cap;
     out.n_cells = n_cells;
     out.n_points = n;
-    CK(cudaMalloc(&out.slots, sizeof(float4) * 4 * (size_t)cap));
+    // cap probe slots + one always-empty sentinel slot (index cap) that out-of-bbox queries read
+    CK(cudaMalloc(&out.slots, sizeof(float4) * 4 * (size_t)(cap + 1)));
     m.slots = out.slots;
     out.meta = m;
-    init_slots_kernel<<<(cap + 255) / 256, 256, 0, st>>>(out.slots, cap);
+    init_slots_kernel<<<(cap + 1 + 255) / 256, 256, 0, st>>>(out.slots, cap + 1);
     aggregate_insert_kernel<<<g, 256, 0, st>>>(skeys, sidx, head, n, d_mean3, d_cov6, inv_r, m,
                                                out.slots);
     CK(cudaGetLastError());

@@ -32,11 +32,12 @@ constexpr int kMaxNb = MCS_MAX_NEIGHBORS;
 // issued together with the key; the (y, z) pairs (mu'y, mu'z), (S'yy, S'zz), (S'xy, S'xz) land
 // in aligned register pairs, the operands of the sweep's packed FFMA2 math).  Load factor <= 1/4.
 constexpr unsigned int kEmptyKey32 = 0xFFFFFFFFu;  // dx = 2047 never occurs (ex <= 2047)
+constexpr unsigned int kNoKey32 = 0xFFFFFFFEu;     // query key of an out-of-bbox point (dx = 2047)
 constexpr int kMaxEx = 2047, kMaxEy = 2048, kMaxEz = 1024;
 constexpr unsigned int kHashMul32 = 0x9E3779B1u;
 
 struct KfMeta {                 // one per keyframe (device array, read through L1)
-  const float4* slots;          // [cap][4]
+  const float4* slots;          // [cap + 1][4]; slot cap is an always-empty sentinel
   int ox, oy, oz;               // bbox origin (cell coordinates)
   unsigned int ex, ey, ez;      // bbox extents (cells)
   unsigned int shift;           // 32 - log2(cap)

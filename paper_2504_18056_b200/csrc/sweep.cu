@@ -26,6 +26,9 @@ namespace mcs {
 #ifndef MCS_SWEEP_CHUNK
 #define MCS_SWEEP_CHUNK 256
 #endif
+#ifndef MCS_SWEEP_AHEAD
+#define MCS_SWEEP_AHEAD 2   // probe look-ahead distance in points (1 or 2)
+#endif
 #ifndef MCS_SWEEP_MINBLOCKS
 #define MCS_SWEEP_MINBLOCKS 4
 #endif
@@ -36,7 +39,7 @@ struct Probe {
   float4 s0, s1, s2;   // slot payload at the first probe position (speculatively loaded)
   float qx;            // pinned fp32 transform of the point: x, and (y, z) as one register pair
   float2 qyz;
-  unsigned int key;    // bbox-local key; kEmptyKey32 = outside the keyframe bbox
+  unsigned int key;    // bbox-local key; kNoKey32 = outside the keyframe bbox
   unsigned int h;      // slot index of the first probe
 };
 
@@ -73,7 +76,7 @@ __global__ void __launch_bounds__(kSweepThreads, MCS_SWEEP_MINBLOCKS)
     sweep_kernel(const float4* __restrict__ items, const int32_t* __restrict__ order,
                  int n_items, const float4* __restrict__ scan, int S,
                  const KfMeta* __restrict__ kmeta, float inv_r, double* __restrict__ part) {
-  __shared__ float4 s_pt[kChunk * 3];
+  __shared__ float4 s_pt[(kChunk + 2) * 3];
   // two-level accumulation: fp32 registers within a stage, fp64 totals per thread in shared
   // memory across stages (the fp32 running sums over a whole 4,096-point scan lose ~1e-5
   // relative, which an ill-conditioned H turns into >1e-5 m of pose error)
@@ -109,8 +112,8 @@ __global__ void __launch_bounds__(kSweepThreads, MCS_SWEEP_MINBLOCKS)
   const float2 Ryz2 = make_float2(r1.z, r2.z), tyz = make_float2(r1.w, r2.w);
   const float2 ntyz = neg2(tyz);
 
-  // transform, cell, key and the (unconditional) first-probe loads of point j
-  auto issue = [&](int j) {
+  // transform, cell and key of point j (pinned, R27) and its first probe slot
+  auto locate = [&](int j) {
     Probe p;
     const float4 A = s_pt[3 * j];
     // q = kR mu + kt with the pinned chain fma(R2, z, fma(R1, y, fma(R0, x, t))) per lane (R27)
@@ -122,15 +125,21 @@ __global__ void __launch_bounds__(kSweepThreads, MCS_SWEEP_MINBLOCKS)
     const float2 fyz = __fadd2_rd(mul2(p.qyz, bc(inv_r)), bc(kMagic));
     const unsigned int dy = (unsigned)__float_as_int(fyz.x) - offy;
     const unsigned int dz = (unsigned)__float_as_int(fyz.y) - offz;
+    // outside the keyframe's bbox: a key no slot holds, probing the always-empty sentinel slot
     const bool in = (dx < m.ex) & (dy < m.ey) & (dz < m.ez);
-    p.key = in ? local_key(dx, dy, dz) : kEmptyKey32;
-    p.h = slot_hash(p.key, m.shift) & m.mask;
-    const float4* sl = m.slots + 4 * (size_t)p.h;
-    if (active) {
-      // volatile: the compiler may not sink these loads towards their use (that would undo the
-      // prefetch); the payload is consumed one point later
-      ld_slot(sl, p.s0, p.s1, p.s2);
-    }
+    const unsigned int lk = local_key(dx, dy, dz);
+    p.key = in ? lk : kNoKey32;
+    p.h = in ? (slot_hash(lk, m.shift) & m.mask) : m.mask + 1;
+    return p;
+  };
+  // the (unconditional) first-probe loads; volatile: the compiler may not sink them towards
+  // their use (that would undo the look-ahead)
+  auto load = [&](Probe& p) {
+    if (active) ld_slot(m.slots + 4 * (size_t)p.h, p.s0, p.s1, p.s2);
+  };
+  auto issue = [&](int j) {
+    Probe p = locate(j);
+    load(p);
     return p;
   };
 
@@ -143,13 +152,6 @@ __global__ void __launch_bounds__(kSweepThreads, MCS_SWEEP_MINBLOCKS)
 #pragma unroll
   for (int k = 0; k < 6; ++k) bv[k] = 0.f;
 
-  // first probe: 1 = hit, 0 = empty slot or out-of-bbox point (miss), 2 = keep probing
-  auto first_check = [&](const Probe& p) -> int {
-    const unsigned int k0 = __float_as_uint(p.s0.x);
-    if (k0 == p.key) return p.key != kEmptyKey32 ? 1 : 0;
-    if (k0 == kEmptyKey32 || p.key == kEmptyKey32) return 0;
-    return 2;
-  };
   // continue linear probing (rare): loads into fresh registers q.s*, waited on inside this
   // path, so the common path never inherits a pending scoreboard from it
   auto probe_on = [&](Probe& q) -> bool {
@@ -237,6 +239,18 @@ __global__ void __launch_bounds__(kSweepThreads, MCS_SWEEP_MINBLOCKS)
     }
   };
 
+  // first probe: hit -> accumulate; empty slot (or the sentinel) -> miss; else keep probing
+  auto consume = [&](int j, const Probe& p) {
+    const unsigned int k0 = __float_as_uint(p.s0.x);
+    if (k0 == p.key) {
+      accumulate(j, p);
+    } else if (k0 != kEmptyKey32) {
+      Probe q;
+      q.qx = p.qx; q.qyz = p.qyz; q.key = p.key; q.h = p.h;
+      if (probe_on(q)) accumulate(j, q);
+    }
+  };
+
 #pragma unroll
   for (int k = 0; k < 28; ++k) s_acc[k][threadIdx.x] = 0.0;
   auto flush = [&]() {
@@ -254,36 +268,41 @@ __global__ void __launch_bounds__(kSweepThreads, MCS_SWEEP_MINBLOCKS)
     }
   };
 
+  if (threadIdx.x < 6) s_pt[3 * kChunk + threadIdx.x] = make_float4(0.f, 0.f, 0.f, 0.f);
   for (int base = 0; base < S; base += kChunk) {
     const int cnt = min(kChunk, S - base);
     __syncthreads();
     for (int k = threadIdx.x; k < cnt * 3; k += kSweepThreads) s_pt[k] = scan[3 * base + k];
     __syncthreads();
     if (!active) continue;
-    // two probe buffers in flight alternately: the slot of point j+1 is requested before the
-    // math of point j (no register copies between iterations)
-    Probe pa = issue(0), pb;
-    for (int j = 0; j < cnt; j += 2) {
-      const int ra = first_check(pa);
-      if (j + 1 < cnt) pb = issue(j + 1);
-      if (ra == 1) {
-        accumulate(j, pa);
-      } else if (ra == 2) {
-        Probe q;
-        q.qx = pa.qx; q.qyz = pa.qyz; q.key = pa.key; q.h = pa.h;
-        if (probe_on(q)) accumulate(j, q);
-      }
-      if (j + 1 >= cnt) break;
-      const int rb = first_check(pb);
-      if (j + 2 < cnt) pa = issue(j + 2);
-      if (rb == 1) {
-        accumulate(j + 1, pb);
-      } else if (rb == 2) {
-        Probe q;
-        q.qx = pb.qx; q.qyz = pb.qyz; q.key = pb.key; q.h = pb.h;
-        if (probe_on(q)) accumulate(j + 1, q);
-      }
+    // probe buffers in flight in rotation: the slot of point j+2 (j+1 with MCS_SWEEP_AHEAD 1) is
+    // requested before the math of point j, with no register copies between iterations.  s_pt
+    // has two spare points, so the look-ahead issues past the stage end need no guard (their
+    // stale key probes a real slot or the sentinel, and is never consumed)
+#if MCS_SWEEP_AHEAD == 2
+    Probe pa = issue(0), pb = issue(1), pc;
+    int j = 0;
+    for (; j + 2 < cnt; j += 3) {
+      pc = issue(j + 2);
+      consume(j, pa);
+      pa = issue(j + 3);
+      consume(j + 1, pb);
+      pb = issue(j + 4);
+      consume(j + 2, pc);
     }
+    if (j < cnt) consume(j, pa);
+    if (j + 1 < cnt) consume(j + 1, pb);
+#else
+    Probe pa = issue(0), pb;
+    int j = 0;
+    for (; j + 1 < cnt; j += 2) {
+      pb = issue(j + 1);
+      consume(j, pa);
+      pa = issue(j + 2);
+      consume(j + 1, pb);
+    }
+    if (j < cnt) consume(j, pa);
+#endif
     flush();
   }
   if (!active) return;
