@@ -9,10 +9,9 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 VARIANTS = {
-    "a1": [],
-    "a2": ["MCS_SWEEP_AHEAD=2"],
-    "pf": ["MCS_SWEEP_AHEAD=3"],
-    "pf2": ["MCS_SWEEP_AHEAD=3", "MCS_SWEEP_PF2=1"],
+    "a2": [],
+    "b4": ["MCS_SWEEP_AHEAD=4"],
+    "a1": ["MCS_SWEEP_AHEAD=1"],
 }
 OUT = os.path.join(ROOT, "bench", "_variants")
 

@@ -27,7 +27,7 @@ namespace mcs {
 #define MCS_SWEEP_CHUNK 256
 #endif
 #ifndef MCS_SWEEP_AHEAD
-#define MCS_SWEEP_AHEAD 2   // probe look-ahead distance in points (1 or 2)
+#define MCS_SWEEP_AHEAD 4   // 4: probes issued in batches of two, two points ahead; 1: one ahead
 #endif
 #ifndef MCS_SWEEP_MINBLOCKS
 #define MCS_SWEEP_MINBLOCKS 4
@@ -142,6 +142,14 @@ __global__ void __launch_bounds__(kSweepThreads, MCS_SWEEP_MINBLOCKS)
     load(p);
     return p;
   };
+  // issue whose loads are predicated on a key already loaded (never 0xFFFFFFFD: dx = 2047):
+  // ptxas must then drain the earlier probe loads before it issues these (all probe loads
+  // share one scoreboard, so a later wait would also drain the new ones)
+  auto issue_after = [&](int j, unsigned int kdep) {
+    Probe p = locate(j);
+    if (active & (kdep != 0xFFFFFFFDu)) ld_slot(m.slots + 4 * (size_t)p.h, p.s0, p.s1, p.s2);
+    return p;
+  };
 
   float l = 0.f;
   int n = 0;
@@ -155,7 +163,7 @@ __global__ void __launch_bounds__(kSweepThreads, MCS_SWEEP_MINBLOCKS)
   // continue linear probing (rare): loads into fresh registers q.s*, waited on inside this
   // path, so the common path never inherits a pending scoreboard from it
   auto probe_on = [&](Probe& q) -> bool {
-    unsigned int hh = q.h;
+    unsigned int hh = slot_hash(q.key, m.shift) & m.mask;  // (recomputed: rare path)
     while (true) {
       hh = (hh + 1) & m.mask;
       const float4* sl = m.slots + 4 * (size_t)hh;
@@ -240,16 +248,17 @@ __global__ void __launch_bounds__(kSweepThreads, MCS_SWEEP_MINBLOCKS)
   };
 
   // first probe: hit -> accumulate; empty slot (or the sentinel) -> miss; else keep probing
-  auto consume = [&](int j, const Probe& p) {
-    const unsigned int k0 = __float_as_uint(p.s0.x);
+  auto act = [&](int j, const Probe& p, unsigned int k0) {
     if (k0 == p.key) {
       accumulate(j, p);
     } else if (k0 != kEmptyKey32) {
       Probe q;
-      q.qx = p.qx; q.qyz = p.qyz; q.key = p.key; q.h = p.h;
+      q.qx = p.qx; q.qyz = p.qyz; q.key = p.key;
       if (probe_on(q)) accumulate(j, q);
     }
   };
+  auto consume = [&](int j, const Probe& p) { act(j, p, __float_as_uint(p.s0.x)); };
+
 
 #pragma unroll
   for (int k = 0; k < 28; ++k) s_acc[k][threadIdx.x] = 0.0;
@@ -275,23 +284,33 @@ __global__ void __launch_bounds__(kSweepThreads, MCS_SWEEP_MINBLOCKS)
     for (int k = threadIdx.x; k < cnt * 3; k += kSweepThreads) s_pt[k] = scan[3 * base + k];
     __syncthreads();
     if (!active) continue;
-    // probe buffers in flight in rotation: the slot of point j+2 (j+1 with MCS_SWEEP_AHEAD 1) is
-    // requested before the math of point j, with no register copies between iterations.  s_pt
-    // has two spare points, so the look-ahead issues past the stage end need no guard (their
-    // stale key probes a real slot or the sentinel, and is never consumed)
-#if MCS_SWEEP_AHEAD == 2
-    Probe pa = issue(0), pb = issue(1), pc;
+    // Probe buffers in rotation, no register copies between iterations.  Every probe load
+    // shares one scoreboard, so any wait drains all loads issued so far: the loop therefore
+    // drains batch n (its key words), issues batch n+1 (two points, predicated on those keys so
+    // the issue cannot be hoisted above the drain), then does the math of batch n while batch
+    // n+1 is in flight.  s_pt has two spare points, so the look-ahead issues past the stage end
+    // need no guard (their stale key probes a real slot or the sentinel, and is never consumed)
+#if MCS_SWEEP_AHEAD == 4
+    Probe pa = issue(0), pb = issue(1), pc, pd;
     int j = 0;
-    for (; j + 2 < cnt; j += 3) {
-      pc = issue(j + 2);
-      consume(j, pa);
-      pa = issue(j + 3);
-      consume(j + 1, pb);
-      pb = issue(j + 4);
-      consume(j + 2, pc);
+    for (; j + 3 < cnt; j += 4) {
+      const unsigned int ka = __float_as_uint(pa.s0.x), kb = __float_as_uint(pb.s0.x);
+      pc = issue_after(j + 2, ka);
+      pd = issue_after(j + 3, kb);
+      act(j, pa, ka);
+      act(j + 1, pb, kb);
+      const unsigned int kc = __float_as_uint(pc.s0.x), kd = __float_as_uint(pd.s0.x);
+      pa = issue_after(j + 4, kc);
+      pb = issue_after(j + 5, kd);
+      act(j + 2, pc, kc);
+      act(j + 3, pd, kd);
     }
     if (j < cnt) consume(j, pa);
     if (j + 1 < cnt) consume(j + 1, pb);
+    if (j + 2 < cnt) {
+      pc = issue(j + 2);
+      consume(j + 2, pc);
+    }
 #else
     Probe pa = issue(0), pb;
     int j = 0;
