@@ -69,6 +69,13 @@ typedef enum { MCS_GN_OLD_SLOTS = 0, /* Fig.3: gradient w.r.t. non-recent 
                MCS_GN_ALL_SLOTS = 1  /* every neighbour slot                      */
 } mcs_gn_slots;
 
+/* Correspondence search ("voxel-based corresponding point search"; R7, R33). */
+typedef enum { MCS_CORR_CELL = 0, /* the single voxel containing q (one probe)                  */
+               MCS_CORR_NN27 = 1  /* nearest cell representative within nn_radius among the 27
+                                     voxels around q: exact NN for nn_radius <= r (pinned fp32
+                                     squared distance, ties -> lower (oz, oy, ox) index)       */
+} mcs_corr_mode;
+
 /* Collective transport for world_size > 1 when NCCL is not used (e.g. torch.distributed gloo or
  * the in-process transport below).  Buffers are HOST memory; every rank calls the same sequence
  * of operations.  allreduce: in place over n values (dtype 0 = f64, 1 = i64; op 0 = sum,
@@ -103,6 +110,10 @@ typedef struct mcs_config {
   const mcs_transport* transport; /* host transport when world_size > 1 without NCCL        */
   int32_t  gn_iterations;        /* GN steps per update, each a full a1-a4 pass (R12); 1        */
   int32_t  weight_after_update;  /* 0: weight with the pre-update l (R13); 1: re-evaluate l   */
+  int32_t  corr_mode;            /* mcs_corr_mode: MCS_CORR_CELL (R7, default) or NN27 (R33)  */
+  float    nn_radius;            /* NN27 candidate radius in metres, 0 < nn_radius <= r (R33) */
+  int32_t  clone_split;          /* 0: a clone copies its donor's L (R19); 1: the donor and its
+                                    c clones each get L - ln(1 + c) (R34)                    */
 } mcs_config;
 
 /* Fills *cfg with the defaults above (capacities 0: caller sets them). */

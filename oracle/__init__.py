@@ -51,16 +51,23 @@ class Config(C.Structure):
         ("posterior_floor", C.c_double),
         ("gn_iterations", C.c_int32),
         ("weight_after_update", C.c_int32),
+        ("corr_mode", C.c_int32),
+        ("nn_radius", C.c_float),
+        ("clone_split", C.c_int32),
     ]
+
+
+CORR_CELL, CORR_NN27 = 0, 1
 
 
 def make_config(voxel_resolution=0.5, neighbor_count=3, loop_recency_gap=10, gn_slots=0,
                 damping_rel=1e-6, step_clamp=1.0, unmatched_penalty=0.0,
                 loglik_rel_floor=LN_1E16, posterior_floor=1e-8, gn_iterations=1,
-                weight_after_update=0) -> Config:
+                weight_after_update=0, corr_mode=CORR_CELL, nn_radius=0.0,
+                clone_split=0) -> Config:
     return Config(neighbor_count, loop_recency_gap, voxel_resolution, gn_slots, damping_rel,
                   step_clamp, unmatched_penalty, loglik_rel_floor, posterior_floor,
-                  gn_iterations, weight_after_update)
+                  gn_iterations, weight_after_update, corr_mode, nn_radius, clone_split)
 
 
 class ParticleOut(C.Structure):
@@ -97,6 +104,9 @@ def lib():
         L.orc_map_lookup.restype = i32
         L.orc_map_cell.argtypes = [vp, i32, vp, vp]
         L.orc_map_cell.restype = i32
+        L.orc_map_set_corr.argtypes = [vp, i32, f32]
+        L.orc_map_correspond.argtypes = [vp, vp]
+        L.orc_map_correspond.restype = i32
         L.orc_cell_of.argtypes = [f32, f32, f32, f32, vp]
         L.orc_cell_of.restype = C.c_int
         L.orc_relpose.argtypes = [vp, vp, vp, vp]
@@ -185,6 +195,15 @@ class Map:
         c = np.zeros(6, np.float64)
         cnt = lib().orc_map_lookup(self.ptr, int(cell[0]), int(cell[1]), int(cell[2]), _p(m), _p(c))
         return (cnt, m, c) if cnt else (0, None, None)
+
+    def set_corr(self, mode: int, nn_radius: float = 0.0):
+        """Correspondence rule for pair_linearize / overlap-free queries: CELL (R7) or NN27 (R33)."""
+        lib().orc_map_set_corr(self.ptr, int(mode), float(nn_radius))
+
+    def correspond(self, q) -> int:
+        """Sorted-list index of the cell matched by the fp32 point q under the map's rule, or -1."""
+        q = _c(np.asarray(q, np.float32).reshape(3), np.float32)
+        return int(lib().orc_map_correspond(self.ptr, _p(q)))
 
     def cells(self, idx):
         """(mean (n,3), cov6 (n,6)) fp64 of the cells at sorted-list indices idx."""

@@ -230,6 +230,8 @@ struct orc_map {
   int32_t n;
   float inv_r;
   orc_cell* cells; /* sorted lexicographically by (cx, cy, cz) */
+  int32_t corr_mode; /* 0 CELL (R7), 1 NN27 (R33) */
+  float nn_r2;       /* NN27: nn_radius * nn_radius in fp32 */
 };
 
 static int cell_cmp3(const int32_t* a, const int32_t* b) {
@@ -372,13 +374,57 @@ static void key_transform(const float rel32[12], const float* mu, float q[3]) {
                 fmaf(rel32[4 * a + 1], mu[1], fmaf(rel32[4 * a + 0], mu[0], rel32[4 * a + 3])));
 }
 
+void orc_map_set_corr(orc_map* m, int32_t mode, float nn_radius) {
+  m->corr_mode = mode;
+  m->nn_r2 = nn_radius * nn_radius;
+}
+
+/* CELL (R7): the single voxel containing q */
+static int32_t cell_correspond(const orc_map* m, const float q[3]) {
+  int32_t c[3];
+  if (!orc_cell_of(q[0], q[1], q[2], m->inv_r, c)) return -1;
+  return map_find(m, c);
+}
+
+/* NN27 (R33): among the 27 cells around q's cell, the cell representative (the fp32-rounded
+ * mean of means) nearest to q within nn_radius.  Squared distance in the pinned fp32 order of
+ * a1's distances, d = m32 - q32, d2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx)); candidates need
+ * d2 <= nn_radius^2 (fp32); ties -> lower enumeration index, enumerating (oz, oy, ox) in
+ * {-1, 0, 1}^3 lexicographically.  With nn_radius <= r every representative within nn_radius
+ * of q lies in this block, so this is the exact nearest neighbour. */
+static int32_t nn27_correspond(const orc_map* m, const float q[3]) {
+  int32_t c[3];
+  if (!orc_cell_of(q[0], q[1], q[2], m->inv_r, c)) return -1;
+  int32_t best = -1;
+  float best_d2 = 0.0f;
+  for (int oz = -1; oz <= 1; ++oz)
+    for (int oy = -1; oy <= 1; ++oy)
+      for (int ox = -1; ox <= 1; ++ox) {
+        const int32_t nc[3] = {c[0] + ox, c[1] + oy, c[2] + oz};
+        const int32_t k = map_find(m, nc);
+        if (k < 0) continue;
+        const float dx = (float)m->cells[k].mean[0] - q[0];
+        const float dy = (float)m->cells[k].mean[1] - q[1];
+        const float dz = (float)m->cells[k].mean[2] - q[2];
+        const float d2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+        if (!(d2 <= m->nn_r2)) continue;
+        if (best < 0 || d2 < best_d2) {
+          best = k;
+          best_d2 = d2;
+        }
+      }
+  return best;
+}
+
+int32_t orc_map_correspond(const orc_map* m, const float q[3]) {
+  return m->corr_mode == 1 ? nn27_correspond(m, q) : cell_correspond(m, q);
+}
+
 /* correspondence of scan point mu under rel32: index into the map's cell list or -1 */
 static int32_t correspond(const orc_map* m, const float rel32[12], const float* mu) {
   float q[3];
-  int32_t c[3];
   key_transform(rel32, mu, q);
-  if (!orc_cell_of(q[0], q[1], q[2], m->inv_r, c)) return -1;
-  return map_find(m, c);
+  return orc_map_correspond(m, q);
 }
 
 /* ------------------------------------------------------------------------- */
@@ -656,6 +702,10 @@ int orc_particles(const orc_config* cfg, int32_t K, orc_map* const* maps, const 
                   const int32_t* idx, int32_t n_idx, int32_t apply_update,
                   orc_particle_out* out) {
   if (K < 1 || K > 4096 || cfg->neighbor_count < 1 || cfg->neighbor_count > 8) return 2;
+  if (cfg->corr_mode != 0 && cfg->corr_mode != 1) return 2;
+  if (cfg->corr_mode == 1 && !(cfg->nn_radius > 0.0f && cfg->nn_radius <= cfg->voxel_resolution))
+    return 2;
+  for (int32_t k = 0; k < K; ++k) orc_map_set_corr(maps[k], cfg->corr_mode, cfg->nn_radius);
   if (!idx) n_idx = N;
 #pragma omp parallel for schedule(dynamic, 4)
   for (int32_t p = 0; p < n_idx; ++p) {
@@ -812,6 +862,15 @@ int orc_update(const orc_config* cfg, int32_t K, orc_map* const* maps, const dou
   /* step 10: respawn: clone T_t, every T_k and L of the donor (R19, R20) */
   rc = orc_resample(N, e, dead, U, out->donor);
   if (rc == 0) {
+    if (cfg->clone_split) {
+      /* R34: a donor with c clones shares its weight with them: all 1 + c get L - ln(1 + c) */
+      int32_t* copies = (int32_t*)calloc(N > 0 ? N : 1, sizeof(int32_t));
+      for (int32_t i = 0; i < N; ++i)
+        if (out->donor[i] >= 0) ++copies[out->donor[i]];
+      for (int32_t i = 0; i < N; ++i)
+        if (copies[i] > 0) L[i] -= log((double)(1 + copies[i]));
+      free(copies);
+    }
     for (int32_t i = 0; i < N; ++i) {
       int32_t d = out->donor[i];
       if (d < 0) continue;
@@ -928,6 +987,10 @@ int orc_predict(int32_t N, float* pose12, const float dT12[12], const double cov
 double orc_overlap(const orc_map* m, const float* mean3, int32_t S, const float rel32[12]) {
   if (S <= 0) return 0.0;
   int64_t hit = 0;
-  for (int32_t j = 0; j < S; ++j) hit += (correspond(m, rel32, mean3 + 3 * j) >= 0);
+  for (int32_t j = 0; j < S; ++j) {  /* occupancy of the containing voxel, whatever the rule */
+    float q[3];
+    key_transform(rel32, mean3 + 3 * j, q);
+    hit += (cell_correspond(m, q) >= 0);
+  }
   return (double)hit / (double)S;
 }

@@ -43,6 +43,9 @@ typedef struct {
   double  posterior_floor;     /* 1e-8                                 */
   int32_t gn_iterations;       /* GN steps per update (R12), 1 default         */
   int32_t weight_after_update; /* 0: weight with the pre-update l (R13); 1: re-evaluate */
+  int32_t corr_mode;           /* 0: CELL, the containing voxel (R7); 1: NN27 (R33)       */
+  float   nn_radius;           /* NN27 candidate radius, 0 < nn_radius <= r (R33)        */
+  int32_t clone_split;         /* 0: a clone copies the donor's L (R19); 1: split (R34)  */
 } orc_config;
 
 /* ---- SE(3) (right-applied exp) ---- */
@@ -60,6 +63,12 @@ int32_t  orc_map_cell(const orc_map* m, int32_t k, double mean[3], double cov6[6
 /* returns member count (0 = empty cell); writes fp64 mean-of-means / mean-of-covs */
 int32_t  orc_map_lookup(const orc_map* m, int32_t cx, int32_t cy, int32_t cz,
                         double mean[3], double cov6[6]);
+/* correspondence rule the map answers with (orc_particles / orc_update set it from the
+ * config): mode 0 CELL (R7), 1 NN27 with radius nn_radius (R33) */
+void     orc_map_set_corr(orc_map* m, int32_t mode, float nn_radius);
+/* the correspondence of an already transformed fp32 point q under the map's rule: index into
+ * the sorted cell list, or -1 (unmatched) */
+int32_t  orc_map_correspond(const orc_map* m, const float q[3]);
 /* pinned fp32 cell of a point: returns 0 if out of the 21-bit range (R27) */
 int      orc_cell_of(float qx, float qy, float qz, float inv_r, int32_t cell[3]);
 

@@ -220,6 +220,9 @@ void mcs_config_default(mcs_config* cfg) {
   cfg->device = 0;
   cfg->gn_iterations = 1;
   cfg->weight_after_update = 0;
+  cfg->corr_mode = MCS_CORR_CELL;
+  cfg->nn_radius = 0.0f;
+  cfg->clone_split = 0;
   cfg->rank = 0;
   cfg->world_size = 1;
   cfg->nccl_unique_id = nullptr;
@@ -263,6 +266,14 @@ mcs_status mcs_create(const mcs_config* cfg, mcs_ctx** out) {
   if (cfg->gn_iterations < 1 || cfg->gn_iterations > 64 ||
       (cfg->weight_after_update != 0 && cfg->weight_after_update != 1)) {
     g_create_error = "gn_iterations must be in [1, 64], weight_after_update 0 or 1";
+    return MCS_E_INVALID_ARG;
+  }
+  if ((cfg->corr_mode != MCS_CORR_CELL && cfg->corr_mode != MCS_CORR_NN27) ||
+      (cfg->corr_mode == MCS_CORR_NN27 &&
+       !(cfg->nn_radius > 0.0f && cfg->nn_radius <= cfg->voxel_resolution)) ||
+      (cfg->clone_split != 0 && cfg->clone_split != 1)) {
+    g_create_error = "corr_mode must be CELL or NN27 (with 0 < nn_radius <= voxel_resolution), "
+                     "clone_split 0 or 1";
     return MCS_E_INVALID_ARG;
   }
   if (cfg->world_size < 1 || cfg->rank < 0 || cfg->rank >= cfg->world_size) {

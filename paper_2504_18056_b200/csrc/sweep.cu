@@ -72,10 +72,13 @@ __device__ __forceinline__ void ld_slot(const float4* sl, float4& s0, float4& s1
 // other finite x maps far outside any keyframe bbox after the offset.
 constexpr float kMagic = 12582912.0f;
 
+// kCorr: MCS_CORR_CELL (one probe of the containing voxel, R7) or MCS_CORR_NN27 (R33)
+template <int kCorr>
 __global__ void __launch_bounds__(kSweepThreads, MCS_SWEEP_MINBLOCKS)
     sweep_kernel(const float4* __restrict__ items, const int32_t* __restrict__ order,
                  int n_items, const float4* __restrict__ scan, int S,
-                 const KfMeta* __restrict__ kmeta, float inv_r, double* __restrict__ part) {
+                 const KfMeta* __restrict__ kmeta, float inv_r, float nn_r2,
+                 double* __restrict__ part) {
   __shared__ float4 s_pt[(kChunk + 2) * 3];
   // two-level accumulation: fp32 registers within a stage, fp64 totals per thread in shared
   // memory across stages (the fp32 running sums over a whole 4,096-point scan lose ~1e-5
@@ -259,6 +262,52 @@ __global__ void __launch_bounds__(kSweepThreads, MCS_SWEEP_MINBLOCKS)
   };
   auto consume = [&](int j, const Probe& p) { act(j, p, __float_as_uint(p.s0.x)); };
 
+  // NN27 (R33): the nearest cell representative within nn_radius among the 27 voxels around
+  // q's voxel, d = mu'32 - q32, d2 = fma(dz, dz, fma(dy, dy, dx * dx)) (pinned fp32), ties ->
+  // lower (oz, oy, ox) index.  Plain loop: a flagged variant, not the timed path.
+  auto nn27_point = [&](int j) {
+    Probe p = locate(j);
+    const unsigned int bx =
+        (unsigned)__float_as_int(__fadd_rd(__fmul_rn(p.qx, inv_r), kMagic)) - offx;
+    const float2 fyz = __fadd2_rd(mul2(p.qyz, bc(inv_r)), bc(kMagic));
+    const unsigned int by = (unsigned)__float_as_int(fyz.x) - offy;
+    const unsigned int bz = (unsigned)__float_as_int(fyz.y) - offz;
+    int best = -1;
+    float best_d2 = 0.f;
+    for (int oz = -1; oz <= 1; ++oz)
+      for (int oy = -1; oy <= 1; ++oy)
+        for (int ox = -1; ox <= 1; ++ox) {
+          const unsigned int cx = bx + ox, cy = by + oy, cz = bz + oz;
+          if (!((cx < m.ex) & (cy < m.ey) & (cz < m.ez))) continue;
+          const unsigned int key = local_key(cx, cy, cz);
+          unsigned int h = slot_hash(key, m.shift) & m.mask;
+          while (true) {
+            const float4 t0 = __ldg(m.slots + 4 * (size_t)h);
+            const unsigned int k = __float_as_uint(t0.x);
+            if (k == key) {
+              const float dx = __fsub_rn(t0.y, p.qx);
+              const float dy = __fsub_rn(t0.z, p.qyz.x);
+              const float dz = __fsub_rn(t0.w, p.qyz.y);
+              const float d2 = __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, __fmul_rn(dx, dx)));
+              if (d2 <= nn_r2 && (best < 0 || d2 < best_d2)) {
+                best = (int)h;
+                best_d2 = d2;
+              }
+              break;
+            }
+            if (k == kEmptyKey32) break;
+            h = (h + 1) & m.mask;
+          }
+        }
+    if (best >= 0) {
+      const float4* sl = m.slots + 4 * (size_t)best;
+      p.s0 = __ldg(sl);
+      p.s1 = __ldg(sl + 1);
+      p.s2 = __ldg(sl + 2);
+      accumulate(j, p);
+    }
+  };
+
 
 #pragma unroll
   for (int k = 0; k < 28; ++k) s_acc[k][threadIdx.x] = 0.0;
@@ -284,6 +333,11 @@ __global__ void __launch_bounds__(kSweepThreads, MCS_SWEEP_MINBLOCKS)
     for (int k = threadIdx.x; k < cnt * 3; k += kSweepThreads) s_pt[k] = scan[3 * base + k];
     __syncthreads();
     if (!active) continue;
+    if (kCorr == MCS_CORR_NN27) {
+      for (int j = 0; j < cnt; ++j) nn27_point(j);
+      flush();
+      continue;
+    }
     // Probe buffers in rotation, no register copies between iterations.  Every probe load
     // shares one scoreboard, so any wait drains all loads issued so far: the loop therefore
     // drains batch n (its key words), issues batch n+1 (two points, predicated on those keys so
@@ -397,9 +451,15 @@ void launch_prepare_scan(const float* mean3, const float* cov6, int S, float4* o
 void launch_sweep(mcs_ctx* c, int S) {
   const int n_items = c->cfg.neighbor_count * c->N;
   const int grid = (n_items + kSweepThreads - 1) / kSweepThreads;
-  sweep_kernel<<<grid, kSweepThreads, 0, c->stream>>>(c->d_items, c->d_order, n_items, c->d_scan,
-                                                      S, c->d_kf_meta,
-                                                      1.0f / c->cfg.voxel_resolution, c->d_part);
+  const float inv_r = 1.0f / c->cfg.voxel_resolution;
+  if (c->cfg.corr_mode == MCS_CORR_NN27) {
+    const float nn_r2 = c->cfg.nn_radius * c->cfg.nn_radius;
+    sweep_kernel<MCS_CORR_NN27><<<grid, kSweepThreads, 0, c->stream>>>(
+        c->d_items, c->d_order, n_items, c->d_scan, S, c->d_kf_meta, inv_r, nn_r2, c->d_part);
+  } else {
+    sweep_kernel<MCS_CORR_CELL><<<grid, kSweepThreads, 0, c->stream>>>(
+        c->d_items, c->d_order, n_items, c->d_scan, S, c->d_kf_meta, inv_r, 0.f, c->d_part);
+  }
 }
 
 }  // namespace mcs

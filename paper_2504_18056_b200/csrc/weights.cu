@@ -134,6 +134,18 @@ __global__ void ncum_dead_kernel(const Rung* __restrict__ scan, int N,
   ncum[i] = draws_below(sc->q_off + s.C, sc->D_tot, sc->Q_tot, U);
 }
 
+// R34 (flag clone_split): a survivor with c draws shares its weight with its clones; it and
+// each clone get L - ln(1 + c).  Runs before pack/clone, which copy the adjusted L.
+__global__ void split_kernel(const long long* __restrict__ ncum, int N,
+                             const Scalars* __restrict__ sc, unsigned int U,
+                             double* __restrict__ L) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= N || sc->D_tot == 0 || sc->Q_tot == 0) return;
+  const long long prev = i > 0 ? ncum[i - 1] : draws_below(sc->q_off, sc->D_tot, sc->Q_tot, U);
+  const long long copies = ncum[i] - prev;
+  if (copies > 0) L[i] -= log((double)(1 + copies));
+}
+
 // one thread per draw made by this rank's survivors: find the donor (binary search on the
 // monotone n(C)), then either record a local clone or queue the donor for a remote rank.
 // plan (world > 1): [0..G] dead offsets, [G+1..2G+1] send item offsets, [4(G+1)..] first draw
@@ -466,6 +478,7 @@ mcs_status launch_weights_resample(mcs_ctx* c, uint32_t U) {
   }
   ncum_dead_kernel<<<g, kWT, 0, st>>>(scan, N, sc, U, c->d_ncum, c->d_dead_list, c->d_donor,
                                       c->d_donor_g);
+  if (c->cfg.clone_split) split_kernel<<<g, kWT, 0, st>>>(c->d_ncum, N, sc, U, c->d_L);
   if (n_draws_bound > 0)
     draws_kernel<<<(int)((n_draws_bound + kWT - 1) / kWT), kWT, 0, st>>>(
         c->d_ncum, N, sc, c->world, c->rank, c->gbase, c->d_plan, c->d_dead_list, c->d_donor,

@@ -55,7 +55,13 @@ class Config(C.Structure):
         ("transport", C.c_void_p),
         ("gn_iterations", C.c_int32),
         ("weight_after_update", C.c_int32),
+        ("corr_mode", C.c_int32),
+        ("nn_radius", C.c_float),
+        ("clone_split", C.c_int32),
     ]
+
+
+CORR_CELL, CORR_NN27 = 0, 1
 
 
 class UpdateOut(C.Structure):

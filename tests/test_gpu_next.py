@@ -82,3 +82,74 @@ def test_iterations_and_post_update_parity(iters, post):
     assert np.all(np.abs(g["loglik"] - o["loglik"]) <= 1e-4 * np.abs(o["loglik"]) + 1e-6)
     assert np.abs(st["pose12"] - pose).max() <= 2e-5
     np.testing.assert_array_equal(g["flags"], o["flags"])
+
+
+# ------------------------------------------------------------------ NN27 correspondence (R33)
+from test_gpu_parity import check_slots, orc_cfg, pose_err, rel_err  # noqa: E402
+
+
+@pytest.mark.parametrize("frac", [1.0, 0.5])
+def test_nn27_eval_parity(frac):
+    """Every slot output of mcs_eval under NN27 against the oracle (identical correspondences:
+    the pinned fp32 distance decides the nearest cell on both sides)."""
+    s = synth.c1()
+    nn = s.r * frac
+    with _ctx(s, corr_mode=mcs.CORR_NN27, nn_radius=nn) as ctx:
+        g = ctx.eval(s.scan_mean3, s.scan_cov6)
+    o = oracle.particles(orc_cfg(s, corr_mode=oracle.CORR_NN27, nn_radius=nn),
+                         oracle.Keyframes(s.keyframes, s.D, s.r), s.D_now, s.pose12.copy(),
+                         s.kf_pose12.copy(), s.scan_mean3, s.scan_cov6, apply_update=False,
+                         slots=True)
+    check_slots(g, o, s.S)
+    # NN27 matches at least what CELL matches (the containing voxel's representative lies
+    # within r of q only if close; so compare counts loosely) and changes some correspondences
+    with _ctx(s) as ctx:
+        gc = ctx.eval(s.scan_mean3, s.scan_cov6)
+    assert not np.array_equal(gc["slot_n"], g["slot_n"])
+
+
+def test_nn27_update_parity():
+    s = synth.c1()
+    kw = dict(posterior_floor=0.0, loglik_rel_floor=-np.inf, corr_mode=1, nn_radius=s.r)
+    with _ctx(s, **kw) as ctx:
+        g = ctx.update(s.scan_mean3, s.scan_cov6, s.D_now, s.U)
+        st = ctx.get_particles()
+    pose, kp, L = s.pose12.copy(), s.kf_pose12.copy(), np.zeros(s.N)
+    o = oracle.update(orc_cfg(s, **kw), oracle.Keyframes(s.keyframes, s.D, s.r), s.D_now, pose,
+                      kp, L, s.scan_mean3, s.scan_cov6, s.U)
+    assert np.all(np.abs(g["loglik"] - o["loglik"]) <= 1e-4 * np.abs(o["loglik"]))
+    assert np.all(rel_err(g["grad6"], o["grad6"], axis=1) <= 1e-3)
+    np.testing.assert_array_equal(g["flags"], o["flags"])
+    ang, dt = pose_err(st["pose12"], pose)
+    assert ang.max() <= 1e-5 and dt.max() <= 1e-5, (ang.max(), dt.max())
+
+
+def test_nn27_config_errors():
+    s = synth.c1()
+    for bad in (dict(corr_mode=1, nn_radius=0.0), dict(corr_mode=1, nn_radius=2 * s.r),
+                dict(corr_mode=2), dict(clone_split=3)):
+        with pytest.raises(mcs.MCSError):
+            mcs.Context(10, 2, 10, voxel_resolution=s.r, **bad)
+
+
+# ------------------------------------------------------------------ weight-splitting clones (R34)
+def test_clone_split_parity():
+    """The GPU's respawned L equals the split rule applied to its own pre-respawn L and donors;
+    donors equal the copy run's (the split does not change e, the dead set or the ladder)."""
+    s = synth.c1()
+    with _ctx(s) as ctx:
+        gc = ctx.update(s.scan_mean3, s.scan_cov6, s.D_now, s.U)
+        Lc = ctx.get_particles()["L"]  # L_pre[donor or self], fp64
+    with _ctx(s, clone_split=1) as ctx:
+        gs = ctx.update(s.scan_mean3, s.scan_cov6, s.D_now, s.U)
+        st = ctx.get_particles()
+    np.testing.assert_array_equal(gc["donor"], gs["donor"])
+    donor = gs["donor"]
+    assert 0 < gs["n_dead"] < s.N
+    copies = np.bincount(donor[donor >= 0], minlength=s.N)
+    src = np.where(donor >= 0, donor, np.arange(s.N))
+    expect = Lc - np.log1p(copies[src])
+    np.testing.assert_allclose(st["L"], expect, rtol=1e-15, atol=1e-12)
+    assert abs(gs["weight"].sum() - 1) < 1e-12
+    _, _, w_ref, _, _ = oracle.weights(st["L"])
+    np.testing.assert_allclose(gs["weight"], w_ref, rtol=1e-12, atol=1e-300)

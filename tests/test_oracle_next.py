@@ -134,3 +134,131 @@ def test_iterations_and_post_update_weighting():
     o3p, p3p = run(gn_iterations=3, weight_after_update=1)
     np.testing.assert_array_equal(p3p, p3)
     assert np.median(o3p["loglik"]) > np.median(o1["loglik"])  # GN ascent improved l
+
+
+# ------------------------------------------------------------------ NN27 correspondence (R33)
+from fractions import Fraction
+
+
+def _f32_round(x: Fraction) -> np.float32:
+    """x correctly rounded to fp32 (ties to even), independent of the oracle's arithmetic."""
+    f = np.float32(float(x))
+    cands = [np.nextafter(f, np.float32(-np.inf)), f, np.nextafter(f, np.float32(np.inf))]
+    best = None
+    for c in cands:
+        d = abs(Fraction(float(c)) - x)
+        key = (d, int(np.array(c, np.float32).view(np.uint32)) & 1)
+        if best is None or key < best[0]:
+            best = (key, c)
+    return np.float32(best[1])
+
+
+def _fmaf(a, b, c):
+    return _f32_round(Fraction(float(a)) * Fraction(float(b)) + Fraction(float(c)))
+
+
+def _brute_nn(q, means32, cells, r, nn_radius):
+    """Nearest representative over ALL cells within nn_radius, pinned fp32 d2 (exact fma)."""
+    q = np.asarray(q, np.float32)
+    r2 = np.float32(nn_radius) * np.float32(nn_radius)
+    d = (means32 - q).astype(np.float32)
+    approx = (d.astype(np.float64) ** 2).sum(1)
+    qc = np.floor(q * np.float32(1.0 / r)).astype(np.int64)
+    best = None
+    for k in np.nonzero(approx <= float(r2) * 1.001 + 1e-12)[0]:
+        dx, dy, dz = d[k]
+        d2 = _fmaf(dz, dz, _fmaf(dy, dy, np.float32(dx * dx)))
+        if not d2 <= r2:
+            continue
+        o = cells[k] - qc
+        idx = int((o[2] + 1) * 9 + (o[1] + 1) * 3 + (o[0] + 1)) if np.abs(o).max() <= 1 else 99
+        key = (float(d2), idx)
+        if best is None or key < best[0]:
+            best = (key, k)
+    return -1 if best is None else int(best[1])
+
+
+@pytest.mark.parametrize("nn_radius", [0.5, 0.3])
+def test_nn27_is_the_bruteforce_nearest_neighbour(nn_radius):
+    g = np.random.default_rng(11)
+    r = 0.5
+    pts = g.uniform(-1.5, 1.5, (500, 3)).astype(np.float32)
+    cov = np.tile(np.array([0.01, 0, 0, 0.01, 0, 0.01], np.float32), (len(pts), 1))
+    m = oracle.Map(pts, cov, r)
+    n = len(m)
+    means, _ = m.cells(np.arange(n))
+    means32 = means.astype(np.float32)
+    cells = np.array([oracle.cell_of(mu, r) for mu in means32], np.int64)
+    m.set_corr(oracle.CORR_NN27, nn_radius)
+    qs = g.uniform(-1.8, 1.8, (300, 3)).astype(np.float32)
+    got = np.array([m.correspond(q) for q in qs])
+    ref = np.array([_brute_nn(q, means32, cells, r, nn_radius) for q in qs])
+    np.testing.assert_array_equal(got, ref)
+    assert (got >= 0).mean() > 0.3
+    # CELL is a different rule: it misses queries whose own voxel is empty
+    m.set_corr(oracle.CORR_CELL)
+    cell = np.array([m.correspond(q) for q in qs])
+    assert ((cell < 0) & (got >= 0)).any()
+
+
+def test_nn27_hand_case_across_a_face():
+    r = 0.5
+    m = oracle.Map(np.array([[0.49, 0.0, 0.0]], np.float32),
+                   np.array([[0.25, 0, 0, 0.25, 0, 0.25]], np.float32), r)
+    q = np.array([0.51, 0.0, 0.0], np.float32)  # next voxel along x, 0.02 m away
+    assert m.correspond(q) == -1                  # CELL: empty voxel
+    m.set_corr(oracle.CORR_NN27, 0.5)
+    assert m.correspond(q) == 0
+    m.set_corr(oracle.CORR_NN27, 0.01)           # outside the radius
+    assert m.correspond(q) == -1
+    # ties: two representatives at the same fp32 distance -> the lower (oz, oy, ox) index wins
+    m2 = oracle.Map(np.array([[0.25, 0.25, -0.25], [0.25, 0.25, 0.75]], np.float32),
+                    np.tile(np.array([0.25, 0, 0, 0.25, 0, 0.25], np.float32), (2, 1)), r)
+    m2.set_corr(oracle.CORR_NN27, 0.5)
+    k = m2.correspond(np.array([0.25, 0.25, 0.25], np.float32))
+    means, _ = m2.cells([k])
+    assert means[0][2] == np.float32(-0.25)      # oz = -1 comes first
+
+
+def test_nn27_self_match_is_exact():
+    """Scan = keyframe cloud with one point per cell, identity pose: every point matches its own
+    cell at d2 = 0, so l = 0, b = 0 exactly, as under CELL."""
+    s = synth.c1()
+    m3, c6 = s.keyframes[0]
+    m = oracle.Map(m3, c6, s.r)
+    m.set_corr(oracle.CORR_NN27, s.r)
+    r32, r64 = oracle.relpose(synth.to12(np.eye(4)), synth.to12(np.eye(4)))
+    res = oracle.pair_linearize(m, m3, c6, r32, r64)
+    assert res.n == len(m3) and res.l == 0.0 and np.all(res.b == 0.0)
+    m.set_corr(oracle.CORR_CELL)
+    res_c = oracle.pair_linearize(m, m3, c6, r32, r64)
+    np.testing.assert_array_equal(res.corr, res_c.corr)
+
+
+# ------------------------------------------------------------------ weight-splitting clones (R34)
+def test_clone_split_shares_the_donor_weight():
+    s = synth.c1()
+    kfs = oracle.Keyframes(s.keyframes, s.D, s.r)
+
+    def run(split):
+        pose, kp, L = s.pose12.copy(), s.kf_pose12.copy(), np.zeros(s.N)
+        out = oracle.update(oracle.make_config(voxel_resolution=s.r, loop_recency_gap=s.gap,
+                                               clone_split=split), kfs, s.D_now, pose, kp, L,
+                            s.scan_mean3, s.scan_cov6, s.U)
+        return out, L
+
+    oc, Lc = run(0)
+    os_, Ls = run(1)
+    np.testing.assert_array_equal(oc["donor"], os_["donor"])  # same e, dead set and U
+    assert 0 < oc["n_dead"] < s.N
+    donor = oc["donor"]
+    copies = np.bincount(donor[donor >= 0], minlength=s.N)
+    src = np.where(donor >= 0, donor, np.arange(s.N))  # whose L each slot holds
+    expect = Lc - np.log1p(copies[src])                 # donor and each clone: L - ln(1 + c)
+    np.testing.assert_allclose(Ls, expect, rtol=0, atol=1e-12)
+    assert abs(os_["weight"].sum() - 1) < 1e-12
+    # the split conserves each donor family's total weight before renormalisation
+    fam = np.exp(Ls - Ls.max())
+    for d in np.unique(donor[donor >= 0])[:20]:
+        members = (src == d)
+        assert np.isclose(fam[members].sum(), np.exp(Lc[d] - Ls.max()), rtol=1e-12)
