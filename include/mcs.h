@@ -90,6 +90,17 @@ typedef struct mcs_transport {
                    void* const* recv, const size_t* recv_bytes);
 } mcs_transport;
 
+/* Device-memory hook (e.g. PyTorch's caching allocator).  Every device buffer of a context is
+ * taken from alloc(bytes, stream, user) and returned through free(ptr, stream, user), with the
+ * context's stream at the time of the call (persistent buffers: the stream current at create).
+ * alloc returns NULL on failure (-> MCS_E_OUT_OF_MEMORY).  Both must be thread-compatible with
+ * the caller; the struct is copied at mcs_create. */
+typedef struct mcs_allocator {
+  void* (*alloc)(size_t bytes, void* cuda_stream, void* user);
+  void  (*free)(void* ptr, void* cuda_stream, void* user);
+  void* user;
+} mcs_allocator;
+
 typedef struct mcs_config {
   uint32_t abi_version;          /* MCS_ABI_VERSION                                         */
   int32_t  capacity_particles;   /* particles on this device (its shard when world_size>1)  */
@@ -114,6 +125,7 @@ typedef struct mcs_config {
   float    nn_radius;            /* NN27 candidate radius in metres, 0 < nn_radius <= r (R33) */
   int32_t  clone_split;          /* 0: a clone copies its donor's L (R19); 1: the donor and its
                                     c clones each get L - ln(1 + c) (R34)                    */
+  const mcs_allocator* allocator; /* NULL: cudaMalloc / cudaMallocAsync on the context stream */
 } mcs_config;
 
 /* Fills *cfg with the defaults above (capacities 0: caller sets them). */

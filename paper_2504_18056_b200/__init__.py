@@ -3,10 +3,10 @@
 The product is the C-ABI library ``libmcs.so`` (hand-written sm_100a CUDA, see
 ``include/mcs.h``); :mod:`paper_2504_18056_b200.mcs` is its thin ctypes binding.
 """
-from .mcs import (ABI_VERSION, CORR_CELL, CORR_NN27, Config, Context, InprocTransport, MCSError, default_config,
+from .mcs import (ABI_VERSION, CORR_CELL, CORR_NN27, Allocator, Config, Context, InprocTransport, MCSError, default_config,
                   header_symbols, load, nccl_unique_id, plan_ladder, plan_migration,
-                  state_bytes_per_particle, unpack_h21)
+                  state_bytes_per_particle, TorchAllocator, unpack_h21)
 
-__all__ = ["ABI_VERSION", "CORR_CELL", "CORR_NN27", "Config", "Context", "InprocTransport", "MCSError", "default_config",
+__all__ = ["ABI_VERSION", "CORR_CELL", "CORR_NN27", "Allocator", "Config", "Context", "InprocTransport", "MCSError", "default_config",
            "header_symbols", "load", "nccl_unique_id", "plan_ladder", "plan_migration",
-           "state_bytes_per_particle", "unpack_h21"]
+           "state_bytes_per_particle", "TorchAllocator", "unpack_h21"]

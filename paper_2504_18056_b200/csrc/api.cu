@@ -152,9 +152,38 @@ __global__ void gather_outputs_kernel(OutPtrs o, int N, int capN, const double* 
 }
 
 // ------------------------------------------------------------------ helpers
+namespace mcs {
+cudaError_t mem_alloc(mcs_ctx* c, void** p, size_t bytes) {
+  if (!bytes) bytes = 1;
+  if (c->alloc.alloc) {
+    *p = c->alloc.alloc(bytes, (void*)c->stream, c->alloc.user);
+    return *p ? cudaSuccess : cudaErrorMemoryAllocation;
+  }
+  return cudaMalloc(p, bytes);
+}
+void mem_free(mcs_ctx* c, void* p) {
+  if (!p) return;
+  if (c->alloc.alloc) c->alloc.free(p, (void*)c->stream, c->alloc.user);
+  else cudaFree(p);
+}
+cudaError_t mem_alloc_async(mcs_ctx* c, void** p, size_t bytes, cudaStream_t st) {
+  if (!bytes) bytes = 1;
+  if (c->alloc.alloc) {
+    *p = c->alloc.alloc(bytes, (void*)st, c->alloc.user);
+    return *p ? cudaSuccess : cudaErrorMemoryAllocation;
+  }
+  return cudaMallocAsync(p, bytes, st);
+}
+void mem_free_async(mcs_ctx* c, void* p, cudaStream_t st) {
+  if (!p) return;
+  if (c->alloc.alloc) c->alloc.free(p, (void*)st, c->alloc.user);
+  else cudaFreeAsync(p, st);
+}
+}  // namespace mcs
+
 template <typename T>
-static cudaError_t dalloc(T** p, size_t count) {
-  return cudaMalloc((void**)p, sizeof(T) * (count ? count : 1));
+static cudaError_t dalloc(mcs_ctx* c, T** p, size_t count) {
+  return mem_alloc(c, (void**)p, sizeof(T) * (count ? count : 1));
 }
 
 static bool is_pow2_float(float r) {
@@ -165,7 +194,7 @@ static bool is_pow2_float(float r) {
 }
 
 static void free_all(mcs_ctx* c) {
-  for (auto& k : c->kf) cudaFree(k.slots);
+  for (auto& k : c->kf) mem_free(c, k.slots);
   void* ptrs[] = {c->d_kf_meta, c->d_D,       c->d_pose,     c->d_kfpose,   c->d_L,
                   c->d_snapshot, c->d_scan_raw, c->d_scan,    c->d_items,    c->d_order,
                   c->d_part,    c->d_meta,    c->d_to,       c->d_l,        c->d_psi,
@@ -174,8 +203,7 @@ static void free_all(mcs_ctx* c) {
                   c->d_ipartials, c->d_scal,  c->d_cub_temp, c->d_skeys, c->d_skeys_out,
                   c->d_sids,    c->d_stage,   c->d_bad,      c->d_dead_list, c->d_donor_g,
                   c->d_plan,    c->d_pack_src, c->d_send,    c->d_recv};
-  for (void* p : ptrs)
-    if (p) cudaFree(p);
+  for (void* p : ptrs) mem_free(c, p);
   if (c->h_scal) cudaFreeHost(c->h_scal);
   if (c->h_stage) cudaFreeHost(c->h_stage);
   dist_destroy(c);
@@ -292,8 +320,14 @@ mcs_status mcs_create(const mcs_config* cfg, mcs_ctx** out) {
     g_create_error = "capacity_particles > 2^21 per device (integer-ladder bound, R18)";
     return MCS_E_CAPACITY;
   }
+  if (cfg->allocator && (!cfg->allocator->alloc || !cfg->allocator->free)) {
+    g_create_error = "allocator needs both alloc and free";
+    return MCS_E_INVALID_ARG;
+  }
   mcs_ctx* c = new mcs_ctx();
   c->cfg = *cfg;
+  if (cfg->allocator) c->alloc = *cfg->allocator;
+  c->cfg.allocator = nullptr;  // copied above; the caller's struct need not outlive the call
   c->dev = cfg->device;
   c->capN = cfg->capacity_particles;
   c->capK = cfg->capacity_keyframes;
@@ -304,25 +338,25 @@ mcs_status mcs_create(const mcs_config* cfg, mcs_ctx** out) {
   c->own_stream = (e == cudaSuccess);
   const size_t N = c->capN, K = c->capK, S = c->capS, nb = c->nbcap;
   const size_t maxb = (N + 127) / 128 + 64;
-  if (e == cudaSuccess) e = dalloc(&c->d_kf_meta, K);
-  if (e == cudaSuccess) e = dalloc(&c->d_D, K);
-  if (e == cudaSuccess) e = dalloc(&c->d_pose, 12 * N);
-  if (e == cudaSuccess) e = dalloc(&c->d_kfpose, N * K * 12);
-  if (e == cudaSuccess) e = dalloc(&c->d_L, N);
-  if (e == cudaSuccess) e = dalloc(&c->d_scan_raw, 9 * S);
-  if (e == cudaSuccess) e = dalloc(&c->d_scan, 3 * S);
-  if (e == cudaSuccess) e = dalloc(&c->d_items, 4 * nb * N);
-  if (e == cudaSuccess) e = dalloc(&c->d_order, nb * N);
-  if (e == cudaSuccess) e = dalloc(&c->d_skeys, nb * N);
-  if (e == cudaSuccess) e = dalloc(&c->d_skeys_out, nb * N);
-  if (e == cudaSuccess) e = dalloc(&c->d_sids, nb * N);
-  if (e == cudaSuccess) e = dalloc(&c->d_bad, 1);
-  if (e == cudaSuccess) e = dalloc(&c->d_dead_list, N);
-  if (e == cudaSuccess) e = dalloc(&c->d_donor_g, N);
-  if (e == cudaSuccess) e = dalloc(&c->d_plan, 5 * (size_t)(cfg->world_size + 1));
+  if (e == cudaSuccess) e = dalloc(c, &c->d_kf_meta, K);
+  if (e == cudaSuccess) e = dalloc(c, &c->d_D, K);
+  if (e == cudaSuccess) e = dalloc(c, &c->d_pose, 12 * N);
+  if (e == cudaSuccess) e = dalloc(c, &c->d_kfpose, N * K * 12);
+  if (e == cudaSuccess) e = dalloc(c, &c->d_L, N);
+  if (e == cudaSuccess) e = dalloc(c, &c->d_scan_raw, 9 * S);
+  if (e == cudaSuccess) e = dalloc(c, &c->d_scan, 3 * S);
+  if (e == cudaSuccess) e = dalloc(c, &c->d_items, 4 * nb * N);
+  if (e == cudaSuccess) e = dalloc(c, &c->d_order, nb * N);
+  if (e == cudaSuccess) e = dalloc(c, &c->d_skeys, nb * N);
+  if (e == cudaSuccess) e = dalloc(c, &c->d_skeys_out, nb * N);
+  if (e == cudaSuccess) e = dalloc(c, &c->d_sids, nb * N);
+  if (e == cudaSuccess) e = dalloc(c, &c->d_bad, 1);
+  if (e == cudaSuccess) e = dalloc(c, &c->d_dead_list, N);
+  if (e == cudaSuccess) e = dalloc(c, &c->d_donor_g, N);
+  if (e == cudaSuccess) e = dalloc(c, &c->d_plan, 5 * (size_t)(cfg->world_size + 1));
   if (e == cudaSuccess) {
     c->stage_bytes = StageLayout(N).total;
-    e = dalloc(&c->d_stage, c->stage_bytes);
+    e = dalloc(c, &c->d_stage, c->stage_bytes);
   }
   if (e == cudaSuccess) {  // keep stream-ordered allocations mapped between calls
     cudaMemPool_t pool;
@@ -331,28 +365,28 @@ mcs_status mcs_create(const mcs_config* cfg, mcs_ctx** out) {
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     }
   }
-  if (e == cudaSuccess) e = dalloc(&c->d_part, (size_t)kSlotWords * nb * N);
-  if (e == cudaSuccess) e = dalloc(&c->d_meta, N);
-  if (e == cudaSuccess) e = dalloc(&c->d_to, N);
-  if (e == cudaSuccess) e = dalloc(&c->d_l, N);
-  if (e == cudaSuccess) e = dalloc(&c->d_psi, 6 * N);
-  if (e == cudaSuccess) e = dalloc(&c->d_grad, 6 * N);
-  if (e == cudaSuccess) e = dalloc(&c->d_hess, 21 * N);
-  if (e == cudaSuccess) e = dalloc(&c->d_flags, N);
-  if (e == cudaSuccess) e = dalloc(&c->d_e, N);
-  if (e == cudaSuccess) e = dalloc(&c->d_w, N);
-  if (e == cudaSuccess) e = cudaMalloc(&c->d_ladder, 16 * N);
-  if (e == cudaSuccess) e = cudaMalloc(&c->d_ladder_scan, 16 * N);
-  if (e == cudaSuccess) e = dalloc(&c->d_ncum, N);
-  if (e == cudaSuccess) e = dalloc(&c->d_donor, N);
-  if (e == cudaSuccess) e = dalloc(&c->d_partials, 2 * maxb);
-  if (e == cudaSuccess) e = dalloc(&c->d_ipartials, 2 * maxb);
-  if (e == cudaSuccess) e = dalloc(&c->d_scal, 1);
+  if (e == cudaSuccess) e = dalloc(c, &c->d_part, (size_t)kSlotWords * nb * N);
+  if (e == cudaSuccess) e = dalloc(c, &c->d_meta, N);
+  if (e == cudaSuccess) e = dalloc(c, &c->d_to, N);
+  if (e == cudaSuccess) e = dalloc(c, &c->d_l, N);
+  if (e == cudaSuccess) e = dalloc(c, &c->d_psi, 6 * N);
+  if (e == cudaSuccess) e = dalloc(c, &c->d_grad, 6 * N);
+  if (e == cudaSuccess) e = dalloc(c, &c->d_hess, 21 * N);
+  if (e == cudaSuccess) e = dalloc(c, &c->d_flags, N);
+  if (e == cudaSuccess) e = dalloc(c, &c->d_e, N);
+  if (e == cudaSuccess) e = dalloc(c, &c->d_w, N);
+  if (e == cudaSuccess) e = mem_alloc(c, &c->d_ladder, 16 * N);
+  if (e == cudaSuccess) e = mem_alloc(c, &c->d_ladder_scan, 16 * N);
+  if (e == cudaSuccess) e = dalloc(c, &c->d_ncum, N);
+  if (e == cudaSuccess) e = dalloc(c, &c->d_donor, N);
+  if (e == cudaSuccess) e = dalloc(c, &c->d_partials, 2 * maxb);
+  if (e == cudaSuccess) e = dalloc(c, &c->d_ipartials, 2 * maxb);
+  if (e == cudaSuccess) e = dalloc(c, &c->d_scal, 1);
   if (e == cudaSuccess) e = cudaMemset(c->d_scal, 0, sizeof(Scalars));
   if (e == cudaSuccess) e = cudaMallocHost((void**)&c->h_scal, sizeof(Scalars));
   if (e == cudaSuccess) {
     c->cub_temp_bytes = std::max(cub_temp_needed((int)N), sort_temp_needed((int)(nb * N), (int)K));
-    e = cudaMalloc(&c->d_cub_temp, c->cub_temp_bytes ? c->cub_temp_bytes : 1);
+    e = mem_alloc(c, &c->d_cub_temp, c->cub_temp_bytes);
   }
   for (int k = 0; k < 6 && e == cudaSuccess; ++k) e = cudaEventCreate(&c->ev[k]);
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
@@ -417,9 +451,9 @@ mcs_status mcs_add_keyframe(mcs_ctx* ctx, const float* mean3, const float* cov6,
   cudaStream_t st = ctx->stream;
   float *dm = nullptr, *dc = nullptr;
   int* bad = nullptr;
-  CUDA_TRY(ctx, cudaMallocAsync(&dm, sizeof(float) * 3 * n, st));
-  CUDA_TRY(ctx, cudaMallocAsync(&dc, sizeof(float) * 6 * n, st));
-  CUDA_TRY(ctx, cudaMallocAsync(&bad, sizeof(int), st));
+  CUDA_TRY(ctx, mem_alloc_async(ctx, (void**)&dm, sizeof(float) * 3 * n, st));
+  CUDA_TRY(ctx, mem_alloc_async(ctx, (void**)&dc, sizeof(float) * 6 * n, st));
+  CUDA_TRY(ctx, mem_alloc_async(ctx, (void**)&bad, sizeof(int), st));
   CUDA_TRY(ctx, cudaMemsetAsync(bad, 0, sizeof(int), st));
   CUDA_TRY(ctx, to_device(dm, mean3, sizeof(float) * 3 * n, st));
   CUDA_TRY(ctx, to_device(dc, cov6, sizeof(float) * 6 * n, st));
@@ -428,20 +462,20 @@ mcs_status mcs_add_keyframe(mcs_ctx* ctx, const float* mean3, const float* cov6,
   CUDA_TRY(ctx, cudaMemcpyAsync(&h_bad, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
   CUDA_TRY(ctx, cudaStreamSynchronize(st));
   if (h_bad) {
-    cudaFreeAsync(dm, st); cudaFreeAsync(dc, st); cudaFreeAsync(bad, st);
+    mem_free_async(ctx, dm, st); mem_free_async(ctx, dc, st); mem_free_async(ctx, bad, st);
     FAIL(ctx, MCS_E_INVALID_ARG, "%d keyframe points non-finite or covariance not SPD", h_bad);
   }
   KfHost kh;
   int bad_cell = 0, bad_extent = 0;
   cudaError_t e = kf_build(ctx, dm, dc, n, kh, &bad_cell, &bad_extent);
-  cudaFreeAsync(dm, st);
-  cudaFreeAsync(dc, st);
-  cudaFreeAsync(bad, st);
+  mem_free_async(ctx, dm, st);
+  mem_free_async(ctx, dc, st);
+  mem_free_async(ctx, bad, st);
   CUDA_TRY(ctx, e);
   if (bad_cell)
     FAIL(ctx, MCS_E_INVALID_ARG, "%d keyframe points outside the 21-bit cell range", bad_cell);
   if (bad_extent) {
-    if (kh.slots) cudaFree(kh.slots);
+    if (kh.slots) mem_free(ctx, kh.slots);
     FAIL(ctx, MCS_E_INVALID_ARG,
          "keyframe occupied extent exceeds 2047 x 2048 x 1024 cells at r = %g m",
          (double)ctx->cfg.voxel_resolution);
@@ -475,19 +509,19 @@ mcs_status mcs_set_particles(mcs_ctx* ctx, int32_t n, const float* pose12,
   float *tp = nullptr, *tk = nullptr;
   double* tl = nullptr;
   int* bad = nullptr;
-  CUDA_TRY(ctx, cudaMallocAsync(&tp, sizeof(float) * 12 * n, st));
-  CUDA_TRY(ctx, cudaMallocAsync(&bad, sizeof(int), st));
+  CUDA_TRY(ctx, mem_alloc_async(ctx, (void**)&tp, sizeof(float) * 12 * n, st));
+  CUDA_TRY(ctx, mem_alloc_async(ctx, (void**)&bad, sizeof(int), st));
   CUDA_TRY(ctx, cudaMemsetAsync(bad, 0, sizeof(int), st));
   CUDA_TRY(ctx, to_device(tp, pose12, sizeof(float) * 12 * n, st));
   validate_poses_kernel<<<(n + 255) / 256, 256, 0, st>>>(tp, n, bad);
   if (kf_pose12 && K > 0) {
     const long long np = (long long)n * K;
-    CUDA_TRY(ctx, cudaMallocAsync(&tk, sizeof(float) * 12 * np, st));
+    CUDA_TRY(ctx, mem_alloc_async(ctx, (void**)&tk, sizeof(float) * 12 * np, st));
     CUDA_TRY(ctx, to_device(tk, kf_pose12, sizeof(float) * 12 * np, st));
     validate_poses_kernel<<<(int)((np + 255) / 256), 256, 0, st>>>(tk, np, bad);
   }
   if (cum_loglik) {
-    CUDA_TRY(ctx, cudaMallocAsync(&tl, sizeof(double) * n, st));
+    CUDA_TRY(ctx, mem_alloc_async(ctx, (void**)&tl, sizeof(double) * n, st));
     CUDA_TRY(ctx, to_device(tl, cum_loglik, sizeof(double) * n, st));
   }
   int h_bad = 0;
@@ -500,10 +534,10 @@ mcs_status mcs_set_particles(mcs_ctx* ctx, int32_t n, const float* pose12,
     for (double v : hl) lbad |= !std::isfinite(v);
   }
   if (h_bad || lbad) {
-    cudaFreeAsync(tp, st);
-    if (tk) cudaFreeAsync(tk, st);
-    if (tl) cudaFreeAsync(tl, st);
-    cudaFreeAsync(bad, st);
+    mem_free_async(ctx, tp, st);
+    if (tk) mem_free_async(ctx, tk, st);
+    if (tl) mem_free_async(ctx, tl, st);
+    mem_free_async(ctx, bad, st);
     FAIL(ctx, MCS_E_INVALID_ARG, "non-finite or non-orthonormal pose / non-finite L (%d)", h_bad);
   }
   // commit
@@ -526,10 +560,10 @@ mcs_status mcs_set_particles(mcs_ctx* ctx, int32_t n, const float* pose12,
   }
   fill_double_kernel<<<(n + 255) / 256, 256, 0, st>>>(ctx->d_w, n, 1.0 / n);
   CUDA_TRY(ctx, cudaGetLastError());
-  cudaFreeAsync(tp, st);
-  if (tk) cudaFreeAsync(tk, st);
-  if (tl) cudaFreeAsync(tl, st);
-  cudaFreeAsync(bad, st);
+  mem_free_async(ctx, tp, st);
+  if (tk) mem_free_async(ctx, tk, st);
+  if (tl) mem_free_async(ctx, tl, st);
+  mem_free_async(ctx, bad, st);
   CUDA_TRY(ctx, cudaStreamSynchronize(st));
   ctx->N = n;
   // global index base of this shard (collective over ranks)
@@ -553,10 +587,10 @@ mcs_status mcs_get_particles(mcs_ctx* ctx, float* pose12, float* kf_pose12, doub
   if (n == 0) return MCS_OK;
   if (pose12) {
     float* tp = nullptr;
-    CUDA_TRY(ctx, cudaMallocAsync(&tp, sizeof(float) * 12 * n, st));
+    CUDA_TRY(ctx, mem_alloc_async(ctx, (void**)&tp, sizeof(float) * 12 * n, st));
     soa_to_aos_kernel<<<(n + 255) / 256, 256, 0, st>>>(ctx->d_pose, n, ctx->capN, tp);
     CUDA_TRY(ctx, cudaMemcpyAsync(pose12, tp, sizeof(float) * 12 * n, cudaMemcpyDefault, st));
-    cudaFreeAsync(tp, st);
+    mem_free_async(ctx, tp, st);
   }
   if (kf_pose12 && K > 0)
     CUDA_TRY(ctx, cudaMemcpy2DAsync(kf_pose12, sizeof(float) * 12 * K, ctx->d_kfpose,
@@ -726,12 +760,12 @@ mcs_status mcs_eval(mcs_ctx* ctx, const float* scan_mean3, const float* scan_cov
   float *dH = nullptr, *db = nullptr;
   int32_t *dn = nullptr, *dk = nullptr;
   uint8_t* dloop = nullptr;
-  CUDA_TRY(ctx, cudaMallocAsync(&dl, 8 * NS, st));
-  CUDA_TRY(ctx, cudaMallocAsync(&dH, 84 * NS, st));
-  CUDA_TRY(ctx, cudaMallocAsync(&db, 24 * NS, st));
-  CUDA_TRY(ctx, cudaMallocAsync(&dn, 4 * NS, st));
-  CUDA_TRY(ctx, cudaMallocAsync(&dk, 4 * NS, st));
-  CUDA_TRY(ctx, cudaMallocAsync(&dloop, ctx->N, st));
+  CUDA_TRY(ctx, mem_alloc_async(ctx, (void**)&dl, 8 * NS, st));
+  CUDA_TRY(ctx, mem_alloc_async(ctx, (void**)&dH, 84 * NS, st));
+  CUDA_TRY(ctx, mem_alloc_async(ctx, (void**)&db, 24 * NS, st));
+  CUDA_TRY(ctx, mem_alloc_async(ctx, (void**)&dn, 4 * NS, st));
+  CUDA_TRY(ctx, mem_alloc_async(ctx, (void**)&dk, 4 * NS, st));
+  CUDA_TRY(ctx, mem_alloc_async(ctx, (void**)&dloop, ctx->N, st));
   launch_select(ctx, kSelectEval);
   launch_sweep(ctx, n_pts);
   launch_combine(ctx, n_pts, kCombineEval, dl, dH, db, dn, dk, dloop);
@@ -742,8 +776,8 @@ mcs_status mcs_eval(mcs_ctx* ctx, const float* scan_mean3, const float* scan_cov
   if (slot_n) CUDA_TRY(ctx, cudaMemcpyAsync(slot_n, dn, 4 * NS, cudaMemcpyDefault, st));
   if (slot_kf) CUDA_TRY(ctx, cudaMemcpyAsync(slot_kf, dk, 4 * NS, cudaMemcpyDefault, st));
   if (loop) CUDA_TRY(ctx, cudaMemcpyAsync(loop, dloop, ctx->N, cudaMemcpyDefault, st));
-  cudaFreeAsync(dl, st); cudaFreeAsync(dH, st); cudaFreeAsync(db, st);
-  cudaFreeAsync(dn, st); cudaFreeAsync(dk, st); cudaFreeAsync(dloop, st);
+  mem_free_async(ctx, dl, st); mem_free_async(ctx, dH, st); mem_free_async(ctx, db, st);
+  mem_free_async(ctx, dn, st); mem_free_async(ctx, dk, st); mem_free_async(ctx, dloop, st);
   CUDA_TRY(ctx, cudaStreamSynchronize(st));
   return MCS_OK;
 }
@@ -756,18 +790,18 @@ mcs_status mcs_resample(mcs_ctx* ctx, const double* e, const uint8_t* dead, int3
   cudaStream_t st = ctx->stream;
   uint8_t* dd = nullptr;
   double* de = nullptr;
-  CUDA_TRY(ctx, cudaMallocAsync(&dd, n, st));
-  CUDA_TRY(ctx, cudaMallocAsync(&de, 8 * (size_t)n, st));
+  CUDA_TRY(ctx, mem_alloc_async(ctx, (void**)&dd, n, st));
+  CUDA_TRY(ctx, mem_alloc_async(ctx, (void**)&de, 8 * (size_t)n, st));
   CUDA_TRY(ctx, to_device(dd, dead, n, st));
   CUDA_TRY(ctx, to_device(de, e, 8 * (size_t)n, st));
   int32_t* ddon = nullptr;
-  CUDA_TRY(ctx, cudaMallocAsync(&ddon, 4 * (size_t)n, st));
+  CUDA_TRY(ctx, mem_alloc_async(ctx, (void**)&ddon, 4 * (size_t)n, st));
   if (launch_resample_only(ctx, de, dd, n, u, ddon) != MCS_OK) CUDA_TRY(ctx, cudaGetLastError());
   CUDA_TRY(ctx, cudaGetLastError());
   CUDA_TRY(ctx, cudaMemcpyAsync(donor_out, ddon, 4 * (size_t)n, cudaMemcpyDefault, st));
   CUDA_TRY(ctx, cudaMemcpyAsync(ctx->h_scal, ctx->d_scal, sizeof(Scalars), cudaMemcpyDeviceToHost,
                                 st));
-  cudaFreeAsync(dd, st); cudaFreeAsync(de, st); cudaFreeAsync(ddon, st);
+  mem_free_async(ctx, dd, st); mem_free_async(ctx, de, st); mem_free_async(ctx, ddon, st);
   CUDA_TRY(ctx, cudaStreamSynchronize(st));
   if (ctx->h_scal->status == MCS_E_DEGENERATE)
     FAIL(ctx, MCS_E_DEGENERATE, "every particle dead (S:381)");
@@ -794,11 +828,11 @@ mcs_status mcs_predict(mcs_ctx* ctx, const float* dT12, const double* cov36, uin
         FAIL(ctx, MCS_E_INVALID_ARG, "covariance not finite/symmetric");
   cudaStream_t st = ctx->stream;
   double* d = nullptr;
-  CUDA_TRY(ctx, cudaMallocAsync(&d, sizeof(double) * 84, st));
+  CUDA_TRY(ctx, mem_alloc_async(ctx, (void**)&d, sizeof(double) * 84, st));
   CUDA_TRY(ctx, cudaMemcpyAsync(d, hbuf, sizeof(double) * 48, cudaMemcpyHostToDevice, st));
   CUDA_TRY(ctx, cudaMemsetAsync(ctx->d_bad, 0, sizeof(int), st));
   const mcs_status s = launch_predict(ctx, d, ctx->d_bad, seed, frame, vertical_sigma);
-  cudaFreeAsync(d, st);
+  mem_free_async(ctx, d, st);
   CUDA_TRY(ctx, cudaStreamSynchronize(st));
   if (s == MCS_E_INVALID_ARG) FAIL(ctx, s, "covariance neither SPD nor zero");
   if (s != MCS_OK) CUDA_TRY(ctx, cudaGetLastError());
@@ -814,13 +848,13 @@ mcs_status mcs_overlap(mcs_ctx* ctx, const float* scan_mean3, int32_t n_pts, con
   cudaStream_t st = ctx->stream;
   char* d = nullptr;
   const size_t bm = (sizeof(float) * 3 * (size_t)n_pts + 255) & ~(size_t)255;  // keep alignment
-  CUDA_TRY(ctx, cudaMallocAsync(&d, bm + 64 + 8, st));
+  CUDA_TRY(ctx, mem_alloc_async(ctx, (void**)&d, bm + 64 + 8, st));
   CUDA_TRY(ctx, to_device(d, scan_mean3, bm, st));
   CUDA_TRY(ctx, to_device(d + bm, rel12, 48, st));
   unsigned long long cnt = 0;
   const mcs_status s = launch_overlap(ctx, (const float*)d, n_pts, (const float*)(d + bm), kf,
                                       (unsigned long long*)(d + bm + 64), &cnt);
-  cudaFreeAsync(d, st);
+  mem_free_async(ctx, d, st);
   if (s != MCS_OK) CUDA_TRY(ctx, cudaGetLastError());
   *out_rate = (double)cnt / (double)n_pts;
   return s;
@@ -831,7 +865,7 @@ mcs_status mcs_snapshot(mcs_ctx* ctx) {
   const size_t bp = sizeof(float) * 12 * ctx->capN, bk = sizeof(float) * 12 * ctx->capN * ctx->capK,
                bl = sizeof(double) * ctx->capN;
   if (!ctx->d_snapshot) {
-    CUDA_TRY(ctx, cudaMalloc(&ctx->d_snapshot, bp + bk + bl));
+    CUDA_TRY(ctx, mem_alloc(ctx, &ctx->d_snapshot, bp + bk + bl));
     ctx->snapshot_bytes = bp + bk + bl;
   }
   char* s = (char*)ctx->d_snapshot;

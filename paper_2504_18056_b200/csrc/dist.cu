@@ -329,7 +329,7 @@ mcs_status dist_allgather_host(mcs_ctx* c, const void* send, void* recv, size_t 
   if (c->nccl_comm) {
     NcclApi* a = nccl();
     char* d = nullptr;
-    if (cudaMalloc(&d, bytes * (c->world + 1)) != cudaSuccess) return MCS_E_OUT_OF_MEMORY;
+    if (mem_alloc(c, (void**)&d, bytes * (c->world + 1)) != cudaSuccess) return MCS_E_OUT_OF_MEMORY;
     mcs_status st = MCS_OK;
     if (cudaMemcpyAsync(d, send, bytes, cudaMemcpyHostToDevice, c->stream) != cudaSuccess)
       st = MCS_E_CUDA;
@@ -340,7 +340,7 @@ mcs_status dist_allgather_host(mcs_ctx* c, const void* send, void* recv, size_t 
                                          c->stream) != cudaSuccess ||
                          cudaStreamSynchronize(c->stream) != cudaSuccess))
       st = MCS_E_CUDA;
-    cudaFree(d);
+    mem_free(c, d);
     return st;
   }
   return c->tr->allgather(c->tr->user, c->rank, send, recv, bytes) ? MCS_E_NCCL : MCS_OK;

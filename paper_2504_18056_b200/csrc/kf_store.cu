@@ -114,14 +114,14 @@ cudaError_t kf_build(mcs_ctx* c, const float* d_mean3, const float* d_cov6, int 
     e = (x);                            \
     if (e != cudaSuccess) goto cleanup; \
   } while (0)
-  CK(cudaMallocAsync(&keys, sizeof(unsigned long long) * n, st));
-  CK(cudaMallocAsync(&skeys, sizeof(unsigned long long) * n, st));
-  CK(cudaMallocAsync(&idx, sizeof(int) * n, st));
-  CK(cudaMallocAsync(&sidx, sizeof(int) * n, st));
-  CK(cudaMallocAsync(&head, sizeof(int) * n, st));
-  CK(cudaMallocAsync(&cid, sizeof(int) * n, st));
-  CK(cudaMallocAsync(&bad, sizeof(int), st));
-  CK(cudaMallocAsync(&bbox, sizeof(int) * 6, st));
+  CK(mem_alloc_async(c, (void**)&keys, sizeof(unsigned long long) * n, st));
+  CK(mem_alloc_async(c, (void**)&skeys, sizeof(unsigned long long) * n, st));
+  CK(mem_alloc_async(c, (void**)&idx, sizeof(int) * n, st));
+  CK(mem_alloc_async(c, (void**)&sidx, sizeof(int) * n, st));
+  CK(mem_alloc_async(c, (void**)&head, sizeof(int) * n, st));
+  CK(mem_alloc_async(c, (void**)&cid, sizeof(int) * n, st));
+  CK(mem_alloc_async(c, (void**)&bad, sizeof(int), st));
+  CK(mem_alloc_async(c, (void**)&bbox, sizeof(int) * 6, st));
   CK(cudaMemsetAsync(bad, 0, sizeof(int), st));
   CK(cudaMemcpyAsync(bbox, bbox_init, sizeof(bbox_init), cudaMemcpyHostToDevice, st));
   {
@@ -131,7 +131,7 @@ cudaError_t kf_build(mcs_ctx* c, const float* d_mean3, const float* d_cov6, int 
     cub::DeviceRadixSort::SortPairs(nullptr, tb1, keys, skeys, idx, sidx, n, 0, 63, st);
     cub::DeviceScan::ExclusiveSum(nullptr, tb2, head, cid, n, st);
     size_t tb = tb1 > tb2 ? tb1 : tb2;
-    CK(cudaMallocAsync(&temp, tb, st));
+    CK(mem_alloc_async(c, (void**)&temp, tb, st));
     CK(cub::DeviceRadixSort::SortPairs(temp, tb, keys, skeys, idx, sidx, n, 0, 63, st));
     heads_kernel<<<g, 256, 0, st>>>(skeys, n, head);
     CK(cudaGetLastError());
@@ -164,7 +164,7 @@ cudaError_t kf_build(mcs_ctx* c, const float* d_mean3, const float* d_cov6, int 
     out.n_cells = n_cells;
     out.n_points = n;
     // cap probe slots + one always-empty sentinel slot (index cap) that out-of-bbox queries read
-    CK(cudaMalloc(&out.slots, sizeof(float4) * 4 * (size_t)(cap + 1)));
+    CK(mem_alloc(c, (void**)&out.slots, sizeof(float4) * 4 * (size_t)(cap + 1)));
     m.slots = out.slots;
     out.meta = m;
     init_slots_kernel<<<(cap + 1 + 255) / 256, 256, 0, st>>>(out.slots, cap + 1);
@@ -173,15 +173,15 @@ cudaError_t kf_build(mcs_ctx* c, const float* d_mean3, const float* d_cov6, int 
     CK(cudaGetLastError());
   }
 cleanup:
-  cudaFreeAsync(keys, st);
-  cudaFreeAsync(skeys, st);
-  cudaFreeAsync(idx, st);
-  cudaFreeAsync(sidx, st);
-  cudaFreeAsync(head, st);
-  cudaFreeAsync(cid, st);
-  cudaFreeAsync(bad, st);
-  cudaFreeAsync(bbox, st);
-  if (temp) cudaFreeAsync(temp, st);
+  mem_free_async(c, keys, st);
+  mem_free_async(c, skeys, st);
+  mem_free_async(c, idx, st);
+  mem_free_async(c, sidx, st);
+  mem_free_async(c, head, st);
+  mem_free_async(c, cid, st);
+  mem_free_async(c, bad, st);
+  mem_free_async(c, bbox, st);
+  if (temp) mem_free_async(c, temp, st);
 #undef CK
   return e;
 }

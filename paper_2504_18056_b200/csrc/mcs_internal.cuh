@@ -91,6 +91,7 @@ struct mcs_ctx {
   int dev = 0;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
+  mcs_allocator alloc{};      // user device-memory hook (alloc.alloc == nullptr: CUDA's own)
   std::string err;
   mcs_status sticky = MCS_OK;
   bool profiling = false;
@@ -179,6 +180,13 @@ enum { kSelectUpdate = 0, kSelectEval = 1, kSelectWeight = 2 };
 void launch_select(mcs_ctx* c, int mode);
 // a2
 void launch_sweep(mcs_ctx* c, int S);
+
+// device memory through the allocator hook (include/mcs.h): persistent buffers (context
+// lifetime) and stream-ordered temporaries
+cudaError_t mem_alloc(mcs_ctx* c, void** p, size_t bytes);
+void mem_free(mcs_ctx* c, void* p);
+cudaError_t mem_alloc_async(mcs_ctx* c, void** p, size_t bytes, cudaStream_t st);
+void mem_free_async(mcs_ctx* c, void* p, cudaStream_t st);
 // a3; modes: per-slot eval outputs; GN update and/or L += l with the first a5 reduction
 enum { kCombineEval = 0, kCombineUpdateWeight = 1, kCombineUpdate = 2, kCombineWeight = 3 };
 void launch_combine(mcs_ctx* c, int S, int mode, double* slot_l, float* slot_H21,

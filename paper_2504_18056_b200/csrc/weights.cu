@@ -434,15 +434,16 @@ static mcs_status plan_global(mcs_ctx* c, uint32_t U, long long* n_send_items,
 
 static mcs_status ensure_xfer(mcs_ctx* c, long long items) {
   if ((size_t)items <= c->xfer_cap_items) return MCS_OK;
-  cudaFree(c->d_send);
-  cudaFree(c->d_recv);
-  cudaFree(c->d_pack_src);
+  mem_free(c, c->d_send);
+  mem_free(c, c->d_recv);
+  mem_free(c, c->d_pack_src);
   c->d_send = c->d_recv = nullptr;
   c->d_pack_src = nullptr;
   const size_t cap = (size_t)items + (items >> 2) + 1024;
   const size_t bytes = cap * (sizeof(float) * 12 * (1 + c->capK) + 16);
-  if (cudaMalloc(&c->d_send, bytes) != cudaSuccess || cudaMalloc(&c->d_recv, bytes) != cudaSuccess ||
-      cudaMalloc(&c->d_pack_src, sizeof(int32_t) * cap) != cudaSuccess)
+  if (mem_alloc(c, (void**)&c->d_send, bytes) != cudaSuccess ||
+      mem_alloc(c, (void**)&c->d_recv, bytes) != cudaSuccess ||
+      mem_alloc(c, (void**)&c->d_pack_src, sizeof(int32_t) * cap) != cudaSuccess)
     return MCS_E_OUT_OF_MEMORY;
   c->xfer_cap_items = cap;
   return MCS_OK;

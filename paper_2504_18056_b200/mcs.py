@@ -58,7 +58,44 @@ class Config(C.Structure):
         ("corr_mode", C.c_int32),
         ("nn_radius", C.c_float),
         ("clone_split", C.c_int32),
+        ("allocator", C.c_void_p),
     ]
+
+
+ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
+FREE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_void_p, C.c_void_p)
+
+
+class Allocator(C.Structure):
+    """mcs_allocator (include/mcs.h): the device-memory hook."""
+    _fields_ = [("alloc", ALLOC_FN), ("free", FREE_FN), ("user", C.c_void_p)]
+
+
+class TorchAllocator:
+    """Routes every libmcs device buffer through PyTorch's caching allocator, on the stream the
+    library passes (its context stream), so library and torch tensors share one memory pool."""
+
+    def __init__(self, device=None):
+        import torch
+        self._torch = torch
+        self.device = torch.cuda.current_device() if device is None else int(device)
+
+        def _alloc(nbytes, stream, user):
+            try:
+                return torch.cuda.caching_allocator_alloc(int(nbytes), self.device,
+                                                          int(stream or 0))
+            except Exception:  # out of memory -> NULL -> MCS_E_OUT_OF_MEMORY
+                return None
+
+        def _free(ptr, stream, user):
+            torch.cuda.caching_allocator_delete(int(ptr))
+
+        self._fns = (ALLOC_FN(_alloc), FREE_FN(_free))
+        self.struct = Allocator(self._fns[0], self._fns[1], None)
+
+    @property
+    def ptr(self):
+        return C.cast(C.pointer(self.struct), C.c_void_p)
 
 
 CORR_CELL, CORR_NN27 = 0, 1
@@ -166,6 +203,14 @@ class Context:
         self._keep = []
         tr = cfg_kw.pop("transport", None)
         nid = cfg_kw.pop("nccl_unique_id", None)
+        al = cfg_kw.pop("allocator", None)
+        if al is not None:
+            self._keep.append(al)
+            if isinstance(al, TorchAllocator):
+                al = al.ptr
+            elif isinstance(al, Allocator):
+                al = C.cast(C.pointer(al), C.c_void_p)
+            cfg_kw["allocator"] = al
         if tr is not None:
             cfg_kw["transport"] = tr.ptr if isinstance(tr, InprocTransport) else tr
             self._keep.append(tr)

@@ -45,7 +45,11 @@ def test_state_bytes_linear_in_keyframes_and_paper_memory_figure():
 
 def test_create_validates_before_touching_the_device():
     bad = [dict(capacity_particles=0), dict(neighbor_count=5), dict(voxel_resolution=0.3),
-           dict(abi_version=99), dict(world_size=2, rank=1), dict(capacity_particles=(1 << 21) + 1)]
+           dict(abi_version=99), dict(world_size=2, rank=1), dict(capacity_particles=(1 << 21) + 1),
+           dict(corr_mode=1, nn_radius=0.0), dict(corr_mode=1, nn_radius=1.0), dict(corr_mode=3),
+           dict(clone_split=2),
+           dict(allocator=mcs.Allocator(mcs.mcs.ALLOC_FN(lambda n, s, u: None),
+                                        mcs.mcs.FREE_FN(), None))]
     for kw in bad:
         base = dict(capacity_particles=100, capacity_keyframes=4, capacity_scan_points=64)
         base.update(kw)

@@ -153,3 +153,27 @@ def test_clone_split_parity():
     assert abs(gs["weight"].sum() - 1) < 1e-12
     _, _, w_ref, _, _ = oracle.weights(st["L"])
     np.testing.assert_allclose(gs["weight"], w_ref, rtol=1e-12, atol=1e-300)
+
+
+# ------------------------------------------------------------------ allocator hook (mcs_allocator)
+def test_torch_allocator_hook_gives_identical_results():
+    import torch
+    s = synth.c1()
+    with _ctx(s) as ctx:
+        g0 = ctx.update(s.scan_mean3, s.scan_cov6, s.D_now, s.U)
+        st0 = ctx.get_particles()
+    torch.cuda.synchronize()
+    base = torch.cuda.memory_allocated()
+    ctx = _ctx(s, allocator=mcs.TorchAllocator())
+    during = torch.cuda.memory_allocated()
+    g1 = ctx.update(s.scan_mean3, s.scan_cov6, s.D_now, s.U)
+    st1 = ctx.get_particles()
+    ctx.close()
+    torch.cuda.synchronize()
+    after = torch.cuda.memory_allocated()
+    assert during - base >= mcs.state_bytes_per_particle(s.K) * s.N  # state lives in torch's pool
+    assert after == base                                              # and is all returned
+    for k in g0:
+        np.testing.assert_array_equal(np.asarray(g0[k]), np.asarray(g1[k]), err_msg=k)
+    for k in ("pose12", "kf_pose12", "L"):
+        np.testing.assert_array_equal(st0[k], st1[k])
