@@ -378,6 +378,12 @@ class Keyframes:
     def K(self):
         return len(self.maps)
 
+    def append(self, mean3, cov6, D_k: float, r: float):
+        """Register one more keyframe."""
+        self.maps.append(Map(mean3, cov6, r))
+        self.D = np.append(self.D, float(D_k))
+        self._ptrs = (C.c_void_p * len(self.maps))(*[m.ptr for m in self.maps])
+
 
 def particles(cfg: Config, kfs: Keyframes, D_now, pose12, kf_pose12, scan_mean3, scan_cov6,
               idx=None, apply_update=True, slots=False):

@@ -7,6 +7,8 @@ from .mcs import (ABI_VERSION, CORR_CELL, CORR_NN27, Allocator, Config, Context,
                   header_symbols, load, nccl_unique_id, plan_ladder, plan_migration,
                   state_bytes_per_particle, TorchAllocator, unpack_h21)
 
-__all__ = ["ABI_VERSION", "CORR_CELL", "CORR_NN27", "Allocator", "Config", "Context", "InprocTransport", "MCSError", "default_config",
+from .slam import MonteCarloSLAM, in_elevator
+
+__all__ = ["MonteCarloSLAM", "in_elevator", "ABI_VERSION", "CORR_CELL", "CORR_NN27", "Allocator", "Config", "Context", "InprocTransport", "MCSError", "default_config",
            "header_symbols", "load", "nccl_unique_id", "plan_ladder", "plan_migration",
            "state_bytes_per_particle", "TorchAllocator", "unpack_h21"]

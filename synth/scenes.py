@@ -463,3 +463,57 @@ def subset(scene: Scene, N: int) -> Scene:
     import dataclasses
     return dataclasses.replace(scene, pose12=np.ascontiguousarray(scene.pose12[:N]),
                                kf_pose12=np.ascontiguousarray(scene.kf_pose12[:N]))
+
+
+# ------------------------------------------------------------------ trajectories (multi-frame)
+@dataclass
+class Trajectory:
+    name: str
+    r: float
+    gap: int
+    scans: list                # [(mean3 (S,3) f32, cov6 (S,6) f32)] in the sensor frame
+    clouds: list               # [(mean3, cov6)] the whole frame downsampled at r (keyframe /
+                               # overlap cloud)
+    gt: np.ndarray             # (F, 4, 4) true sensor poses
+    odom: np.ndarray           # (F, 4, 4) drifting odometry poses T^o_t
+    odom_cov: np.ndarray       # (6, 6) covariance of one relative motion, twist order (rho, phi)
+    D: np.ndarray              # (F,) cumulative odometry path length (R14)
+    U: np.ndarray              # (F,) uint32 resampling uniforms
+
+    @property
+    def F(self):
+        return len(self.scans)
+
+
+def corridor_lap(seed: int = 0, n_frames: int = 90, step: float = 2.0, S: int = 1024,
+                 r: float = 0.5, gap: int = 10, sig_t: float = 0.03, sig_r: float = 0.003,
+                 n_az: int = 360, n_el: int = 64, arc0: float = 0.0) -> Trajectory:
+    """A lap of the loop corridor (perimeter 160 m) and back past the start: GT poses every
+    `step` metres, LiDAR-like scans at r/2 subsampled to S points, and an odometry whose every
+    relative motion carries N(0, diag(sig_t^2 I, sig_r^2 I)) noise, so it drifts and the loop
+    must be closed by the filter."""
+    world = loop_corridor(seed)
+    arcs = arc0 + step * np.arange(n_frames)
+    gt = np.stack([loop_path(a) for a in arcs])
+    g = rng(seed, "traj/odom")
+    odom = np.empty_like(gt)
+    odom[0] = gt[0]
+    for k in range(1, n_frames):
+        rel = np.linalg.inv(gt[k - 1]) @ gt[k]
+        odom[k] = odom[k - 1] @ perturb(rel, sig_t, sig_r, g, 1)[0]
+    scans, clouds = [], []
+    for k in range(n_frames):
+        g = rng(seed, f"traj/scan{k}")
+        pw = raycast(world, gt[k], n_az, n_el, g)
+        Ti = np.linalg.inv(gt[k])
+        ps = (pw @ Ti[:3, :3].T + Ti[:3, 3]).astype(np.float32)
+        full = downsample(ps, r, g)
+        clouds.append((np.ascontiguousarray(full), covariances(full)))
+        fine = downsample(ps, r / 2, g)
+        sel = np.sort(g.choice(len(fine), S, replace=False))
+        scans.append((np.ascontiguousarray(fine[sel]), covariances(fine)[sel]))
+    D = np.concatenate([[0.0], np.cumsum(np.linalg.norm(np.diff(odom[:, :3, 3], axis=0),
+                                                          axis=1))])
+    cov = np.diag([sig_t ** 2] * 3 + [sig_r ** 2] * 3)
+    U = rng(seed, "traj/U").integers(0, 2**32, n_frames).astype(np.uint32)
+    return Trajectory("corridor_lap", r, gap, scans, clouds, gt, odom, cov, D, U)
