@@ -100,6 +100,15 @@ def measured_peaks():
     return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
 
 
+def own_peaks():
+    """bench/peaks.cu results committed under profiles/ (L2 random-gather bandwidth etc.)."""
+    p = os.path.join(ROOT, "profiles", "r01_peaks.json")
+    try:
+        return json.load(open(p))
+    except Exception:
+        return {}
+
+
 def committed_traffic():
     p = os.path.join(ROOT, "profiles", "sweep_traffic.json")
     if os.path.exists(p):
@@ -171,6 +180,15 @@ def run_reference(args):
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
+
+
+def gather_roofline(gather_bytes, sweep_ms):
+    """The co-bound: algorithmic probe bytes (56 B per matched triple, 8 B per
+    unmatched) per sweep vs the L2 random 32-B gather bandwidth measured by bench/peaks.cu."""
+    peak = own_peaks().get("l2_gather_32B_GBps")
+    ach = gather_bytes / (sweep_ms * 1e-3) / 1e9
+    return {"achieved_GBps": ach, "peak_GBps": peak, "frac": (ach / peak) if peak else None,
+            "peak_source": "profiles/r01_peaks.json (bench/peaks.cu, measured)" if peak else None}
 
 
 # ------------------------------------------------------------------ GPU arm
@@ -296,7 +314,8 @@ def run_gpu(args):
                      "peak_source": f"148 SM x 128 FP32 lanes x 2 x {sm_mhz:.0f} MHz "
                                     f"({peak_src} sm_max_mhz)",
                      "flops_per_launch": flops, "sweep_ms": sweep_avg,
-                     "l2_gather_GBps": gather / (sweep_avg * 1e-3) / 1e9},
+                     "l2_gather_GBps": gather / (sweep_avg * 1e-3) / 1e9,
+                     "gather": gather_roofline(gather, sweep_avg)},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(36 * S),
                 "d2h_bytes_per_step": int(16 * N + 4 + 8), "ms_per_step": 1e3 * e2e_mean},
         "gpu_launches": LAUNCHES_PER_UPDATE * args.steps,
