@@ -9,9 +9,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 VARIANTS = {
-    "a2": [],
-    "b4": ["MCS_SWEEP_AHEAD=4"],
-    "a1": ["MCS_SWEEP_AHEAD=1"],
+    "base": [],
 }
 OUT = os.path.join(ROOT, "bench", "_variants")
 

@@ -122,10 +122,10 @@ __global__ void __launch_bounds__(kSweepThreads, MCS_SWEEP_MINBLOCKS)
     // q = kR mu + kt with the pinned chain fma(R2, z, fma(R1, y, fma(R0, x, t))) per lane (R27)
     p.qx = __fmaf_rn(R02, A.z, __fmaf_rn(R01, A.y, __fmaf_rn(R00, A.x, tx)));
     p.qyz = fma2(Ryz2, bc(A.z), fma2(Ryz1, bc(A.y), fma2(Ryz0, bc(A.x), tyz)));
-    // floor(q / r) (exact power-of-two scaling, R27) -> bbox-local cell coordinates
-    const unsigned int dx =
-        (unsigned)__float_as_int(__fadd_rd(__fmul_rn(p.qx, inv_r), kMagic)) - offx;
-    const float2 fyz = __fadd2_rd(mul2(p.qyz, bc(inv_r)), bc(kMagic));
+    // floor(q / r) -> bbox-local cell coordinates.  q * (1/r) is exact (r a power of two,
+    // R27), so one fma rounded toward -inf equals the separate multiply and add
+    const unsigned int dx = (unsigned)__float_as_int(__fmaf_rd(p.qx, inv_r, kMagic)) - offx;
+    const float2 fyz = __ffma2_rd(p.qyz, bc(inv_r), bc(kMagic));
     const unsigned int dy = (unsigned)__float_as_int(fyz.x) - offy;
     const unsigned int dz = (unsigned)__float_as_int(fyz.y) - offz;
     // outside the keyframe's bbox: a key no slot holds, probing the always-empty sentinel slot
@@ -267,9 +267,8 @@ __global__ void __launch_bounds__(kSweepThreads, MCS_SWEEP_MINBLOCKS)
   // lower (oz, oy, ox) index.  Plain loop: a flagged variant, not the timed path.
   auto nn27_point = [&](int j) {
     Probe p = locate(j);
-    const unsigned int bx =
-        (unsigned)__float_as_int(__fadd_rd(__fmul_rn(p.qx, inv_r), kMagic)) - offx;
-    const float2 fyz = __fadd2_rd(mul2(p.qyz, bc(inv_r)), bc(kMagic));
+    const unsigned int bx = (unsigned)__float_as_int(__fmaf_rd(p.qx, inv_r, kMagic)) - offx;
+    const float2 fyz = __ffma2_rd(p.qyz, bc(inv_r), bc(kMagic));
     const unsigned int by = (unsigned)__float_as_int(fyz.x) - offy;
     const unsigned int bz = (unsigned)__float_as_int(fyz.y) - offz;
     int best = -1;
