@@ -132,7 +132,7 @@ __global__ void __launch_bounds__(kSweepThreads, MCS_SWEEP_MINBLOCKS)
     const bool in = (dx < m.ex) & (dy < m.ey) & (dz < m.ez);
     const unsigned int lk = local_key(dx, dy, dz);
     p.key = in ? lk : kNoKey32;
-    p.h = in ? (slot_hash(lk, m.shift) & m.mask) : m.mask + 1;
+    p.h = in ? slot_hash(lk, m.shift) : m.mask + 1;  // the hash is < cap already
     return p;
   };
   // the (unconditional) first-probe loads; volatile: the compiler may not sink them towards
