@@ -53,6 +53,17 @@ def build(force: bool = False, verbose: bool = False, defines=(), lib: str | Non
         BUILD, LIB = saved
 
 
+CHECKED_LIB = os.path.join(HERE, "libmcs_checked.so")
+
+
+def build_checked(force: bool = False) -> str:
+    """The same library with the device-side invariant checks compiled in (-DMCS_DEVICE_CHECKS:
+    index bounds, probe-loop termination, ladder/donor invariants; a failure traps).  Used by
+    tests/test_gpu_checked.py; never the product path."""
+    return build(force=force, defines=["MCS_DEVICE_CHECKS"], lib=CHECKED_LIB,
+                 build_dir=os.path.join(HERE, "_build_checked"))
+
+
 def _build(force: bool, verbose: bool, defines: list[str]) -> str:
     os.makedirs(BUILD, exist_ok=True)
     hdrs = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(ROOT, "include", "mcs.h"),

@@ -76,6 +76,7 @@ __global__ void aggregate_insert_kernel(const unsigned long long* __restrict__ s
     unsigned int prev = atomicCAS(kw, kEmptyKey32, lk);
     if (prev == kEmptyKey32) break;
     h = (h + 1) & m.mask;
+    MCS_DCHECK(h != (slot_hash(lk, m.shift) & m.mask));  // table never full (load <= 1/4)
   }
   // layout (mcs_internal.cuh): the (y, z) pairs sit in aligned register pairs for the sweep's
   // packed FFMA2 math; s[] = (xx, xy, xz, yy, yz, zz)

@@ -19,6 +19,23 @@
 
 namespace mcs {
 
+// Device-side invariant checks: compiled in with -DMCS_DEVICE_CHECKS (the checked build that
+// tests/test_gpu_checked.py runs), nothing otherwise.  A failed check prints and traps, so the
+// call returns MCS_E_CUDA.
+#ifdef MCS_DEVICE_CHECKS
+#define MCS_DCHECK(cond)                                                                      \
+  do {                                                                                        \
+    if (!(cond)) {                                                                            \
+      printf("MCS_DCHECK %s:%d: %s\n", __FILE__, __LINE__, #cond);                           \
+      __trap();                                                                               \
+    }                                                                                         \
+  } while (0)
+#else
+#define MCS_DCHECK(cond) \
+  do {                   \
+  } while (0)
+#endif
+
 constexpr int kCellMin = -1048576;               // 21-bit signed cell coordinates (R27)
 constexpr int kCellMax = 1048575;
 constexpr int kSlotWords = 32;                    // sweep partial record per (particle, slot), fp64

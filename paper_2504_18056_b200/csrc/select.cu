@@ -88,6 +88,7 @@ __global__ void select_kernel(const float* __restrict__ pose, int capN, int N,
   for (int s = 0; s < nb_max; ++s) {
     float4* it = items + 4 * ((size_t)s * capN + i);
     const int k = s < nb ? bk[s] : -1;
+    MCS_DCHECK(k < K && (s >= nb || k >= 0));
     skeys[(size_t)s * N + i] = inactive_key;
     sids[(size_t)s * N + i] = s * capN + i;
     if (k < 0) {

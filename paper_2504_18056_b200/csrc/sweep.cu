@@ -94,6 +94,7 @@ __global__ void __launch_bounds__(kSweepThreads, MCS_SWEEP_MINBLOCKS)
     inf = items[4 * (size_t)item + 3];
   }
   const int kf = item >= 0 ? __float_as_int(inf.x) : -1;
+  MCS_DCHECK(t >= n_items || (item >= 0 && kf < 4096));
   const bool active = kf >= 0;
   const bool hb = active && (__float_as_int(inf.z) & 1);
   KfMeta m;
@@ -133,6 +134,7 @@ __global__ void __launch_bounds__(kSweepThreads, MCS_SWEEP_MINBLOCKS)
     const unsigned int lk = local_key(dx, dy, dz);
     p.key = in ? lk : kNoKey32;
     p.h = in ? slot_hash(lk, m.shift) : m.mask + 1;  // the hash is < cap already
+    MCS_DCHECK(!active || p.h <= m.mask + 1);
     return p;
   };
   // the (unconditional) first-probe loads; volatile: the compiler may not sink them towards
@@ -169,6 +171,7 @@ __global__ void __launch_bounds__(kSweepThreads, MCS_SWEEP_MINBLOCKS)
     unsigned int hh = slot_hash(q.key, m.shift) & m.mask;  // (recomputed: rare path)
     while (true) {
       hh = (hh + 1) & m.mask;
+      MCS_DCHECK(hh != (slot_hash(q.key, m.shift) & m.mask));  // table never full (load <= 1/4)
       const float4* sl = m.slots + 4 * (size_t)hh;
       const float4 t0 = __ldg(sl);
       const unsigned int kk = __float_as_uint(t0.x);

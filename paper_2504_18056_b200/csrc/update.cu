@@ -309,6 +309,7 @@ __global__ void propagate_kernel(float* __restrict__ kfpose, int capK, int K, in
   double xi[6];
 #pragma unroll
   for (int c = 0; c < 6; ++c) xi[c] = r * psi[(size_t)c * capN + i];
+  MCS_DCHECK(k >= 0 && k < K && K <= capK);
   float* Tk = kfpose + ((size_t)i * capK + k) * 12;
   float T[12];
   const float4* p4 = reinterpret_cast<const float4*>(Tk);

@@ -127,6 +127,7 @@ __global__ void ncum_dead_kernel(const Rung* __restrict__ scan, int N,
   if (i >= N) return;
   const Rung s = scan[i];
   const Rung prev = i > 0 ? scan[i - 1] : Rung{0ull, 0u, 0u};
+  MCS_DCHECK(s.d >= prev.d && s.d - prev.d <= 1u && s.d <= (unsigned)N);
   if (s.d != prev.d) dead_list[s.d - 1] = i;  // this particle is dead
   donor_local[i] = -1;
   if (donor_g) donor_g[i] = -1;
@@ -165,6 +166,7 @@ __global__ void draws_kernel(const long long* __restrict__ ncum, int N,
     if (ncum[mid] > R) hi = mid; else lo = mid + 1;
   }
   const int j = lo;
+  MCS_DCHECK(j >= 0 && j < N && ncum[j] > R && (j == 0 || ncum[j - 1] <= R));
   int dst = me;
   if (world > 1) {
     const long long* doffs = plan;
@@ -176,7 +178,9 @@ __global__ void draws_kernel(const long long* __restrict__ ncum, int N,
     dst = a;
   }
   if (dst == me) {
+    MCS_DCHECK(R - sc->d_off >= 0 && R - sc->d_off < N);
     const int slot = dead_list[R - sc->d_off];
+    MCS_DCHECK(slot >= 0 && slot < N && slot != j);
     donor_local[slot] = j;
     if (donor_g) donor_g[slot] = (int32_t)(gbase + j);
   } else {
@@ -195,6 +199,7 @@ __global__ void clone_kernel(const int32_t* __restrict__ donor, int N, int K, in
   const int i = (int)(t / KK), k = (int)(t - (long long)i * KK);
   const int d = donor[i];
   if (d < 0) return;
+  MCS_DCHECK(d < N && donor[d] < 0);  // a donor is a survivor, never itself overwritten
   if (k == K) {
 #pragma unroll
     for (int e = 0; e < 12; ++e) pose[(size_t)e * capN + i] = pose[(size_t)e * capN + d];
@@ -221,6 +226,7 @@ __global__ void pack_kernel(const int32_t* __restrict__ pack_src, long long n_it
   const long long it = t / KK;
   const int k = (int)(t - it * KK);
   const int j = pack_src[it];
+  MCS_DCHECK(j >= 0 && j < capN);
   float* o = out + it * state_floats(K);
   if (k == K) {
     for (int e = 0; e < 12; ++e) o[e] = pose[(size_t)e * capN + j];
@@ -252,7 +258,9 @@ __global__ void unpack_kernel(const float* __restrict__ in, long long n_items, i
     const int mid = (a + b + 1) >> 1;
     if (roff[mid] <= it) a = mid; else b = mid - 1;
   }
+  MCS_DCHECK(kstart[a] + (it - roff[a]) >= 0 && kstart[a] + (it - roff[a]) < capN);
   const int slot = dead_list[kstart[a] + (it - roff[a])];
+  MCS_DCHECK(slot >= 0 && slot < capN);
   const float* s = in + it * state_floats(K);
   if (k == K) {
     for (int e = 0; e < 12; ++e) pose[(size_t)e * capN + slot] = s[e];
