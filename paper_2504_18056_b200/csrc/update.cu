@@ -84,65 +84,56 @@ __global__ void __launch_bounds__(128) combine_kernel(CombineArgs a) {
       unmatched += a.S - ns;
       if (!a.eval_mode && !a.do_gn) continue;  // weighting-only pass: l is all it needs
       if (!(in_G || a.eval_mode)) continue;
-      // full symmetric H~ in the rotated frame
-      double Ht[36];
-#pragma unroll
-      for (int r = 0; r < 6; ++r)
-#pragma unroll
-        for (int c = r; c < 6; ++c) {
-          const double v = o[2 + up_idx(r, c)];
-          Ht[6 * r + c] = v;
-          Ht[6 * c + r] = v;
-        }
-      double bt[6];
-#pragma unroll
-      for (int k = 0; k < 6; ++k) bt[k] = o[23 + k];
-      // H_s = B^T H~ B, b_s = B^T b~ with B = blockdiag(R, R)
-      double Hs[36], bs[6];
+      const size_t so = (size_t)i * a.nb_max + s;
+      float* hs_out = (a.eval_mode && a.slot_H21) ? a.slot_H21 + so * 21 : nullptr;
+      // H_s = B^T H~ B with B = blockdiag(R, R), block by block on the upper triangle only
+      // (blocks (0,0), (0,1), (1,1); block (1,0) lies below the diagonal): T = H~_pq R,
+      // H_s,pq = R^T T, accumulated straight into H (slots in G) / written out (eval)
 #pragma unroll
       for (int p = 0; p < 2; ++p)
 #pragma unroll
-        for (int q = 0; q < 2; ++q) {
-          double T[9];  // H~_pq R
+        for (int q = p; q < 2; ++q) {
+          double Hb[9];
+#pragma unroll
+          for (int x = 0; x < 3; ++x)
+#pragma unroll
+            for (int y = 0; y < 3; ++y) {
+              const int r = 3 * p + x, c = 3 * q + y;
+              Hb[3 * x + y] = o[2 + (r <= c ? up_idx(r, c) : up_idx(c, r))];
+            }
+          double T[9];
 #pragma unroll
           for (int x = 0; x < 3; ++x)
 #pragma unroll
             for (int y = 0; y < 3; ++y)
-              T[3 * x + y] = Ht[6 * (3 * p + x) + 3 * q + 0] * R[0 * 3 + y] +
-                             Ht[6 * (3 * p + x) + 3 * q + 1] * R[1 * 3 + y] +
-                             Ht[6 * (3 * p + x) + 3 * q + 2] * R[2 * 3 + y];
+              T[3 * x + y] = Hb[3 * x + 0] * R[0 * 3 + y] + Hb[3 * x + 1] * R[1 * 3 + y] +
+                             Hb[3 * x + 2] * R[2 * 3 + y];
 #pragma unroll
           for (int x = 0; x < 3; ++x)
 #pragma unroll
-            for (int y = 0; y < 3; ++y)
-              Hs[6 * (3 * p + x) + 3 * q + y] =
-                  R[0 * 3 + x] * T[0 * 3 + y] + R[1 * 3 + x] * T[1 * 3 + y] +
-                  R[2 * 3 + x] * T[2 * 3 + y];
+            for (int y = 0; y < 3; ++y) {
+              if (p == q && y < x) continue;
+              const double v = R[0 * 3 + x] * T[0 * 3 + y] + R[1 * 3 + x] * T[1 * 3 + y] +
+                               R[2 * 3 + x] * T[2 * 3 + y];
+              const int u = up_idx(3 * p + x, 3 * q + y);
+              if (in_G) H[u] += v;
+              if (hs_out) hs_out[u] = (float)v;
+            }
         }
+      // b_s = B^T b~
 #pragma unroll
       for (int p = 0; p < 2; ++p)
 #pragma unroll
-        for (int x = 0; x < 3; ++x)
-          bs[3 * p + x] = R[0 * 3 + x] * bt[3 * p + 0] + R[1 * 3 + x] * bt[3 * p + 1] +
-                          R[2 * 3 + x] * bt[3 * p + 2];
+        for (int x = 0; x < 3; ++x) {
+          const double v = R[0 * 3 + x] * o[23 + 3 * p + 0] + R[1 * 3 + x] * o[23 + 3 * p + 1] +
+                           R[2 * 3 + x] * o[23 + 3 * p + 2];
+          if (in_G) b[3 * p + x] += v;
+          if (a.eval_mode && a.slot_b6) a.slot_b6[so * 6 + 3 * p + x] = (float)v;
+        }
       if (a.eval_mode) {
-        const size_t so = (size_t)i * a.nb_max + s;
         if (a.slot_l) a.slot_l[so] = ls;
         if (a.slot_n) a.slot_n[so] = ns;
         if (a.slot_kf) a.slot_kf[so] = kf;
-        if (a.slot_H21)
-          for (int r = 0; r < 6; ++r)
-            for (int c = r; c < 6; ++c) a.slot_H21[so * 21 + up_idx(r, c)] = (float)Hs[6 * r + c];
-        if (a.slot_b6)
-          for (int k = 0; k < 6; ++k) a.slot_b6[so * 6 + k] = (float)bs[k];
-      }
-      if (in_G) {
-#pragma unroll
-        for (int r = 0; r < 6; ++r)
-#pragma unroll
-          for (int c = r; c < 6; ++c) H[up_idx(r, c)] += Hs[6 * r + c];
-#pragma unroll
-        for (int k = 0; k < 6; ++k) b[k] += bs[k];
       }
     }
     l = lsum - a.kappa * (double)unmatched;
@@ -152,45 +143,65 @@ __global__ void __launch_bounds__(128) combine_kernel(CombineArgs a) {
     } else if (a.do_gn) {
       uint8_t flags = loop;
       double psi[6] = {0, 0, 0, 0, 0, 0};
+      // outputs that do not depend on the solve first (frees H's registers for it)
+#pragma unroll
+      for (int k = 0; k < 6; ++k) a.grad[(size_t)k * a.capN + i] = (float)(-2.0 * b[k]);
+#pragma unroll
+      for (int k = 0; k < 21; ++k) a.hess[(size_t)k * a.capN + i] = (float)H[k];
       if (loop) {
-        // Eq.5 with Levenberg damping (R11): (H + lambda I) psi = -b via Cholesky
-        double A[36];
+        // Eq.5 with Levenberg damping (R11): (H + lambda I) psi = -b via Cholesky, in place on
+        // the packed lower triangle Lc[r(r+1)/2 + c] (fully unrolled: register-resident); a
+        // non-positive pivot marks the system singular, the rest runs on a stand-in value
+        const double tr = H[up_idx(0, 0)] + H[up_idx(1, 1)] + H[up_idx(2, 2)] +
+                          H[up_idx(3, 3)] + H[up_idx(4, 4)] + H[up_idx(5, 5)];
+        const double lam = a.damping * tr / 6.0;
+        double Lc[21];
 #pragma unroll
         for (int r = 0; r < 6; ++r)
 #pragma unroll
-          for (int c = r; c < 6; ++c) { A[6 * r + c] = H[up_idx(r, c)]; A[6 * c + r] = A[6 * r + c]; }
-        double tr = A[0] + A[7] + A[14] + A[21] + A[28] + A[35];
-        const double lam = a.damping * tr / 6.0;
-#pragma unroll
-        for (int k = 0; k < 6; ++k) A[7 * k] += lam;
-        double Lc[36];
+          for (int c = 0; c <= r; ++c) Lc[r * (r + 1) / 2 + c] = H[up_idx(c, r)] + (r == c ? lam : 0.0);
+        // (inner loops have constant trip counts with index guards so that every loop unrolls
+        // and Lc stays in registers)
         bool ok = true;
 #pragma unroll
-        for (int k = 0; k < 36; ++k) Lc[k] = 0.0;
-        for (int j = 0; j < 6 && ok; ++j) {
-          double d = A[6 * j + j];
-          for (int k = 0; k < j; ++k) d -= Lc[6 * j + k] * Lc[6 * j + k];
-          if (!(d > 0.0)) { ok = false; break; }
-          Lc[6 * j + j] = sqrt(d);
-          for (int r = j + 1; r < 6; ++r) {
-            double s = A[6 * r + j];
-            for (int k = 0; k < j; ++k) s -= Lc[6 * r + k] * Lc[6 * j + k];
-            Lc[6 * r + j] = s / Lc[6 * j + j];
+        for (int j = 0; j < 6; ++j) {
+          double d = Lc[j * (j + 1) / 2 + j];
+#pragma unroll
+          for (int k = 0; k < 6; ++k)
+            if (k < j) d -= Lc[j * (j + 1) / 2 + k] * Lc[j * (j + 1) / 2 + k];
+          ok = ok && (d > 0.0);
+          const double ljj = sqrt(d > 0.0 ? d : 1.0);
+          Lc[j * (j + 1) / 2 + j] = ljj;
+#pragma unroll
+          for (int r = 0; r < 6; ++r) {
+            if (r <= j) continue;
+            double t = Lc[r * (r + 1) / 2 + j];
+#pragma unroll
+            for (int k = 0; k < 6; ++k)
+              if (k < j) t -= Lc[r * (r + 1) / 2 + k] * Lc[j * (j + 1) / 2 + k];
+            Lc[r * (r + 1) / 2 + j] = t / ljj;
           }
         }
         if (!ok) {
           flags |= 4;
         } else {
           double z[6];
+#pragma unroll
           for (int r = 0; r < 6; ++r) {
-            double s = -b[r];
-            for (int k = 0; k < r; ++k) s -= Lc[6 * r + k] * z[k];
-            z[r] = s / Lc[6 * r + r];
+            double t = -b[r];
+#pragma unroll
+            for (int k = 0; k < 6; ++k)
+              if (k < r) t -= Lc[r * (r + 1) / 2 + k] * z[k];
+            z[r] = t / Lc[r * (r + 1) / 2 + r];
           }
-          for (int r = 5; r >= 0; --r) {
-            double s = z[r];
-            for (int k = r + 1; k < 6; ++k) s -= Lc[6 * k + r] * psi[k];
-            psi[r] = s / Lc[6 * r + r];
+#pragma unroll
+          for (int rr = 0; rr < 6; ++rr) {
+            const int r = 5 - rr;
+            double t = z[r];
+#pragma unroll
+            for (int k = 0; k < 6; ++k)
+              if (k > r) t -= Lc[k * (k + 1) / 2 + r] * psi[k];
+            psi[r] = t / Lc[r * (r + 1) / 2 + r];
           }
           double nrm = 0.0;
 #pragma unroll
@@ -216,12 +227,7 @@ __global__ void __launch_bounds__(128) combine_kernel(CombineArgs a) {
         }
       }
 #pragma unroll
-      for (int k = 0; k < 6; ++k) {
-        a.psi[(size_t)k * a.capN + i] = psi[k];
-        a.grad[(size_t)k * a.capN + i] = (float)(-2.0 * b[k]);
-      }
-#pragma unroll
-      for (int k = 0; k < 21; ++k) a.hess[(size_t)k * a.capN + i] = (float)H[k];
+      for (int k = 0; k < 6; ++k) a.psi[(size_t)k * a.capN + i] = psi[k];
       a.flags[i] = flags;
     }
     if (!a.eval_mode && a.do_weight) {
