@@ -42,18 +42,35 @@ def _subsample_parity(s, step, no_death=True):
     assert ak.max() <= ROT_TOL and dk.max() <= T_TOL, (ak.max(), dk.max())
     L, e, w, _, _ = oracle.weights(np.zeros(s.N), g["loglik"])
     np.testing.assert_allclose(g["weight"], w, rtol=1e-12, atol=1e-300)
-    return g, ou, ok
+    return g, ou, ok, st
 
 
 def test_c3_forest_200_keyframes():
     s = synth.c3()
-    g, ou, _ = _subsample_parity(s, 64)
+    g, ou, _, st = _subsample_parity(s, 64)
     assert (ou["flags"] & 1).mean() > 0.2  # a real share of particles closes the loop
+
+
+@pytest.mark.parametrize("kappa,ok", [(0.0, False), (1.0, True), (20.0, True)])
+def test_c3_representative_needs_the_unmatched_penalty(kappa, ok):
+    """Behaviour, not parity (R8): with unmatched points skipped (kappa = 0, the literal reading)
+    a particle one tree pitch off, whose scan points fall outside the forest, scores higher
+    because it has fewer (all non-positive) terms; with kappa > 0 per unmatched (point, slot)
+    the representative is the true-mode particle."""
+    s = synth.c3()
+    with mcs.Context(s.N, s.K, s.S, loop_recency_gap=s.gap, voxel_resolution=s.r,
+                     unmatched_penalty=kappa) as ctx:
+        for (m3, c6), d in zip(s.keyframes, s.D):
+            ctx.add_keyframe(m3, c6, d)
+        ctx.set_particles(s.pose12, s.kf_pose12)
+        g = ctx.update(s.scan_mean3, s.scan_cov6, s.D_now, s.U)
+        t = ctx.get_particles()["pose12"][g["representative"]].reshape(3, 4)[:, 3]
+    assert (np.linalg.norm(t - s.T_gt[:3, 3]) < 0.5) == ok, np.linalg.norm(t - s.T_gt[:3, 3])
 
 
 def test_c5_two_floors():
     s = synth.c5()
-    g, ou, _ = _subsample_parity(s, 64)
+    g, ou, _, st = _subsample_parity(s, 64)
     assert (ou["flags"] & 2).mean() > 0.5   # loop closure updates (a3/a4 run)
 
 
