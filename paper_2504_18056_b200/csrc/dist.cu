@@ -354,18 +354,20 @@ mcs_status dist_alltoallv(mcs_ctx* c, const float* d_send, const size_t* send_by
   if (c->nccl_comm) {
     NcclApi* a = nccl();
     if (a->GroupStart() != 0) return MCS_E_NCCL;
-    for (int p = 0; p < G; ++p) {
+    bool ok = true;  // the group is always closed, even after a failed enqueue
+    for (int p = 0; p < G && ok; ++p) {
       if (p == c->rank) continue;
       if (send_bytes[p] &&
           a->Send((const char*)d_send + send_off[p], send_bytes[p], kNcclUint8, p, c->nccl_comm,
                   c->stream) != 0)
-        return MCS_E_NCCL;
-      if (recv_bytes[p] &&
+        ok = false;
+      if (ok && recv_bytes[p] &&
           a->Recv((char*)d_recv + recv_off[p], recv_bytes[p], kNcclUint8, p, c->nccl_comm,
                   c->stream) != 0)
-        return MCS_E_NCCL;
+        ok = false;
     }
-    return a->GroupEnd() == 0 ? MCS_OK : MCS_E_NCCL;
+    const bool closed = a->GroupEnd() == 0;
+    return (ok && closed) ? MCS_OK : MCS_E_NCCL;
   }
   size_t ts = send_off[G], tr = recv_off[G];
   if (stage(c, ts + tr + 16) != MCS_OK) return MCS_E_OUT_OF_MEMORY;
