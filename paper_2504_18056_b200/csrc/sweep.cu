@@ -79,11 +79,14 @@ __global__ void __launch_bounds__(kSweepThreads, MCS_SWEEP_MINBLOCKS)
                  int n_items, const float4* __restrict__ scan, int S,
                  const KfMeta* __restrict__ kmeta, float inv_r, float nn_r2,
                  double* __restrict__ part) {
-  __shared__ float4 s_pt[(kChunk + 2) * 3];
+  // dynamic shared memory: [(kChunk + 2) * 3] float4 scan stage, then [28][threads] fp64 totals
+  extern __shared__ float4 smem_dyn[];
+  float4* s_pt = smem_dyn;
   // two-level accumulation: fp32 registers within a stage, fp64 totals per thread in shared
   // memory across stages (the fp32 running sums over a whole 4,096-point scan lose ~1e-5
   // relative, which an ill-conditioned H turns into >1e-5 m of pose error)
-  __shared__ double s_acc[28][kSweepThreads];
+  double(*s_acc)[kSweepThreads] =
+      reinterpret_cast<double(*)[kSweepThreads]>(smem_dyn + (kChunk + 2) * 3);
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   const int item = t < n_items ? order[t] : -1;
   float4 r0 = make_float4(0, 0, 0, 0), r1 = r0, r2 = r0, inf = r0;
@@ -454,12 +457,21 @@ void launch_sweep(mcs_ctx* c, int S) {
   const int n_items = c->cfg.neighbor_count * c->N;
   const int grid = (n_items + kSweepThreads - 1) / kSweepThreads;
   const float inv_r = 1.0f / c->cfg.voxel_resolution;
+  constexpr size_t smem = sizeof(float4) * (kChunk + 2) * 3 + sizeof(double) * 28 * kSweepThreads;
+  static bool attr_set[128] = {};  // opt in beyond 48 KB once per device (both instantiations)
+  if (c->dev < 0 || c->dev >= 128 || !attr_set[c->dev]) {
+    cudaFuncSetAttribute(sweep_kernel<MCS_CORR_CELL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    cudaFuncSetAttribute(sweep_kernel<MCS_CORR_NN27>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    if (c->dev >= 0 && c->dev < 128) attr_set[c->dev] = true;
+  }
   if (c->cfg.corr_mode == MCS_CORR_NN27) {
     const float nn_r2 = c->cfg.nn_radius * c->cfg.nn_radius;
-    sweep_kernel<MCS_CORR_NN27><<<grid, kSweepThreads, 0, c->stream>>>(
+    sweep_kernel<MCS_CORR_NN27><<<grid, kSweepThreads, smem, c->stream>>>(
         c->d_items, c->d_order, n_items, c->d_scan, S, c->d_kf_meta, inv_r, nn_r2, c->d_part);
   } else {
-    sweep_kernel<MCS_CORR_CELL><<<grid, kSweepThreads, 0, c->stream>>>(
+    sweep_kernel<MCS_CORR_CELL><<<grid, kSweepThreads, smem, c->stream>>>(
         c->d_items, c->d_order, n_items, c->d_scan, S, c->d_kf_meta, inv_r, 0.f, c->d_part);
   }
 }
