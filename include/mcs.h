@@ -126,6 +126,12 @@ typedef struct mcs_config {
   int32_t  clone_split;          /* 0: a clone copies its donor's L (R19); 1: the donor and its
                                     c clones each get L - ln(1 + c) (R34)                    */
   const mcs_allocator* allocator; /* NULL: cudaMalloc / cudaMallocAsync on the context stream */
+  int32_t  peer_migration;       /* world_size > 1: 1 (default) = respawned particles that land
+                                    on another rank are written straight into that rank's state
+                                    by the draws kernel over peer memory (NVLink; CUDA IPC across
+                                    processes) when every rank's state is reachable, else (and
+                                    with 0) packed and exchanged by NCCL send/recv or the
+                                    transport's alltoallv                                     */
 } mcs_config;
 
 /* Fills *cfg with the defaults above (capacities 0: caller sets them). */
@@ -256,6 +262,10 @@ MCS_API size_t mcs_state_bytes_per_particle(int32_t n_keyframes);
  * Only filled when profiling is enabled with mcs_set_profiling(ctx, 1). */
 MCS_API mcs_status mcs_set_profiling(mcs_ctx* ctx, int32_t enable);
 MCS_API mcs_status mcs_get_phase_ms(const mcs_ctx* ctx, float* ms5);
+/* Migration path of a multi-rank context after its first respawn: 1 peer-direct (the draws
+ * kernel writes clones into other ranks' memory), -1 packed + NCCL / transport exchange,
+ * 0 not decided yet (no respawn so far, or world_size 1 without an exchange path). */
+MCS_API int32_t mcs_peer_migration_state(const mcs_ctx* ctx);
 
 #ifdef __cplusplus
 }

@@ -5,10 +5,10 @@ The product is the C-ABI library ``libmcs.so`` (hand-written sm_100a CUDA, see
 """
 from .mcs import (ABI_VERSION, CORR_CELL, CORR_NN27, Allocator, Config, Context, InprocTransport, MCSError, default_config,
                   header_symbols, load, nccl_unique_id, plan_ladder, plan_migration,
-                  state_bytes_per_particle, TorchAllocator, unpack_h21)
+                  state_bytes_per_particle, TorchAllocator, TorchDistTransport, unpack_h21)
 
 from .slam import MonteCarloSLAM, in_elevator
 
 __all__ = ["MonteCarloSLAM", "in_elevator", "ABI_VERSION", "CORR_CELL", "CORR_NN27", "Allocator", "Config", "Context", "InprocTransport", "MCSError", "default_config",
            "header_symbols", "load", "nccl_unique_id", "plan_ladder", "plan_migration",
-           "state_bytes_per_particle", "TorchAllocator", "unpack_h21"]
+           "state_bytes_per_particle", "TorchAllocator", "TorchDistTransport", "unpack_h21"]

@@ -251,6 +251,7 @@ void mcs_config_default(mcs_config* cfg) {
   cfg->corr_mode = MCS_CORR_CELL;
   cfg->nn_radius = 0.0f;
   cfg->clone_split = 0;
+  cfg->peer_migration = 1;
   cfg->rank = 0;
   cfg->world_size = 1;
   cfg->nccl_unique_id = nullptr;
@@ -299,9 +300,10 @@ mcs_status mcs_create(const mcs_config* cfg, mcs_ctx** out) {
   if ((cfg->corr_mode != MCS_CORR_CELL && cfg->corr_mode != MCS_CORR_NN27) ||
       (cfg->corr_mode == MCS_CORR_NN27 &&
        !(cfg->nn_radius > 0.0f && cfg->nn_radius <= cfg->voxel_resolution)) ||
-      (cfg->clone_split != 0 && cfg->clone_split != 1)) {
+      (cfg->clone_split != 0 && cfg->clone_split != 1) ||
+      (cfg->peer_migration != 0 && cfg->peer_migration != 1)) {
     g_create_error = "corr_mode must be CELL or NN27 (with 0 < nn_radius <= voxel_resolution), "
-                     "clone_split 0 or 1";
+                     "clone_split and peer_migration 0 or 1";
     return MCS_E_INVALID_ARG;
   }
   if (cfg->world_size < 1 || cfg->rank < 0 || cfg->rank >= cfg->world_size) {
@@ -894,6 +896,8 @@ mcs_status mcs_set_profiling(mcs_ctx* ctx, int32_t enable) {
   ctx->profiling = enable != 0;
   return MCS_OK;
 }
+
+int32_t mcs_peer_migration_state(const mcs_ctx* ctx) { return ctx ? ctx->p2p : 0; }
 
 mcs_status mcs_get_phase_ms(const mcs_ctx* ctx, float* ms5) {
   if (!ctx || !ms5) return MCS_E_INVALID_ARG;

@@ -93,6 +93,7 @@ mcs_status mcs_plan_migration(int32_t world, const int64_t* clones_per_rank,
 // ======================================================================================
 #include <dlfcn.h>
 #include <string.h>
+#include <unistd.h>
 
 #include <chrono>
 #include <condition_variable>
@@ -284,6 +285,13 @@ mcs_status dist_init(mcs_ctx* c, std::string& err) {
 }
 
 void dist_destroy(mcs_ctx* c) {
+  for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
+  c->ipc_opened.clear();
+  if (c->d_peers) cudaFree(c->d_peers);
+  c->d_peers = nullptr;
+  if (c->d_ag) mem_free(c, c->d_ag);
+  c->d_ag = nullptr;
+  c->d_ag_bytes = 0;
   if (c->nccl_comm) {
     NcclApi* a = nccl();
     if (a && a->CommDestroy) a->CommDestroy(c->nccl_comm);
@@ -328,8 +336,15 @@ mcs_status dist_allgather_host(mcs_ctx* c, const void* send, void* recv, size_t 
   }
   if (c->nccl_comm) {
     NcclApi* a = nccl();
-    char* d = nullptr;
-    if (mem_alloc(c, (void**)&d, bytes * (c->world + 1)) != cudaSuccess) return MCS_E_OUT_OF_MEMORY;
+    const size_t need = bytes * (c->world + 1);
+    if (c->d_ag_bytes < need) {  // persistent scratch: no allocation on the per-update path
+      mem_free(c, c->d_ag);
+      c->d_ag = nullptr;
+      c->d_ag_bytes = 0;
+      if (mem_alloc(c, (void**)&c->d_ag, need) != cudaSuccess) return MCS_E_OUT_OF_MEMORY;
+      c->d_ag_bytes = need;
+    }
+    char* d = c->d_ag;
     mcs_status st = MCS_OK;
     if (cudaMemcpyAsync(d, send, bytes, cudaMemcpyHostToDevice, c->stream) != cudaSuccess)
       st = MCS_E_CUDA;
@@ -340,10 +355,111 @@ mcs_status dist_allgather_host(mcs_ctx* c, const void* send, void* recv, size_t 
                                          c->stream) != cudaSuccess ||
                          cudaStreamSynchronize(c->stream) != cudaSuccess))
       st = MCS_E_CUDA;
-    mem_free(c, d);
     return st;
   }
   return c->tr->allgather(c->tr->user, c->rank, send, recv, bytes) ? MCS_E_NCCL : MCS_OK;
+}
+
+mcs_status dist_barrier(mcs_ctx* c) {
+  if (!dist_active(c)) return MCS_OK;
+  if (c->nccl_comm) {  // a 1-element allreduce: later work on this stream waits for every rank
+    if (c->d_ag_bytes < 8) {
+      mem_free(c, c->d_ag);
+      c->d_ag = nullptr;
+      c->d_ag_bytes = 0;
+      if (mem_alloc(c, (void**)&c->d_ag, 64) != cudaSuccess) return MCS_E_OUT_OF_MEMORY;
+      c->d_ag_bytes = 64;
+    }
+    NcclApi* a = nccl();
+    return a->AllReduce(c->d_ag, c->d_ag, 1, kNcclFloat64, kNcclMax, c->nccl_comm, c->stream) == 0
+               ? MCS_OK : MCS_E_NCCL;
+  }
+  if (cudaStreamSynchronize(c->stream) != cudaSuccess) return MCS_E_CUDA;
+  double z = 0.0;
+  return c->tr->allreduce(c->tr->user, c->rank, &z, 1, 0, 1) ? MCS_E_NCCL : MCS_OK;
+}
+
+namespace {
+struct PeerInfo {  // what a rank publishes about its state buffers
+  int32_t pid, dev, capN, capK, ipc_ok, pad;
+  uint64_t ptr[5];                 // pose, kfpose, L, dead_list, donor_g
+  cudaIpcMemHandle_t handle[5];
+};
+}  // namespace
+
+mcs_status dist_peer_setup(mcs_ctx* c) {
+  if (c->p2p != 0) return MCS_OK;
+  c->p2p = -1;
+  if (!dist_active(c) || !c->cfg.peer_migration) return MCS_OK;
+  const int G = c->world;
+  PeerInfo me;
+  memset(&me, 0, sizeof(me));
+  me.pid = (int32_t)getpid();
+  me.dev = c->dev;
+  me.capN = c->capN;
+  me.capK = c->capK;
+  void* mine[5] = {c->d_pose, c->d_kfpose, c->d_L, c->d_dead_list, c->d_donor_g};
+  // CUDA IPC needs whole cudaMalloc allocations: not available under a user allocator
+  me.ipc_ok = c->alloc.alloc ? 0 : 1;
+  for (int k = 0; k < 5; ++k) {
+    me.ptr[k] = (uint64_t)(uintptr_t)mine[k];
+    if (me.ipc_ok && cudaIpcGetMemHandle(&me.handle[k], mine[k]) != cudaSuccess) me.ipc_ok = 0;
+  }
+  cudaGetLastError();
+  std::vector<PeerInfo> all(G);
+  MCS_TRY(dist_allgather_host(c, &me, all.data(), sizeof(PeerInfo)));
+  std::vector<PeerView> views(G);
+  int32_t ok = 1;
+  std::vector<void*> opened;
+  for (int p = 0; p < G && ok; ++p) {
+    const PeerInfo& q = all[p];
+    void* ptr[5];
+    if (q.pid == me.pid) {  // same process: raw pointers (peer access if another device)
+      for (int k = 0; k < 5; ++k) ptr[k] = (void*)(uintptr_t)q.ptr[k];
+      if (q.dev != c->dev) {
+        int can = 0;
+        if (cudaDeviceCanAccessPeer(&can, c->dev, q.dev) != cudaSuccess || !can) {
+          ok = 0;
+          break;
+        }
+        const cudaError_t e = cudaDeviceEnablePeerAccess(q.dev, 0);
+        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) ok = 0;
+        cudaGetLastError();
+      }
+    } else {
+      if (!q.ipc_ok) {
+        ok = 0;
+        break;
+      }
+      for (int k = 0; k < 5 && ok; ++k) {
+        if (cudaIpcOpenMemHandle(&ptr[k], q.handle[k], cudaIpcMemLazyEnablePeerAccess) !=
+            cudaSuccess) {
+          ok = 0;
+          cudaGetLastError();
+        } else {
+          opened.push_back(ptr[k]);
+        }
+      }
+    }
+    if (!ok) break;
+    views[p] = PeerView{(float*)ptr[0], (float*)ptr[1], (double*)ptr[2], (int32_t*)ptr[3],
+                        (int32_t*)ptr[4], q.capN, q.capK};
+  }
+  // every rank must agree (one failed open anywhere -> all use the transport path)
+  std::vector<int32_t> oks(G);
+  MCS_TRY(dist_allgather_host(c, &ok, oks.data(), sizeof(int32_t)));
+  for (int p = 0; p < G; ++p) ok &= oks[p];
+  if (!ok) {
+    for (void* p : opened) cudaIpcCloseMemHandle(p);
+    return MCS_OK;
+  }
+  c->ipc_opened = opened;
+  if (cudaMalloc(&c->d_peers, sizeof(PeerView) * G) != cudaSuccess) return MCS_E_OUT_OF_MEMORY;
+  if (cudaMemcpy(c->d_peers, views.data(), sizeof(PeerView) * G, cudaMemcpyHostToDevice) !=
+      cudaSuccess)
+    return MCS_E_CUDA;
+  c->p2p = 1;
+  return MCS_OK;
 }
 
 mcs_status dist_alltoallv(mcs_ctx* c, const float* d_send, const size_t* send_bytes,

@@ -36,6 +36,17 @@ namespace mcs {
   } while (0)
 #endif
 
+// status plumbing of the host-side launch sequences
+#define MCS_TRY(x)               \
+  do {                           \
+    const mcs_status _s = (x);   \
+    if (_s != MCS_OK) return _s; \
+  } while (0)
+#define MCS_CUDA(x)                            \
+  do {                                         \
+    if ((x) != cudaSuccess) return MCS_E_CUDA; \
+  } while (0)
+
 constexpr int kCellMin = -1048576;               // 21-bit signed cell coordinates (R27)
 constexpr int kCellMax = 1048575;
 constexpr int kSlotWords = 32;                    // sweep partial record per (particle, slot), fp64
@@ -80,6 +91,8 @@ struct KfHost {
   int32_t cap = 0, n_cells = 0, n_points = 0;
   KfMeta meta{};
 };
+
+struct PeerView;                // dist.cu: a rank's state as another rank writes it
 
 struct Scalars {                // device-side reduction results of one update
   double m;                     // max_i L_i (after L += l)            } exchanged together
@@ -178,6 +191,12 @@ struct mcs_ctx {
   size_t xfer_cap_items = 0;
   void* h_stage = nullptr;            // pinned host staging for the host transport
   size_t h_stage_bytes = 0;
+  char* d_ag = nullptr;               // device scratch of the NCCL host allgather / barrier
+  size_t d_ag_bytes = 0;
+  // peer-direct migration (cfg.peer_migration): 0 not set up yet, 1 on, -1 off
+  int p2p = 0;
+  mcs::PeerView* d_peers = nullptr;    // [world] device views of every rank's state
+  std::vector<void*> ipc_opened;       // CUDA IPC mappings of other processes' buffers
 };
 
 namespace mcs {
@@ -217,9 +236,24 @@ mcs_status launch_resample_only(mcs_ctx* c, const double* d_e, const uint8_t* d_
                                 uint32_t U, int32_t* d_donor);
 size_t cub_temp_needed(int n);
 
+// A rank's particle state as another rank writes it (peer-direct migration).
+struct PeerView {
+  float* pose;         // SoA [12][capN]
+  float* kfpose;       // [capN][capK][12]
+  double* L;           // [capN]
+  int32_t* dead_list;  // [capN] local dead slots, ascending
+  int32_t* donor_g;    // [capN] global donor index
+  int capN, capK;
+};
+
 // ---- multi-rank exchange (dist.cu); world == 1 => no-ops returning MCS_OK ----
 mcs_status dist_init(mcs_ctx* c, std::string& err);
 bool dist_active(const mcs_ctx* c);  // exchange path in use (world > 1, or a transport/NCCL)
+// collective: returns once every rank's stream has reached this point (NCCL: stream-ordered)
+mcs_status dist_barrier(mcs_ctx* c);
+// collective: exchange state views (raw pointers in one process, CUDA IPC across processes);
+// sets c->p2p to 1 when every rank can write every other rank's state, else -1
+mcs_status dist_peer_setup(mcs_ctx* c);
 void dist_destroy(mcs_ctx* c);
 // in place on device doubles; op 0 = sum, 1 = max (stream-ordered; host transport syncs)
 mcs_status dist_allreduce_f64(mcs_ctx* c, double* d_buf, int n, int op);

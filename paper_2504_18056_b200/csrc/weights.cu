@@ -190,6 +190,59 @@ __global__ void draws_kernel(const long long* __restrict__ ncum, int N,
   }
 }
 
+// Peer-direct migration (cfg.peer_migration, world > 1): one warp per draw made by this rank's
+// survivors.  A clone whose dead slot is local is recorded for clone_kernel; one whose slot is
+// on rank p is written straight into p's state (its dead list read over peer memory): pose,
+// every keyframe pose, L and the global donor index -- the pack / send / unpack of the
+// transport path fused into the kernel that decides the transfer.
+__global__ void draws_p2p_kernel(const long long* __restrict__ ncum, int N,
+                                 const Scalars* __restrict__ sc, int world, int me,
+                                 long long gbase, const long long* __restrict__ plan,
+                                 const int32_t* __restrict__ dead_list,
+                                 int32_t* __restrict__ donor_local, int32_t* __restrict__ donor_g,
+                                 const PeerView* __restrict__ peers, int K,
+                                 const float* __restrict__ pose, const float* __restrict__ kfpose,
+                                 const double* __restrict__ L, int capN, int capK) {
+  const long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= sc->clones) return;
+  const long long R = sc->clone_off + w;
+  int lo = 0, hi = N - 1;  // first j with ncum[j] > R (every lane the same: broadcast loads)
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (ncum[mid] > R) hi = mid; else lo = mid + 1;
+  }
+  const int j = lo;
+  MCS_DCHECK(j >= 0 && j < N && ncum[j] > R && (j == 0 || ncum[j - 1] <= R));
+  const long long* doffs = plan;
+  int a = 0, b = world - 1;  // destination: last rank with doffs[rank] <= R
+  while (a < b) {
+    const int mid = (a + b + 1) >> 1;
+    if (doffs[mid] <= R) a = mid; else b = mid - 1;
+  }
+  if (a == me) {
+    if (lane == 0) {
+      const int slot = dead_list[R - sc->d_off];
+      MCS_DCHECK(slot >= 0 && slot < N && slot != j);
+      donor_local[slot] = j;
+      donor_g[slot] = (int32_t)(gbase + j);
+    }
+    return;
+  }
+  const PeerView P = peers[a];
+  const int slot = P.dead_list[R - doffs[a]];
+  MCS_DCHECK(slot >= 0 && slot < P.capN);
+  if (lane < 12) P.pose[(size_t)lane * P.capN + slot] = pose[(size_t)lane * capN + j];
+  const float4* src = reinterpret_cast<const float4*>(kfpose + (size_t)j * capK * 12);
+  float4* dst = reinterpret_cast<float4*>(P.kfpose + (size_t)slot * P.capK * 12);
+  for (int k = lane; k < 3 * K; k += 32) dst[k] = src[k];
+  if (lane == 0) {
+    P.L[slot] = L[j];
+    P.donor_g[slot] = (int32_t)(gbase + j);
+  }
+  __threadfence_system();  // the stores are visible to the peer before this rank's barrier
+}
+
 __global__ void clone_kernel(const int32_t* __restrict__ donor, int N, int K, int capK, int capN,
                              float* __restrict__ pose, float* __restrict__ kfpose,
                              double* __restrict__ L) {
@@ -352,15 +405,6 @@ size_t cub_temp_needed(int n) {
   return b;
 }
 
-#define MCS_TRY(x)                    \
-  do {                                \
-    const mcs_status _s = (x);        \
-    if (_s != MCS_OK) return _s;      \
-  } while (0)
-#define MCS_CUDA(x)                                  \
-  do {                                               \
-    if ((x) != cudaSuccess) return MCS_E_CUDA;       \
-  } while (0)
 
 // Global respawn plan for world > 1: allgather (Q_g, D_g), plan on the host, upload.
 static mcs_status plan_global(mcs_ctx* c, uint32_t U, long long* n_send_items,
@@ -478,21 +522,31 @@ mcs_status launch_weights_resample(mcs_ctx* c, uint32_t U) {
   totals_kernel<<<1, 1, 0, st>>>(scan, N, single ? 1 : 0, sc);
   long long n_send = 0, n_recv = 0, n_draws_bound = N;
   std::vector<size_t> sb, so, rb, ro;
+  if (!single) MCS_TRY(dist_peer_setup(c));  // once per context (collective)
+  const bool p2p = !single && c->p2p == 1;
   if (!single) {
     MCS_TRY(plan_global(c, U, &n_send, &n_recv, sb, so, rb, ro));
     long long h_clones = 0;
     MCS_CUDA(cudaMemcpy(&h_clones, &sc->clones, sizeof(long long), cudaMemcpyDeviceToHost));
     n_draws_bound = h_clones;
-    MCS_TRY(ensure_xfer(c, std::max(n_send, n_recv)));
+    if (!p2p) MCS_TRY(ensure_xfer(c, std::max(n_send, n_recv)));
   }
   ncum_dead_kernel<<<g, kWT, 0, st>>>(scan, N, sc, U, c->d_ncum, c->d_dead_list, c->d_donor,
                                       c->d_donor_g);
   if (c->cfg.clone_split) split_kernel<<<g, kWT, 0, st>>>(c->d_ncum, N, sc, U, c->d_L);
-  if (n_draws_bound > 0)
+  if (p2p) {
+    // every rank's dead list is complete before any rank writes into it
+    MCS_TRY(dist_barrier(c));
+    if (n_draws_bound > 0)
+      draws_p2p_kernel<<<(int)((n_draws_bound * 32 + 255) / 256), 256, 0, st>>>(
+          c->d_ncum, N, sc, c->world, c->rank, c->gbase, c->d_plan, c->d_dead_list, c->d_donor,
+          c->d_donor_g, c->d_peers, c->K, c->d_pose, c->d_kfpose, c->d_L, c->capN, c->capK);
+  } else if (n_draws_bound > 0) {
     draws_kernel<<<(int)((n_draws_bound + kWT - 1) / kWT), kWT, 0, st>>>(
         c->d_ncum, N, sc, c->world, c->rank, c->gbase, c->d_plan, c->d_dead_list, c->d_donor,
         c->d_donor_g, c->d_pack_src);
-  if (!single && n_send > 0) {
+  }
+  if (!p2p && !single && n_send > 0) {
     const long long tot = n_send * (c->K + 1);
     pack_kernel<<<(int)((tot + 255) / 256), 256, 0, st>>>(c->d_pack_src, n_send, c->K, c->capK,
                                                           c->capN, c->gbase, c->d_pose,
@@ -501,7 +555,9 @@ mcs_status launch_weights_resample(mcs_ctx* c, uint32_t U) {
   const long long tot = (long long)N * (c->K + 1);
   clone_kernel<<<(int)((tot + 255) / 256), 256, 0, st>>>(c->d_donor, N, c->K, c->capK, c->capN,
                                                          c->d_pose, c->d_kfpose, c->d_L);
-  if (!single) {
+  if (p2p) {
+    MCS_TRY(dist_barrier(c));  // every rank's incoming clones have landed
+  } else if (!single) {
     MCS_TRY(dist_alltoallv(c, c->d_send, sb.data(), so.data(), c->d_recv, rb.data(), ro.data()));
     if (n_recv > 0) {
       const long long tr = n_recv * (c->K + 1);

@@ -59,6 +59,7 @@ class Config(C.Structure):
         ("nn_radius", C.c_float),
         ("clone_split", C.c_int32),
         ("allocator", C.c_void_p),
+        ("peer_migration", C.c_int32),
     ]
 
 
@@ -146,6 +147,7 @@ def load() -> C.CDLL:
         "mcs_inproc_transport_create": (vp, [i32]),
         "mcs_inproc_transport_destroy": (None, [vp]),
         "mcs_plan_migration": (st, [i32, vp, vp, vp]),
+        "mcs_peer_migration_state": (i32, [vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -212,7 +214,8 @@ class Context:
                 al = C.cast(C.pointer(al), C.c_void_p)
             cfg_kw["allocator"] = al
         if tr is not None:
-            cfg_kw["transport"] = tr.ptr if isinstance(tr, InprocTransport) else tr
+            cfg_kw["transport"] = tr.ptr if isinstance(tr, (InprocTransport,
+                                                            TorchDistTransport)) else tr
             self._keep.append(tr)
         if nid is not None:
             idbuf = C.create_string_buffer(bytes(nid), 128)
@@ -275,6 +278,11 @@ class Context:
         pk, kk = _ptr(kf_pose12, np.float32)
         pl, kl = _ptr(cum_loglik, np.float64)
         self._check(self._lib.mcs_set_particles(self._ctx, n, pp, pk, pl))
+
+    @property
+    def peer_migration_state(self) -> int:
+        """1 peer-direct migration, -1 packed exchange, 0 not decided yet."""
+        return int(self._lib.mcs_peer_migration_state(self._ctx))
 
     def get_particles(self):
         n, K = self.sizes
@@ -396,6 +404,90 @@ def nccl_unique_id() -> bytes:
     if st:
         raise MCSError(st, "libnccl.so.2 unavailable")
     return buf.raw
+
+
+ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int32, C.c_void_p, C.c_int32, C.c_int32,
+                          C.c_int32)
+ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_size_t)
+ALLTOALLV_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int32, C.POINTER(C.c_void_p),
+                           C.POINTER(C.c_size_t), C.POINTER(C.c_void_p), C.POINTER(C.c_size_t))
+
+
+class Transport(C.Structure):
+    """mcs_transport (include/mcs.h): host collectives for world_size > 1 without NCCL."""
+    _fields_ = [("user", C.c_void_p), ("allreduce", ALLREDUCE_FN), ("allgather", ALLGATHER_FN),
+                ("alltoallv", ALLTOALLV_FN)]
+
+
+class TorchDistTransport:
+    """mcs_transport over a torch.distributed process group with CPU tensors (e.g. gloo): one
+    process per rank.  Reductions are allgathered and reduced in rank order, so results are
+    bitwise independent of the backend's reduction tree."""
+
+    def __init__(self, group=None):
+        import torch
+        import torch.distributed as dist
+        self._dist, self._torch, self.group = dist, torch, group
+        self.world = dist.get_world_size(group)
+
+        def _gather(b: bytes):
+            t = torch.frombuffer(bytearray(b), dtype=torch.uint8)
+            out = [torch.empty_like(t) for _ in range(self.world)]
+            dist.all_gather(out, t, group=group)
+            return [o.numpy().tobytes() for o in out]
+
+        def allreduce(user, rank, buf, n, dtype, op):
+            try:
+                nbytes = 8 * n
+                parts = _gather(C.string_at(buf, nbytes))
+                arrs = [np.frombuffer(p, np.float64 if dtype == 0 else np.int64) for p in parts]
+                acc = arrs[0].copy()
+                for a in arrs[1:]:
+                    acc = np.maximum(acc, a) if op == 1 else acc + a
+                C.memmove(buf, acc.ctypes.data, nbytes)
+                return 0
+            except Exception:  # surfaced as MCS_E_NCCL by the library
+                return 1
+
+        def allgather(user, rank, send, recv, nbytes):
+            try:
+                parts = _gather(C.string_at(send, nbytes))
+                C.memmove(recv, b"".join(parts), nbytes * self.world)
+                return 0
+            except Exception:
+                return 1
+
+        def alltoallv(user, rank, send, send_bytes, recv, recv_bytes):
+            try:
+                reqs = []
+                bufs = []
+                for p in range(self.world):
+                    if p == rank:
+                        continue
+                    if send_bytes[p]:
+                        t = torch.frombuffer(bytearray(C.string_at(send[p], send_bytes[p])),
+                                             dtype=torch.uint8)
+                        reqs.append(dist.isend(t, p, group=group))
+                    if recv_bytes[p]:
+                        r = torch.empty(recv_bytes[p], dtype=torch.uint8)
+                        bufs.append((p, r))
+                        reqs.append(dist.irecv(r, p, group=group))
+                for q in reqs:
+                    q.wait()
+                for p, r in bufs:
+                    C.memmove(recv[p], r.numpy().ctypes.data, recv_bytes[p])
+                if send_bytes[rank]:
+                    C.memmove(recv[rank], send[rank], send_bytes[rank])
+                return 0
+            except Exception:
+                return 1
+
+        self._fns = (ALLREDUCE_FN(allreduce), ALLGATHER_FN(allgather), ALLTOALLV_FN(alltoallv))
+        self.struct = Transport(None, *self._fns)
+
+    @property
+    def ptr(self):
+        return C.cast(C.pointer(self.struct), C.c_void_p)
 
 
 class InprocTransport:

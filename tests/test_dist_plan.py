@@ -104,3 +104,58 @@ def test_gloo_world_size_2_plan():
         assert p.exitcode == 0
     res = dict(q.get(timeout=10) for _ in range(2))
     assert res == {0: True, 1: True}
+
+
+def _transport_worker(rank, world, port, q):
+    import ctypes as C
+
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        tr = mcs.TorchDistTransport()
+        s = tr.struct
+        ok = True
+        # allreduce: sum and max of f64, sum of i64, reduced in rank order
+        v = np.array([0.1 * (rank + 1), -1.0 * rank, 1e-17], np.float64)
+        ok &= s.allreduce(None, rank, v.ctypes.data, 3, 0, 0) == 0
+        ref = sum(np.array([0.1 * (r + 1), -1.0 * r, 1e-17]) for r in range(world))
+        ok &= np.array_equal(v, ref)
+        m = np.array([float(rank), -float(rank)])
+        ok &= s.allreduce(None, rank, m.ctypes.data, 2, 0, 1) == 0 and m.tolist() == [1.0, 0.0]
+        iv = np.array([rank + 5], np.int64)
+        ok &= s.allreduce(None, rank, iv.ctypes.data, 1, 1, 0) == 0 and int(iv[0]) == 11
+        # allgather of 5 bytes
+        sb = np.full(5, rank + 1, np.uint8)
+        rb = np.zeros(5 * world, np.uint8)
+        ok &= s.allgather(None, rank, sb.ctypes.data, rb.ctypes.data, 5) == 0
+        ok &= rb.tolist() == [1] * 5 + [2] * 5
+        # alltoallv with ragged sizes (rank r sends r + p + 1 bytes to p, valued 10r + p)
+        send = [np.full(rank + p + 1, 10 * rank + p, np.uint8) for p in range(world)]
+        recv = [np.zeros(p + rank + 1, np.uint8) for p in range(world)]
+        sp = (C.c_void_p * world)(*[a.ctypes.data for a in send])
+        rp = (C.c_void_p * world)(*[a.ctypes.data for a in recv])
+        sbs = (C.c_size_t * world)(*[len(a) for a in send])
+        rbs = (C.c_size_t * world)(*[len(a) for a in recv])
+        ok &= s.alltoallv(None, rank, sp, sbs, rp, rbs) == 0
+        ok &= all(np.all(recv[p] == 10 * p + rank) for p in range(world))
+        q.put((rank, bool(ok)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_torch_dist_transport_gloo_world_size_2():
+    """The mcs_transport callbacks over torch.distributed (gloo), called through their C
+    function pointers exactly as libmcs calls them."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 30500 + os.getpid() % 1000
+    procs = [ctx.Process(target=_transport_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+        assert p.exitcode == 0
+    res = dict(q.get(timeout=10) for _ in range(2))
+    assert res == {0: True, 1: True}

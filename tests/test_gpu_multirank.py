@@ -34,6 +34,7 @@ def _run_ranks(s, splits, **kw):
                 ctx.set_particles(s.pose12[idx], s.kf_pose12[idx])
                 out = ctx.update(s.scan_mean3, s.scan_cov6, s.D_now, s.U, raise_degenerate=False)
                 out.update(ctx.get_particles())
+                out["p2p"] = ctx.peer_migration_state
                 results[r] = out
         except Exception as e:  # pragma: no cover - surfaced below
             errors.append((r, repr(e)))
@@ -48,7 +49,7 @@ def _run_ranks(s, splits, **kw):
     for k in ("loglik", "grad6", "hess21", "psi6", "weight", "donor", "flags", "pose12",
               "kf_pose12", "L"):
         cat[k] = np.concatenate([res[k] for res in results])
-    for k in ("representative", "n_dead", "status"):
+    for k in ("representative", "n_dead", "status", "p2p"):
         vals = {res[k] for res in results}
         assert len(vals) == 1, (k, vals)
         cat[k] = vals.pop()
@@ -62,25 +63,32 @@ def _check_equal(a, b):
     assert a["representative"] == b["representative"] and a["n_dead"] == b["n_dead"]
 
 
+@pytest.mark.parametrize("pm", [1, 0])
 @pytest.mark.parametrize("G", [2, 3, 4])
-def test_multirank_equals_single_rank_c1(G):
+def test_multirank_equals_single_rank_c1(G, pm):
+    """pm = 1: clones written straight into the peer context's memory by the draws kernel;
+    pm = 0: packed + exchanged through the transport's alltoallv."""
     s = synth.c1()
     N = s.N
     one = _run_ranks(s, [np.arange(N)])
     cuts = np.linspace(0, N, G + 1).astype(int)
     cuts[1:-1] += np.arange(1, G) * 7  # uneven shards
-    many = _run_ranks(s, [np.arange(cuts[r], cuts[r + 1]) for r in range(G)])
+    many = _run_ranks(s, [np.arange(cuts[r], cuts[r + 1]) for r in range(G)],
+                      peer_migration=pm)
     assert one["n_dead"] > 0
+    assert many["p2p"] == (1 if pm else -1)
     _check_equal(many, one)
 
 
-def test_multirank_migration_heavy():
+@pytest.mark.parametrize("pm", [1, 0])
+def test_multirank_migration_heavy(pm):
     """Most particles dead and every survivor on rank 0: clones cross ranks."""
     s = synth.c1()
     N = s.N
     one = _run_ranks(s, [np.arange(N)], posterior_floor=1e-3)
     many = _run_ranks(s, [np.arange(0, 300), np.arange(300, 700), np.arange(700, N)],
-                      posterior_floor=1e-3)
+                      posterior_floor=1e-3, peer_migration=pm)
+    assert many["p2p"] == (1 if pm else -1)
     _check_equal(many, one)
     donor = one["donor"]
     assert (donor >= 0).sum() == one["n_dead"]
