@@ -230,16 +230,37 @@ def run_gpu(args):
            "representative": torch.zeros(1, dtype=torch.int32, device=dev),
            "n_dead": torch.zeros(1, dtype=torch.int64, device=dev)}
     flush = torch.empty(64 * 2**20, dtype=torch.float32, device=dev)  # 256 MiB > 126 MB L2
-    ctx.set_profiling(True)
+    # single GPU: the whole update is captured once into a CUDA graph and replayed (the
+    # SURVEY 8(d) protocol); multi-rank updates have host-side exchange steps, so they run eagerly
+    use_graph = world == 1 and not args.no_graph
+    graph = None
+    if use_graph:
+        ctx.set_profiling(False)
+        ctx.restore()
+        torch.cuda.synchronize()
+        with torch.cuda.stream(stream):  # one eager update first (allocator pools, CUB temp)
+            ctx.update_async(d_m, d_c, s.D_now, s.U, out, stream=stream)
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        ctx.restore()
+        torch.cuda.synchronize()
+        with torch.cuda.graph(graph, stream=stream):
+            ctx.update_async(d_m, d_c, s.D_now, s.U, out, stream=stream)
+        torch.cuda.synchronize()
+    else:
+        ctx.set_profiling(True)
 
-    def one_step():
+    def one_step(profiled=False):
         with torch.cuda.stream(stream):
             ctx.restore()
             flush.fill_(1.0)
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            ctx.update_async(d_m, d_c, s.D_now, s.U, out, stream=stream)
+            if graph is not None and not profiled:
+                graph.replay()
+            else:
+                ctx.update_async(d_m, d_c, s.D_now, s.U, out, stream=stream)
             e1.record(stream)
         return e0, e1
 
@@ -255,13 +276,23 @@ def run_gpu(args):
             e0, e1 = one_step()
             e1.synchronize()
             step_ms.append(e0.elapsed_time(e1))
-            ph = ctx.phase_ms()
-            phases.append(ph)
-            sweep_ms.append(ph["sweep"])
+            if graph is None:
+                ph = ctx.phase_ms()
+                phases.append(ph)
+                sweep_ms.append(ph["sweep"])
         torch.cuda.synchronize()
         if dist:
             dist.barrier()
         torch.cuda.synchronize()
+    if graph is not None:  # phase breakdown (roofline) from profiled eager updates, untimed
+        ctx.set_profiling(True)
+        for k in range(max(3, min(args.steps, 10))):
+            e0, e1 = one_step(profiled=True)
+            e1.synchronize()
+            ph = ctx.phase_ms()
+            phases.append(ph)
+            sweep_ms.append(ph["sweep"])
+        ctx.set_profiling(False)
     total_ms = float(np.sum(step_ms))
     if dist:  # the job's time is the slowest rank's
         t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
@@ -307,7 +338,11 @@ def run_gpu(args):
                    "keyframes": K, "parallelism": f"particle shards x{world} (NCCL)",
                    "keyframe_cells": int(sum(len(k[0]) for k in s.keyframes)),
                    "l2": "particle state restored from a device snapshot and 256 MiB L2 flush "
-                         "before every timed step (untimed)"},
+                         "before every timed step (untimed)",
+                   "timed": ("CUDA-graph replay of the whole update (a1-a7)" if use_graph
+                             else "eager mcs_update_async (multi-rank exchange steps)"),
+                   "phases": ("from separate profiled eager updates" if use_graph
+                              else "library phase events of the timed updates")},
         "roofline": {"kernel": "sweep (a2)", "bound": "alu", "achieved": achieved,
                      "peak": fp32_peak, "unit": "TFLOP/s", "frac": achieved / fp32_peak,
                      "traffic": committed_traffic(),
@@ -348,6 +383,7 @@ def main():
     ap.add_argument("--cpu-budget-s", type=float, default=12.0)
     ap.add_argument("--ref-step-s", type=float, default=4.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="eager updates in the timed loop")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
