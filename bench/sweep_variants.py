@@ -33,12 +33,15 @@ def run_one(name):
     ctx.set_particles(s.pose12, s.kf_pose12)
     ctx.snapshot()
     ctx.set_profiling(True)
-    sw = []
+    sw, sel = [], []
     for k in range(8):
         ctx.restore()
         ctx.update(s.scan_mean3, s.scan_cov6, s.D_now, s.U, outputs=("loglik",))
         if k >= 3:
-            sw.append(ctx.phase_ms()["sweep"])
+            ph = ctx.phase_ms()
+            sw.append(ph["sweep"])
+            sel.append(ph["select"])
+    print(json.dumps({"select_ms": float(np.median(sel))}), file=sys.stderr)
     return float(np.median(sw))
 
 
@@ -52,4 +55,4 @@ if __name__ == "__main__":
             env = dict(os.environ, MCS_LIB=os.path.join(OUT, f"libmcs_{name}.so"))
             r = subprocess.run([sys.executable, __file__, "one", name], env=env,
                                capture_output=True, text=True)
-            print(r.stdout.strip() or r.stderr[-500:], flush=True)
+            print(r.stdout.strip(), r.stderr.strip()[-200:], flush=True)

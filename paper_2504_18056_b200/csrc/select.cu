@@ -18,10 +18,17 @@ namespace mcs {
 
 // Lane-coherence sort key of a work item: the keyframe id in the top bits, then
 // a 6-D Morton code of where the item's relative pose sends two reference points 8 m out on
-// the x and y axes, at 1/16 m steps (6 bits per coordinate, wrapping every 4 m).  Items that
+// the x and y axes, at 1/8 m steps (5 bits per coordinate, wrapping every 4 m: one radix pass
+// fewer than 6 bits at 1/16 m, same sweep time).  Items that
 // are adjacent in this order probe the same cells for the same scan point, so a warp's
 // gathers coalesce and its hit/miss branches agree.
-constexpr int kMortonBitsPerDim = 6;
+#ifndef MCS_MORTON_BITS
+#define MCS_MORTON_BITS 5
+#endif
+#ifndef MCS_MORTON_SCALE
+#define MCS_MORTON_SCALE 8.0f
+#endif
+constexpr int kMortonBitsPerDim = MCS_MORTON_BITS;
 constexpr int kMortonBits = 6 * kMortonBitsPerDim;
 
 __device__ __forceinline__ unsigned long long coherence_key(int kf, const float* rel) {
@@ -34,7 +41,8 @@ __device__ __forceinline__ unsigned long long coherence_key(int kf, const float*
   }
   unsigned int c[6];
 #pragma unroll
-  for (int k = 0; k < 6; ++k) c[k] = (unsigned int)__float2int_rd(q[k] * 16.0f) & 63u;
+  for (int k = 0; k < 6; ++k)
+    c[k] = (unsigned int)__float2int_rd(q[k] * MCS_MORTON_SCALE) & ((1u << kMortonBitsPerDim) - 1u);
   unsigned long long m = 0ull;
 #pragma unroll
   for (int b = kMortonBitsPerDim - 1; b >= 0; --b)
