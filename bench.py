@@ -304,12 +304,16 @@ def run_gpu(args):
     # e2e: the public synchronous call with pinned host buffers (H2D scan, D2H results)
     h_m = torch.from_numpy(s.scan_mean3).pin_memory()
     h_c = torch.from_numpy(s.scan_cov6).pin_memory()
+    h_out = {"loglik": torch.empty(N, dtype=torch.float64).pin_memory(),
+             "weight": torch.empty(N, dtype=torch.float64).pin_memory()}
     e2e_t = []
     for k in range(args.warmup + args.steps):
         ctx.restore()
+        with torch.cuda.stream(stream):
+            flush.fill_(1.0)  # same L2 state as the device-timed steps (untimed)
         torch.cuda.synchronize()
         t1 = time.perf_counter()
-        r = ctx.update(h_m, h_c, s.D_now, s.U, outputs=("loglik", "weight"))
+        r = ctx.update(h_m, h_c, s.D_now, s.U, outputs=(), out=h_out)
         t2 = time.perf_counter()
         if k >= args.warmup:
             e2e_t.append(t2 - t1)

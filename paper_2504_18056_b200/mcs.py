@@ -302,17 +302,31 @@ class Context:
 
     # -------------------------------------------------------------- hot path
     def update(self, scan_mean3, scan_cov6, D_now: float, U: int, outputs=None,
-               raise_degenerate=True):
+               raise_degenerate=True, out=None):
         """mcs_update; returns a dict of numpy outputs (host).  outputs: iterable of names
-        among loglik, grad6, hess21, psi6, weight, donor, flags (default all)."""
+        among loglik, grad6, hess21, psi6, weight, donor, flags (default all).  out: optional
+        dict name -> caller-owned host buffer (numpy array or CPU tensor, e.g. pinned, of the
+        output's dtype and size) written in place instead of fresh arrays."""
         n, _ = self.sizes
+        out = out or {}
         names = ("loglik", "grad6", "hess21", "psi6", "weight", "donor", "flags") \
             if outputs is None else tuple(outputs)
+        names = tuple(dict.fromkeys(names + tuple(out)))
         shapes = {"loglik": ((n,), np.float64), "grad6": ((n, 6), np.float32),
                   "hess21": ((n, 21), np.float32), "psi6": ((n, 6), np.float32),
                   "weight": ((n,), np.float64), "donor": ((n,), np.int32),
                   "flags": ((n,), np.uint8)}
-        res = {k: np.zeros(*shapes[k]) for k in names}
+        res = {}
+        for k in names:
+            if k in out:
+                a = out[k].numpy() if hasattr(out[k], "numpy") else out[k]
+                if (a.dtype != shapes[k][1] or a.size != int(np.prod(shapes[k][0])) or
+                        not a.flags.c_contiguous):
+                    raise ValueError(f"out[{k!r}] must be a contiguous {shapes[k][1].__name__} "
+                                     f"buffer of {int(np.prod(shapes[k][0]))} elements")
+                res[k] = a.reshape(shapes[k][0])
+            else:
+                res[k] = np.zeros(*shapes[k])
         rep = np.zeros(1, np.int32)
         nd = np.zeros(1, np.int64)
         uo = UpdateOut(**{k: (res[k].ctypes.data if k in res else None)
