@@ -139,16 +139,34 @@ def oracle_step(s, n: int, start: int):
     return time.perf_counter() - t0
 
 
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_baseline(s, budget_s: float = 12.0):
     import oracle
     oracle.build()
     oracle_step.kfs = oracle.Keyframes(s.keyframes, s.D, s.r)
+    cores = oracle.num_threads()
     t = oracle_step(s, 64, 0)  # calibration
     n = int(min(s.N, max(64, 64 * budget_s / max(t, 1e-3))))
     t = oracle_step(s, n, 1)
-    return {"value": n * s.S / t, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
+    # one single-thread run on a smaller sample (~budget/4), the per-core figure
+    oracle.set_num_threads(1)
+    n1 = int(min(s.N, max(8, (n / cores) * 0.25)))
+    t1 = oracle_step(s, n1, 2)
+    oracle.set_num_threads(cores)
+    return {"value": n * s.S / t, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "cpu_model": cpu_model(), "single_thread_value": n1 * s.S / t1,
             "sample": f"{n} of {s.N} particles (strided), full 4096-pt scan, 20 keyframes, "
-                      f"whole update a1-a7 on the sample; {t:.2f} s"}, t
+                      f"whole update a1-a7 on the sample; {t:.2f} s on {cores} threads "
+                      f"(+ {n1} particles on 1 thread, {t1:.2f} s)"}, t
 
 
 def run_reference(args):

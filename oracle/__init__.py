@@ -132,6 +132,7 @@ def lib():
         L.orc_update.argtypes = [vp, i32, vp, vp, f64, i32, vp, vp, i32, vp, vp, vp, i32, u32, vp]
         L.orc_update.restype = C.c_int
         L.orc_num_threads.restype = C.c_int
+        L.orc_set_num_threads.argtypes = [C.c_int]
         L.orc_philox4x32_10.argtypes = [vp, vp, vp]
         L.orc_normals8.argtypes = [C.c_uint64, C.c_uint64, C.c_int64, vp]
         L.orc_predict.argtypes = [i32, vp, vp, vp, C.c_uint64, C.c_uint64, C.c_int64, f64]
@@ -151,6 +152,10 @@ def _c(a, dt):
 
 def num_threads() -> int:
     return int(lib().orc_num_threads())
+
+
+def set_num_threads(n: int) -> None:
+    lib().orc_set_num_threads(int(n))
 
 
 # ---------------------------------------------------------------- SE(3)

@@ -174,6 +174,7 @@ void orc_normals8(uint64_t seed, uint64_t frame, int64_t gi, double z[8]);
 double orc_overlap(const orc_map* m, const float* mean3, int32_t S, const float rel32[12]);
 
 int orc_num_threads(void);
+void orc_set_num_threads(int n);  /* OpenMP threads of the particle loops (timing only) */
 
 #ifdef __cplusplus
 }
