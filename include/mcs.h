@@ -132,6 +132,9 @@ typedef struct mcs_config {
                                     processes) when every rank's state is reachable, else (and
                                     with 0) packed and exchanged by NCCL send/recv or the
                                     transport's alltoallv                                     */
+  int32_t  graph_replay;         /* 1 (default): a single-rank update body is captured once into
+                                    a CUDA graph and replayed while the scan size, particle and
+                                    keyframe counts stay the same; 0: launched kernel by kernel */
 } mcs_config;
 
 /* Fills *cfg with the defaults above (capacities 0: caller sets them). */

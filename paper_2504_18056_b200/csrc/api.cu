@@ -206,6 +206,8 @@ static void free_all(mcs_ctx* c) {
   for (void* p : ptrs) mem_free(c, p);
   if (c->h_scal) cudaFreeHost(c->h_scal);
   if (c->h_stage) cudaFreeHost(c->h_stage);
+  if (c->gexec) cudaGraphExecDestroy(c->gexec);
+  c->gexec = nullptr;
   dist_destroy(c);
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
@@ -252,6 +254,7 @@ void mcs_config_default(mcs_config* cfg) {
   cfg->nn_radius = 0.0f;
   cfg->clone_split = 0;
   cfg->peer_migration = 1;
+  cfg->graph_replay = 1;
   cfg->rank = 0;
   cfg->world_size = 1;
   cfg->nccl_unique_id = nullptr;
@@ -301,9 +304,10 @@ mcs_status mcs_create(const mcs_config* cfg, mcs_ctx** out) {
       (cfg->corr_mode == MCS_CORR_NN27 &&
        !(cfg->nn_radius > 0.0f && cfg->nn_radius <= cfg->voxel_resolution)) ||
       (cfg->clone_split != 0 && cfg->clone_split != 1) ||
-      (cfg->peer_migration != 0 && cfg->peer_migration != 1)) {
+      (cfg->peer_migration != 0 && cfg->peer_migration != 1) ||
+      (cfg->graph_replay != 0 && cfg->graph_replay != 1)) {
     g_create_error = "corr_mode must be CELL or NN27 (with 0 < nn_radius <= voxel_resolution), "
-                     "clone_split and peer_migration 0 or 1";
+                     "clone_split, peer_migration and graph_replay 0 or 1";
     return MCS_E_INVALID_ARG;
   }
   if (cfg->world_size < 1 || cfg->rank < 0 || cfg->rank >= cfg->world_size) {
@@ -636,7 +640,7 @@ static void record(mcs_ctx* ctx, int k) {
 }
 
 // the hot path a1..a7, stream-ordered; scan already prepared in d_scan
-static mcs_status run_update(mcs_ctx* ctx, int n_pts, double D_now, uint32_t U) {
+static mcs_status run_update_body(mcs_ctx* ctx, int n_pts, uint32_t U) {
   const int iters = ctx->cfg.gn_iterations > 0 ? ctx->cfg.gn_iterations : 1;
   const bool post = ctx->cfg.weight_after_update != 0;
   record(ctx, 0);
@@ -647,7 +651,7 @@ static mcs_status run_update(mcs_ctx* ctx, int n_pts, double D_now, uint32_t U) 
     if (it == 0) record(ctx, 2);
     launch_combine(ctx, n_pts, (it == 0 && !post) ? kCombineUpdateWeight : kCombineUpdate,
                    nullptr, nullptr, nullptr, nullptr, nullptr, nullptr);  // a3 (+ L += l)
-    launch_propagate(ctx, D_now);                                       // a4
+    launch_propagate(ctx);                                              // a4
   }
   if (post) {  // R13 variant: weight with l re-evaluated at the updated poses
     launch_select(ctx, kSelectWeight);
@@ -659,6 +663,44 @@ static mcs_status run_update(mcs_ctx* ctx, int n_pts, double D_now, uint32_t U) 
   const mcs_status s = launch_weights_resample(ctx, U);                 // a5-a7 (+ exchanges)
   record(ctx, 4);
   return s;
+}
+
+// The update body (a1-a7) of a single-rank context is captured once into a CUDA graph and
+// replayed while its shape holds (scan size, particle and keyframe counts); the per-update
+// scalars D_now and U reach it through d_scal (launch_set_params, outside the graph).
+// Multi-rank updates (host-side exchange steps), profiled updates (phase events) and calls
+// made inside the caller's own stream capture run the body directly.
+static mcs_status run_update(mcs_ctx* ctx, int n_pts, double D_now, uint32_t U) {
+  launch_set_params(ctx, D_now, U);
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(ctx->stream, &cap);
+  const bool graph = ctx->cfg.graph_replay && !ctx->graph_off && !ctx->profiling &&
+                     !dist_active(ctx) && cap == cudaStreamCaptureStatusNone;
+  if (!graph) return run_update_body(ctx, n_pts, U);
+  const long long key[4] = {n_pts, ctx->N, ctx->K, 0};
+  if (!ctx->gexec || memcmp(key, ctx->gkey, sizeof(key)) != 0) {
+    if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
+    ctx->gexec = nullptr;
+    cudaGraph_t g = nullptr;
+    if (cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+      cudaGetLastError();
+      ctx->graph_off = true;
+      return run_update_body(ctx, n_pts, U);
+    }
+    const mcs_status s = run_update_body(ctx, n_pts, U);
+    const cudaError_t ec = cudaStreamEndCapture(ctx->stream, &g);
+    cudaError_t ei = cudaErrorUnknown;
+    if (s == MCS_OK && ec == cudaSuccess && g) ei = cudaGraphInstantiate(&ctx->gexec, g, 0);
+    if (g) cudaGraphDestroy(g);
+    if (ei != cudaSuccess) {  // not capturable here: eager from now on
+      ctx->gexec = nullptr;
+      cudaGetLastError();
+      ctx->graph_off = true;
+      return run_update_body(ctx, n_pts, U);
+    }
+    memcpy(ctx->gkey, key, sizeof(key));
+  }
+  return cudaGraphLaunch(ctx->gexec, ctx->stream) == cudaSuccess ? MCS_OK : MCS_E_CUDA;
 }
 
 mcs_status mcs_update(mcs_ctx* ctx, const float* scan_mean3, const float* scan_cov6,

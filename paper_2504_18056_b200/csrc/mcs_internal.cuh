@@ -112,6 +112,8 @@ struct Scalars {                // device-side reduction results of one update
   long long rep;                // representative (global index)
   int32_t status;               // 0 ok, MCS_E_DEGENERATE
   unsigned int counter[8];      // last-block counters (reset by the last block)
+  double D_now;                 // per-update parameters, written by set_params_kernel before
+  unsigned int U;               // the update body (so a captured CUDA graph can be replayed)
 };
 
 }  // namespace mcs
@@ -195,6 +197,10 @@ struct mcs_ctx {
   size_t d_ag_bytes = 0;
   // peer-direct migration (cfg.peer_migration): 0 not set up yet, 1 on, -1 off
   int p2p = 0;
+  // CUDA graph of the single-rank update body (run_update), replayed while its key holds
+  cudaGraphExec_t gexec = nullptr;
+  long long gkey[4] = {-1, -1, -1, -1};  // n_pts, N, K, flags
+  bool graph_off = false;                // capture failed once: eager from then on
   mcs::PeerView* d_peers = nullptr;    // [world] device views of every rank's state
   std::vector<void*> ipc_opened;       // CUDA IPC mappings of other processes' buffers
 };
@@ -228,7 +234,9 @@ enum { kCombineEval = 0, kCombineUpdateWeight = 1, kCombineUpdate = 2, kCombineW
 void launch_combine(mcs_ctx* c, int S, int mode, double* slot_l, float* slot_H21,
                     float* slot_b6, int32_t* slot_n, int32_t* slot_kf, uint8_t* loop_out);
 // a4
-void launch_propagate(mcs_ctx* c, double D_now);
+void launch_propagate(mcs_ctx* c);  // D_now from d_scal (launch_set_params)
+// writes D_now and U into d_scal (a tiny kernel: by value, outside any captured graph)
+void launch_set_params(mcs_ctx* c, double D_now, uint32_t U);
 // a5-a7 (+ the exchange steps when world > 1); degenerate status in d_scal
 mcs_status launch_weights_resample(mcs_ctx* c, uint32_t U);
 // isolated respawn on caller arrays (single device)

@@ -301,13 +301,15 @@ void launch_combine(mcs_ctx* c, int S, int mode, double* slot_l, float* slot_H21
 __global__ void propagate_kernel(float* __restrict__ kfpose, int capK, int K, int N,
                                  const uint8_t* __restrict__ flags, const int32_t* __restrict__ to,
                                  const double* __restrict__ psi, int capN,
-                                 const double* __restrict__ D, double D_now) {
+                                 const double* __restrict__ D,
+                                 const Scalars* __restrict__ sc) {
   const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= (long long)N * K) return;
   const int i = (int)(t / K), k = (int)(t - (long long)i * K);
   if (!(flags[i] & 2)) return;
   const int t_o = to[i];
   if (k < t_o) return;  // older keyframes untouched (R15)
+  const double D_now = sc->D_now;
   const double den = D_now - D[t_o];
   if (!(den > 0.0)) return;
   const double r = (D[k] - D[t_o]) / den;  // Eqs.8-9 (R14)
@@ -330,12 +332,22 @@ __global__ void propagate_kernel(float* __restrict__ kfpose, int capK, int K, in
   q4[2] = make_float4(T[8], T[9], T[10], T[11]);
 }
 
-void launch_propagate(mcs_ctx* c, double D_now) {
+void launch_propagate(mcs_ctx* c) {
   const long long total = (long long)c->N * c->K;
   if (total == 0) return;
   const int grid = (int)((total + 255) / 256);
   propagate_kernel<<<grid, 256, 0, c->stream>>>(c->d_kfpose, c->capK, c->K, c->N, c->d_flags,
-                                                c->d_to, c->d_psi, c->capN, c->d_D, D_now);
+                                                c->d_to, c->d_psi, c->capN, c->d_D, c->d_scal);
+}
+
+// the per-update scalars, by value at launch (outside any captured graph)
+__global__ void set_params_kernel(Scalars* sc, double D_now, unsigned int U) {
+  sc->D_now = D_now;
+  sc->U = U;
+}
+
+void launch_set_params(mcs_ctx* c, double D_now, uint32_t U) {
+  set_params_kernel<<<1, 1, 0, c->stream>>>(c->d_scal, D_now, U);
 }
 
 }  // namespace mcs

@@ -120,8 +120,7 @@ __device__ __forceinline__ long long draws_below(unsigned long long c, long long
 
 // n(C_i) on the GLOBAL ladder for every local particle; compacted list of local dead slots
 __global__ void ncum_dead_kernel(const Rung* __restrict__ scan, int N,
-                                 const Scalars* __restrict__ sc, unsigned int U,
-                                 long long* __restrict__ ncum, int32_t* __restrict__ dead_list,
+                                 const Scalars* __restrict__ sc, long long* __restrict__ ncum, int32_t* __restrict__ dead_list,
                                  int32_t* __restrict__ donor_local, int32_t* __restrict__ donor_g) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= N) return;
@@ -132,17 +131,17 @@ __global__ void ncum_dead_kernel(const Rung* __restrict__ scan, int N,
   donor_local[i] = -1;
   if (donor_g) donor_g[i] = -1;
   if (sc->D_tot == 0 || sc->Q_tot == 0) return;
-  ncum[i] = draws_below(sc->q_off + s.C, sc->D_tot, sc->Q_tot, U);
+  ncum[i] = draws_below(sc->q_off + s.C, sc->D_tot, sc->Q_tot, sc->U);
 }
 
 // R34 (flag clone_split): a survivor with c draws shares its weight with its clones; it and
 // each clone get L - ln(1 + c).  Runs before pack/clone, which copy the adjusted L.
 __global__ void split_kernel(const long long* __restrict__ ncum, int N,
-                             const Scalars* __restrict__ sc, unsigned int U,
-                             double* __restrict__ L) {
+                             const Scalars* __restrict__ sc, double* __restrict__ L) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= N || sc->D_tot == 0 || sc->Q_tot == 0) return;
-  const long long prev = i > 0 ? ncum[i - 1] : draws_below(sc->q_off, sc->D_tot, sc->Q_tot, U);
+  const long long prev =
+      i > 0 ? ncum[i - 1] : draws_below(sc->q_off, sc->D_tot, sc->Q_tot, sc->U);
   const long long copies = ncum[i] - prev;
   if (copies > 0) L[i] -= log((double)(1 + copies));
 }
@@ -531,9 +530,9 @@ mcs_status launch_weights_resample(mcs_ctx* c, uint32_t U) {
     n_draws_bound = h_clones;
     if (!p2p) MCS_TRY(ensure_xfer(c, std::max(n_send, n_recv)));
   }
-  ncum_dead_kernel<<<g, kWT, 0, st>>>(scan, N, sc, U, c->d_ncum, c->d_dead_list, c->d_donor,
+  ncum_dead_kernel<<<g, kWT, 0, st>>>(scan, N, sc, c->d_ncum, c->d_dead_list, c->d_donor,
                                       c->d_donor_g);
-  if (c->cfg.clone_split) split_kernel<<<g, kWT, 0, st>>>(c->d_ncum, N, sc, U, c->d_L);
+  if (c->cfg.clone_split) split_kernel<<<g, kWT, 0, st>>>(c->d_ncum, N, sc, c->d_L);
   if (p2p) {
     // every rank's dead list is complete before any rank writes into it
     MCS_TRY(dist_barrier(c));
@@ -600,11 +599,12 @@ mcs_status launch_resample_only(mcs_ctx* c, const double* d_e, const uint8_t* d_
   Rung* rung = reinterpret_cast<Rung*>(c->d_ladder);
   Rung* scan = reinterpret_cast<Rung*>(c->d_ladder_scan);
   const int g = (n + kWT - 1) / kWT;
+  launch_set_params(c, 0.0, U);
   rung_from_inputs_kernel<<<g, kWT, 0, st>>>(d_e, d_dead, n, rung);
   size_t tb = c->cub_temp_bytes;
   MCS_CUDA(cub::DeviceScan::InclusiveScan(c->d_cub_temp, tb, rung, scan, RungSum(), n, st));
   totals_kernel<<<1, 1, 0, st>>>(scan, n, 1, c->d_scal);
-  ncum_dead_kernel<<<g, kWT, 0, st>>>(scan, n, c->d_scal, U, c->d_ncum, c->d_dead_list, d_donor,
+  ncum_dead_kernel<<<g, kWT, 0, st>>>(scan, n, c->d_scal, c->d_ncum, c->d_dead_list, d_donor,
                                       nullptr);
   draws_kernel<<<g, kWT, 0, st>>>(c->d_ncum, n, c->d_scal, 1, 0, 0, nullptr, c->d_dead_list,
                                   d_donor, nullptr, nullptr);

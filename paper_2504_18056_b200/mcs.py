@@ -60,6 +60,7 @@ class Config(C.Structure):
         ("clone_split", C.c_int32),
         ("allocator", C.c_void_p),
         ("peer_migration", C.c_int32),
+        ("graph_replay", C.c_int32),
     ]
 
 
