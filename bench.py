@@ -35,7 +35,7 @@ FLOPS_MATCHED = 236.0    # FP32 flops per matched (particle, point, slot) with H
 FLOPS_UNMATCHED = 21.0   # transform + key for an unmatched triple
 GATHER_MATCHED = 56.0    # bytes: 8-B key probe + 48-B payload
 GATHER_UNMATCHED = 8.0
-LAUNCHES_PER_UPDATE = 25  # kernels per mcs_update_async incl. CUB sort/scan (profiles/r01_launch_shares.txt)
+LAUNCHES_PER_UPDATE = 26  # kernels per mcs_update_async incl. CUB sort/scan + set_params (profiles/r01_launches.csv)
 
 
 def dist_env():
