@@ -29,6 +29,9 @@ namespace mcs {
 #ifndef MCS_SWEEP_AHEAD
 #define MCS_SWEEP_AHEAD 4   // 4: probes issued in batches of two, two points ahead; 1: one ahead
 #endif
+#ifndef MCS_SWEEP_TMA
+#define MCS_SWEEP_TMA 0  // 1: scan stages double-buffered by TMA bulk copies + mbarriers
+#endif
 #ifndef MCS_SWEEP_MINBLOCKS
 #define MCS_SWEEP_MINBLOCKS 4
 #endif
@@ -68,6 +71,33 @@ __device__ __forceinline__ void ld_slot(const float4* sl, float4& s0, float4& s1
   s2.w = 0.f;
 }
 
+// ---- TMA bulk-copy staging (MCS_SWEEP_TMA): mbarrier + cp.async.bulk wrappers ----
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_stage(void* dst, const void* src, uint32_t bytes,
+                                           uint64_t* bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+      ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
 // floor(x) as the bits of x + 1.5*2^23 rounded toward -inf: exact for |x| < 2^22, and every
 // other finite x maps far outside any keyframe bbox after the offset.
 constexpr float kMagic = 12582912.0f;
@@ -81,12 +111,14 @@ __global__ void __launch_bounds__(kSweepThreads, MCS_SWEEP_MINBLOCKS)
                  double* __restrict__ part) {
   // dynamic shared memory: [(kChunk + 2) * 3] float4 scan stage, then [28][threads] fp64 totals
   extern __shared__ float4 smem_dyn[];
-  float4* s_pt = smem_dyn;
+  float4* s_pt = smem_dyn;  // the current stage (MCS_SWEEP_TMA: one of two buffers)
+  constexpr int kStage = (kChunk + 2) * 3;  // float4 per stage buffer (2 spare points)
+  constexpr int kBufs = MCS_SWEEP_TMA ? 2 : 1;
   // two-level accumulation: fp32 registers within a stage, fp64 totals per thread in shared
   // memory across stages (the fp32 running sums over a whole 4,096-point scan lose ~1e-5
   // relative, which an ill-conditioned H turns into >1e-5 m of pose error)
   double(*s_acc)[kSweepThreads] =
-      reinterpret_cast<double(*)[kSweepThreads]>(smem_dyn + (kChunk + 2) * 3);
+      reinterpret_cast<double(*)[kSweepThreads]>(smem_dyn + kBufs * kStage);
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   const int item = t < n_items ? order[t] : -1;
   float4 r0 = make_float4(0, 0, 0, 0), r1 = r0, r2 = r0, inf = r0;
@@ -331,17 +363,11 @@ __global__ void __launch_bounds__(kSweepThreads, MCS_SWEEP_MINBLOCKS)
     }
   };
 
-  if (threadIdx.x < 6) s_pt[3 * kChunk + threadIdx.x] = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (int base = 0; base < S; base += kChunk) {
-    const int cnt = min(kChunk, S - base);
-    __syncthreads();
-    for (int k = threadIdx.x; k < cnt * 3; k += kSweepThreads) s_pt[k] = scan[3 * base + k];
-    __syncthreads();
-    if (!active) continue;
+  // the math of one stage of cnt points in s_pt (active threads)
+  auto stage = [&](const int cnt) {
     if (kCorr == MCS_CORR_NN27) {
       for (int j = 0; j < cnt; ++j) nn27_point(j);
-      flush();
-      continue;
+      return;
     }
     // Probe buffers in rotation, no register copies between iterations.  Every probe load
     // shares one scoreboard, so any wait drains all loads issued so far: the loop therefore
@@ -381,8 +407,68 @@ __global__ void __launch_bounds__(kSweepThreads, MCS_SWEEP_MINBLOCKS)
     }
     if (j < cnt) consume(j, pa);
 #endif
+  };
+
+#if MCS_SWEEP_TMA
+  // Scan stages double-buffered in shared memory by TMA bulk copies (cp.async.bulk, one thread
+  // issues, an mbarrier counts the bytes).  No CTA-wide barrier per stage: the last warp to
+  // finish stage k (a shared-memory counter) refills that buffer with stage k + 2, so fast
+  // warps run up to a stage ahead of slow ones.
+  uint64_t* full = reinterpret_cast<uint64_t*>(&s_acc[28][0]);  // [2] mbarriers
+  int* done = reinterpret_cast<int*>(full + 2);                   // [2] warps done with stage
+  const int n_stages = (S + kChunk - 1) / kChunk;
+  constexpr int kWarps = kSweepThreads / 32;
+  auto refill = [&](int k) {  // one thread: stage k into buffer k & 1
+    const int cnt = min(kChunk, S - k * kChunk);
+    bulk_stage(smem_dyn + (k & 1) * kStage, scan + 3 * (size_t)k * kChunk, 48u * cnt,
+               &full[k & 1]);
+  };
+  if (threadIdx.x < 12)
+    smem_dyn[(threadIdx.x / 6) * kStage + 3 * kChunk + threadIdx.x % 6] =
+        make_float4(0.f, 0.f, 0.f, 0.f);
+  if (threadIdx.x == 0) {
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
+    done[0] = done[1] = 0;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    refill(0);
+    if (n_stages > 1) refill(1);
+  }
+  for (int k = 0; k < n_stages; ++k) {
+    s_pt = smem_dyn + (k & 1) * kStage;
+    mbar_wait(&full[k & 1], (k >> 1) & 1);
+    if (active) {
+      stage(min(kChunk, S - k * kChunk));
+      flush();
+    }
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) {
+      __threadfence_block();  // this warp's reads of the buffer precede the count
+      if (atomicAdd(&done[k & 1], 1) == kWarps - 1) {
+        done[k & 1] = 0;
+        if (k + 2 < n_stages) {
+          __threadfence_block();
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          refill(k + 2);
+        }
+      }
+    }
+  }
+#else
+  if (threadIdx.x < 6) s_pt[3 * kChunk + threadIdx.x] = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int base = 0; base < S; base += kChunk) {
+    const int cnt = min(kChunk, S - base);
+    __syncthreads();
+    for (int k = threadIdx.x; k < cnt * 3; k += kSweepThreads) s_pt[k] = scan[3 * base + k];
+    __syncthreads();
+    if (!active) continue;
+    stage(cnt);
     flush();
   }
+#endif
   if (!active) return;
   double* o = part + (size_t)item * kSlotWords;
   o[0] = s_acc[0][threadIdx.x];
@@ -457,7 +543,8 @@ void launch_sweep(mcs_ctx* c, int S) {
   const int n_items = c->cfg.neighbor_count * c->N;
   const int grid = (n_items + kSweepThreads - 1) / kSweepThreads;
   const float inv_r = 1.0f / c->cfg.voxel_resolution;
-  constexpr size_t smem = sizeof(float4) * (kChunk + 2) * 3 + sizeof(double) * 28 * kSweepThreads;
+  constexpr size_t smem = sizeof(float4) * (kChunk + 2) * 3 * (MCS_SWEEP_TMA ? 2 : 1) +
+                          sizeof(double) * 28 * kSweepThreads + (MCS_SWEEP_TMA ? 32 : 0);
   static bool attr_set[128] = {};  // opt in beyond 48 KB once per device (both instantiations)
   if (c->dev < 0 || c->dev >= 128 || !attr_set[c->dev]) {
     cudaFuncSetAttribute(sweep_kernel<MCS_CORR_CELL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
