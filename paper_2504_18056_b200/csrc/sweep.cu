@@ -311,31 +311,51 @@ __global__ void __launch_bounds__(kSweepThreads, MCS_SWEEP_MINBLOCKS)
     const unsigned int bz = (unsigned)__float_as_int(fyz.y) - offz;
     int best = -1;
     float best_d2 = 0.f;
-    for (int oz = -1; oz <= 1; ++oz)
-      for (int oy = -1; oy <= 1; ++oy)
-        for (int ox = -1; ox <= 1; ++ox) {
-          const unsigned int cx = bx + ox, cy = by + oy, cz = bz + oz;
-          if (!((cx < m.ex) & (cy < m.ey) & (cz < m.ez))) continue;
-          const unsigned int key = local_key(cx, cy, cz);
-          unsigned int h = slot_hash(key, m.shift) & m.mask;
+    // candidate: keep the nearest within the radius; strict < keeps the lower enumeration
+    // index on ties (cells are visited in (oz, oy, ox) order)
+    auto consider = [&](unsigned int h, const float4 t0) {  // t0 = {key, mu'} of slot h
+      const float dx = __fsub_rn(t0.y, p.qx);
+      const float dy = __fsub_rn(t0.z, p.qyz.x);
+      const float dz = __fsub_rn(t0.w, p.qyz.y);
+      const float d2 = __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, __fmul_rn(dx, dx)));
+      if (d2 <= nn_r2 && (best < 0 || d2 < best_d2)) {
+        best = (int)h;
+        best_d2 = d2;
+      }
+    };
+#pragma unroll
+    for (int oz = -1; oz <= 1; ++oz) {
+      // one z-layer at a time: the nine first-probe loads (key + mu', 16 B) issue together
+      unsigned int key[9], h[9];
+      float4 t[9];
+#pragma unroll
+      for (int c = 0; c < 9; ++c) {
+        const unsigned int cx = bx + (c % 3 - 1), cy = by + (c / 3 - 1), cz = bz + oz;
+        const bool in = (cx < m.ex) & (cy < m.ey) & (cz < m.ez);
+        key[c] = in ? local_key(cx, cy, cz) : kNoKey32;
+        h[c] = in ? slot_hash(key[c], m.shift) : m.mask + 1;  // sentinel: always empty
+        t[c] = __ldg(m.slots + 4 * (size_t)h[c]);
+      }
+#pragma unroll
+      for (int c = 0; c < 9; ++c) {
+        const unsigned int k0 = __float_as_uint(t[c].x);
+        if (k0 == key[c]) {
+          consider(h[c], t[c]);
+        } else if (k0 != kEmptyKey32) {  // rare: continue linear probing
+          unsigned int hh = h[c];
           while (true) {
-            const float4 t0 = __ldg(m.slots + 4 * (size_t)h);
-            const unsigned int k = __float_as_uint(t0.x);
-            if (k == key) {
-              const float dx = __fsub_rn(t0.y, p.qx);
-              const float dy = __fsub_rn(t0.z, p.qyz.x);
-              const float dz = __fsub_rn(t0.w, p.qyz.y);
-              const float d2 = __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, __fmul_rn(dx, dx)));
-              if (d2 <= nn_r2 && (best < 0 || d2 < best_d2)) {
-                best = (int)h;
-                best_d2 = d2;
-              }
+            hh = (hh + 1) & m.mask;
+            const float4 tt = __ldg(m.slots + 4 * (size_t)hh);
+            const unsigned int kk = __float_as_uint(tt.x);
+            if (kk == key[c]) {
+              consider(hh, tt);
               break;
             }
-            if (k == kEmptyKey32) break;
-            h = (h + 1) & m.mask;
+            if (kk == kEmptyKey32) break;
           }
         }
+      }
+    }
     if (best >= 0) {
       const float4* sl = m.slots + 4 * (size_t)best;
       p.s0 = __ldg(sl);
@@ -344,6 +364,7 @@ __global__ void __launch_bounds__(kSweepThreads, MCS_SWEEP_MINBLOCKS)
       accumulate(j, p);
     }
   };
+
 
 
 #pragma unroll

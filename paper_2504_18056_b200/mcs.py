@@ -285,15 +285,21 @@ class Context:
         """1 peer-direct migration, -1 packed exchange, 0 not decided yet."""
         return int(self._lib.mcs_peer_migration_state(self._ctx))
 
-    def get_particles(self):
+    def get_particles(self, kf: bool = True):
+        """Current poses, cumulative log-likelihoods and weights (and, with kf, every keyframe
+        pose of every particle: N x K x 48 bytes)."""
         n, K = self.sizes
         pose = np.zeros((n, 12), np.float32)
-        kfp = np.zeros((n, K, 12), np.float32)
+        kfp = np.zeros((n, K, 12), np.float32) if kf else None
         L = np.zeros(n, np.float64)
         w = np.zeros(n, np.float64)
-        self._check(self._lib.mcs_get_particles(self._ctx, pose.ctypes.data, kfp.ctypes.data,
+        self._check(self._lib.mcs_get_particles(self._ctx, pose.ctypes.data,
+                                                kfp.ctypes.data if kf else None,
                                                 L.ctypes.data, w.ctypes.data))
-        return {"pose12": pose, "kf_pose12": kfp, "L": L, "weight": w}
+        out = {"pose12": pose, "L": L, "weight": w}
+        if kf:
+            out["kf_pose12"] = kfp
+        return out
 
     def snapshot(self):
         self._check(self._lib.mcs_snapshot(self._ctx))

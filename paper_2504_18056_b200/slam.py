@@ -74,13 +74,14 @@ class MonteCarloSLAM:
         self.close()
 
     def step(self, scan_mean3, scan_cov6, odom_pose, odom_cov, path_length: float,
-             U: int | None = None, cloud=None) -> dict:
+             U: int | None = None, cloud=None, state: bool = False) -> dict:
         """One frame.  scan (S,3)/(S,6) fp32 in the sensor frame (the correction's points);
         cloud = (mean3, cov6) the whole frame downsampled at r, used for the overlap test and
         registered as the keyframe (default: the scan); odom_pose the odometry pose T^o_t
         (4x4); odom_cov the (6,6) covariance of the relative motion (rho, phi); path_length the
         cumulative odometry path length D_t (R14); U the resampling uniform (uint32; drawn from
-        the seeded generator when None)."""
+        the seeded generator when None); state: also return every particle's pose, L and weight
+        (and keyframe poses) in out["state"]."""
         cloud_m, cloud_c = (scan_mean3, scan_cov6) if cloud is None else cloud
         self.frame += 1
         odom_pose = np.asarray(odom_pose, np.float64)
@@ -110,9 +111,10 @@ class MonteCarloSLAM:
             self.K += 1
             out["inserted"] = True
         # (4) representative
-        st = self.ctx.get_particles()
+        st = self.ctx.get_particles(kf=state)
         rep = out["update"]["representative"] if out["update"] is not None else 0
         out["representative"] = int(rep)
         out["pose"] = _to44(st["pose12"][rep]) if 0 <= rep < self.N else None
-        out["state"] = st
+        if state:
+            out["state"] = st
         return out

@@ -78,7 +78,7 @@ def test_driver_equals_oracle_twin_frame_by_frame():
             ro = o.step(*tr.scans[k], tr.odom[k], tr.odom_cov, tr.D[k], tr.U[k],
                         cloud=tr.clouds[k])
             rg = g.step(*tr.scans[k], tr.odom[k], tr.odom_cov, tr.D[k], U=int(tr.U[k]),
-                        cloud=tr.clouds[k])
+                        cloud=tr.clouds[k], state=True)
             assert rg["inserted"] == ro["inserted"], k
             if ro["overlap"] is not None:
                 assert rg["overlap"] == ro["overlap"], k  # exact: pinned fp32 cells, both sides
