@@ -163,6 +163,10 @@ MCS_API mcs_status mcs_set_particles(mcs_ctx* ctx, int32_t n_local, const float*
 MCS_API mcs_status mcs_get_particles(mcs_ctx* ctx, float* pose12, float* kf_pose12, double* cum_loglik,
                              double* weight);
 MCS_API mcs_status mcs_get_sizes(const mcs_ctx* ctx, int32_t* n_local, int32_t* n_keyframes);
+/* One local particle's current pose (row-major 3x4 [R|t] into pose12[12], host or device), e.g.
+ * the representative's without reading back the whole set.  MCS_E_INVALID_ARG if
+ * index is outside [0, n_local). */
+MCS_API mcs_status mcs_get_pose(mcs_ctx* ctx, int32_t index, float* pose12);
 
 /* Outputs of one update; every pointer optional (NULL = not produced).  Per-particle rows are
  * indexed by LOCAL particle index.  loglik = l_i over ALL neighbour slots (Eq.2) minus the kappa

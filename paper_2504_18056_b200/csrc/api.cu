@@ -610,6 +610,18 @@ mcs_status mcs_get_particles(mcs_ctx* ctx, float* pose12, float* kf_pose12, doub
   return MCS_OK;
 }
 
+mcs_status mcs_get_pose(mcs_ctx* ctx, int32_t index, float* pose12) {
+  CHECK_CTX(ctx);
+  if (!pose12 || index < 0 || index >= ctx->N)
+    FAIL(ctx, MCS_E_INVALID_ARG, "mcs_get_pose: index %d outside [0, %d)", index, ctx->N);
+  // SoA column: 12 strided floats in one 2-D copy
+  CUDA_TRY(ctx, cudaMemcpy2DAsync(pose12, sizeof(float), ctx->d_pose + index,
+                                  sizeof(float) * ctx->capN, sizeof(float), 12, cudaMemcpyDefault,
+                                  ctx->stream));
+  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  return MCS_OK;
+}
+
 // validate a scan already in device memory (d_scan_raw layout: mean3 then cov6)
 static mcs_status validate_scan(mcs_ctx* ctx, int n_pts) {
   cudaStream_t st = ctx->stream;

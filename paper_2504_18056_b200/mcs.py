@@ -149,6 +149,7 @@ def load() -> C.CDLL:
         "mcs_inproc_transport_destroy": (None, [vp]),
         "mcs_plan_migration": (st, [i32, vp, vp, vp]),
         "mcs_peer_migration_state": (i32, [vp]),
+        "mcs_get_pose": (st, [vp, i32, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -284,6 +285,12 @@ class Context:
     def peer_migration_state(self) -> int:
         """1 peer-direct migration, -1 packed exchange, 0 not decided yet."""
         return int(self._lib.mcs_peer_migration_state(self._ctx))
+
+    def get_pose(self, index: int) -> np.ndarray:
+        """One local particle's current pose (12,) fp32 [R|t] row-major (mcs_get_pose)."""
+        p = np.zeros(12, np.float32)
+        self._check(self._lib.mcs_get_pose(self._ctx, int(index), p.ctypes.data))
+        return p
 
     def get_particles(self, kf: bool = True):
         """Current poses, cumulative log-likelihoods and weights (and, with kf, every keyframe

@@ -48,13 +48,14 @@ class MonteCarloSLAM:
     def __init__(self, n_particles: int, capacity_keyframes: int, capacity_scan_points: int, *,
                  init_pose, init_cov=None, seed: int = 0, overlap_threshold: float = 0.7,
                  elevator_median_range: float | None = None, vertical_sigma: float = 0.0,
-                 **cfg):
+                 outputs=("donor",), **cfg):
         self.ctx = Context(n_particles, capacity_keyframes, capacity_scan_points, **cfg)
         self.N = n_particles
         self.seed = int(seed)
         self.overlap_threshold = float(overlap_threshold)
         self.elevator_median_range = elevator_median_range
         self.vertical_sigma = float(vertical_sigma)
+        self.outputs = tuple(outputs)  # per-particle update outputs read back each frame
         self.frame = 0
         self.K = 0
         self.prev_odom = None
@@ -97,7 +98,8 @@ class MonteCarloSLAM:
         self.prev_odom = odom_pose
         # (2) correction (needs a keyframe)
         if self.K > 0:
-            out["update"] = self.ctx.update(scan_mean3, scan_cov6, float(path_length), U)
+            out["update"] = self.ctx.update(scan_mean3, scan_cov6, float(path_length), U,
+                                            outputs=self.outputs)
         # (3) keyframe list
         if self.K == 0:
             insert = True
@@ -111,10 +113,9 @@ class MonteCarloSLAM:
             self.K += 1
             out["inserted"] = True
         # (4) representative
-        st = self.ctx.get_particles(kf=state)
         rep = out["update"]["representative"] if out["update"] is not None else 0
         out["representative"] = int(rep)
-        out["pose"] = _to44(st["pose12"][rep]) if 0 <= rep < self.N else None
+        out["pose"] = _to44(self.ctx.get_pose(rep)) if 0 <= rep < self.N else None
         if state:
-            out["state"] = st
+            out["state"] = self.ctx.get_particles()
         return out

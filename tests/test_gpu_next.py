@@ -177,3 +177,14 @@ def test_torch_allocator_hook_gives_identical_results():
         np.testing.assert_array_equal(np.asarray(g0[k]), np.asarray(g1[k]), err_msg=k)
     for k in ("pose12", "kf_pose12", "L"):
         np.testing.assert_array_equal(st0[k], st1[k])
+
+
+def test_get_pose_equals_get_particles_row():
+    s = synth.c1()
+    with _ctx(s) as ctx:
+        ctx.update(s.scan_mean3, s.scan_cov6, s.D_now, s.U, outputs=())
+        allp = ctx.get_particles(kf=False)["pose12"]
+        for i in (0, 1, 517, s.N - 1):
+            np.testing.assert_array_equal(ctx.get_pose(i), allp[i])
+        with pytest.raises(mcs.MCSError):
+            ctx.get_pose(s.N)
