@@ -7,7 +7,7 @@
 //   cumulative log-lik L   : fp64 [Ncap]                    (R22)
 //   keyframe hash tables   : per keyframe, keys u64 [cap] + payload float4 [cap][3]
 //   work items (a1 -> a2)  : float4 [3*Ncap][4]  = (kR|kt rows, {kf, particle, flags, 0})
-//   sweep partials (a2->a3): fp64 [3*Ncap][32] = {l, n, H~21, b~6, pad}
+//   sweep partials (a2->a3): fp64 SoA [32][3*Ncap] = {l, n, H~21, b~6, pad} per item
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>

@@ -32,6 +32,9 @@ namespace mcs {
 #ifndef MCS_SWEEP_TMA
 #define MCS_SWEEP_TMA 0  // 1: scan stages double-buffered by TMA bulk copies + mbarriers
 #endif
+#ifndef MCS_SWEEP_GACC
+#define MCS_SWEEP_GACC 0  // 1: fp64 stage totals in the (SoA) partial records, not shared memory
+#endif
 #ifndef MCS_SWEEP_MINBLOCKS
 #define MCS_SWEEP_MINBLOCKS 4
 #endif
@@ -108,7 +111,7 @@ __global__ void __launch_bounds__(kSweepThreads, MCS_SWEEP_MINBLOCKS)
     sweep_kernel(const float4* __restrict__ items, const int32_t* __restrict__ order,
                  int n_items, const float4* __restrict__ scan, int S,
                  const KfMeta* __restrict__ kmeta, float inv_r, float nn_r2,
-                 double* __restrict__ part) {
+                 double* __restrict__ part, size_t pstride) {
   // dynamic shared memory: [(kChunk + 2) * 3] float4 scan stage, then [28][threads] fp64 totals
   extern __shared__ float4 smem_dyn[];
   float4* s_pt = smem_dyn;  // the current stage (MCS_SWEEP_TMA: one of two buffers)
@@ -121,6 +124,8 @@ __global__ void __launch_bounds__(kSweepThreads, MCS_SWEEP_MINBLOCKS)
       reinterpret_cast<double(*)[kSweepThreads]>(smem_dyn + kBufs * kStage);
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   const int item = t < n_items ? order[t] : -1;
+  // this item's partial record, SoA: word k at part[k * pstride + item] (coalesced per warp)
+  auto rec = [&](int k) -> double& { return part[(size_t)k * pstride + item]; };
   float4 r0 = make_float4(0, 0, 0, 0), r1 = r0, r2 = r0, inf = r0;
   if (item >= 0) {
     r0 = items[4 * (size_t)item + 0];
@@ -367,19 +372,31 @@ __global__ void __launch_bounds__(kSweepThreads, MCS_SWEEP_MINBLOCKS)
 
 
 
+  // fp64 totals across stages: [0] l, [1..21] H~, [22..27] b~ (shared memory, or with
+  // MCS_SWEEP_GACC the record words 0, 2..22, 23..28 themselves)
+  auto tot = [&](int k) -> double& {
+#if MCS_SWEEP_GACC
+    return rec(k == 0 ? 0 : k + 1);
+#else
+    return s_acc[k][threadIdx.x];
+#endif
+  };
+#if MCS_SWEEP_GACC
+  if (active)
+#endif
 #pragma unroll
-  for (int k = 0; k < 28; ++k) s_acc[k][threadIdx.x] = 0.0;
+    for (int k = 0; k < 28; ++k) tot(k) = 0.0;
   auto flush = [&]() {
-    s_acc[0][threadIdx.x] += (double)l;
+    tot(0) += (double)l;
     l = 0.f;
 #pragma unroll
     for (int k = 0; k < 21; ++k) {
-      s_acc[1 + k][threadIdx.x] += (double)h[k];
+      tot(1 + k) += (double)h[k];
       h[k] = 0.f;
     }
 #pragma unroll
     for (int k = 0; k < 6; ++k) {
-      s_acc[22 + k][threadIdx.x] += (double)bv[k];
+      tot(22 + k) += (double)bv[k];
       bv[k] = 0.f;
     }
   };
@@ -491,13 +508,14 @@ __global__ void __launch_bounds__(kSweepThreads, MCS_SWEEP_MINBLOCKS)
   }
 #endif
   if (!active) return;
-  double* o = part + (size_t)item * kSlotWords;
-  o[0] = s_acc[0][threadIdx.x];
-  o[1] = (double)n;
+  rec(1) = (double)n;
+#if !MCS_SWEEP_GACC
+  rec(0) = tot(0);
 #pragma unroll
-  for (int k = 0; k < 21; ++k) o[2 + k] = s_acc[1 + k][threadIdx.x];
+  for (int k = 0; k < 21; ++k) rec(2 + k) = tot(1 + k);
 #pragma unroll
-  for (int k = 0; k < 6; ++k) o[23 + k] = s_acc[22 + k][threadIdx.x];
+  for (int k = 0; k < 6; ++k) rec(23 + k) = tot(22 + k);
+#endif
 }
 
 // Scan preparation (once per update): Sigma_j = lambda3 I + u u^T + v v^T with u, v the two
@@ -564,8 +582,11 @@ void launch_sweep(mcs_ctx* c, int S) {
   const int n_items = c->cfg.neighbor_count * c->N;
   const int grid = (n_items + kSweepThreads - 1) / kSweepThreads;
   const float inv_r = 1.0f / c->cfg.voxel_resolution;
+  static_assert(!(MCS_SWEEP_TMA && MCS_SWEEP_GACC), "the TMA mbarriers follow s_acc");
   constexpr size_t smem = sizeof(float4) * (kChunk + 2) * 3 * (MCS_SWEEP_TMA ? 2 : 1) +
-                          sizeof(double) * 28 * kSweepThreads + (MCS_SWEEP_TMA ? 32 : 0);
+                          (MCS_SWEEP_GACC ? 0 : sizeof(double) * 28 * kSweepThreads) +
+                          (MCS_SWEEP_TMA ? 32 : 0);
+  const size_t pstride = (size_t)c->cfg.neighbor_count * c->capN;
   static bool attr_set[128] = {};  // opt in beyond 48 KB once per device (both instantiations)
   if (c->dev < 0 || c->dev >= 128 || !attr_set[c->dev]) {
     cudaFuncSetAttribute(sweep_kernel<MCS_CORR_CELL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -577,10 +598,12 @@ void launch_sweep(mcs_ctx* c, int S) {
   if (c->cfg.corr_mode == MCS_CORR_NN27) {
     const float nn_r2 = c->cfg.nn_radius * c->cfg.nn_radius;
     sweep_kernel<MCS_CORR_NN27><<<grid, kSweepThreads, smem, c->stream>>>(
-        c->d_items, c->d_order, n_items, c->d_scan, S, c->d_kf_meta, inv_r, nn_r2, c->d_part);
+        c->d_items, c->d_order, n_items, c->d_scan, S, c->d_kf_meta, inv_r, nn_r2, c->d_part,
+        pstride);
   } else {
     sweep_kernel<MCS_CORR_CELL><<<grid, kSweepThreads, smem, c->stream>>>(
-        c->d_items, c->d_order, n_items, c->d_scan, S, c->d_kf_meta, inv_r, 0.f, c->d_part);
+        c->d_items, c->d_order, n_items, c->d_scan, S, c->d_kf_meta, inv_r, 0.f, c->d_part,
+        pstride);
   }
 }
 

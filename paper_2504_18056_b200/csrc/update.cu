@@ -23,7 +23,8 @@ __device__ __forceinline__ int up_idx(int r, int c) {  // r <= c
 
 struct CombineArgs {
   const float4* items;
-  const double* part;
+  const double* part;    // sweep partials, SoA [kSlotWords][pstride]
+  size_t pstride;
   const uint8_t* meta;
   float* pose;
   double* L;
@@ -76,9 +77,12 @@ __global__ void __launch_bounds__(128) combine_kernel(CombineArgs a) {
                    r2 = a.items[4 * item + 2], inf = a.items[4 * item + 3];
       const int kf = __float_as_int(inf.x);
       const double R[9] = {r0.x, r0.y, r0.z, r1.x, r1.y, r1.z, r2.x, r2.y, r2.z};
-      const double* o = a.part + item * kSlotWords;
-      const double ls = o[0];
-      const int ns = (int)o[1];
+      // sweep partials, SoA: word k of item at part[k * pstride + item] (coalesced across i)
+      const double* pi = a.part + item;
+      const size_t ps = a.pstride;
+      auto o = [&](int k) { return pi[(size_t)k * ps]; };
+      const double ls = o(0);
+      const int ns = (int)o(1);
       const bool in_G = a.gn_all ? true : (kf <= latest - a.gap);
       lsum += ls;
       unmatched += a.S - ns;
@@ -99,7 +103,7 @@ __global__ void __launch_bounds__(128) combine_kernel(CombineArgs a) {
 #pragma unroll
             for (int y = 0; y < 3; ++y) {
               const int r = 3 * p + x, c = 3 * q + y;
-              Hb[3 * x + y] = o[2 + (r <= c ? up_idx(r, c) : up_idx(c, r))];
+              Hb[3 * x + y] = o(2 + (r <= c ? up_idx(r, c) : up_idx(c, r)));
             }
           double T[9];
 #pragma unroll
@@ -125,8 +129,8 @@ __global__ void __launch_bounds__(128) combine_kernel(CombineArgs a) {
       for (int p = 0; p < 2; ++p)
 #pragma unroll
         for (int x = 0; x < 3; ++x) {
-          const double v = R[0 * 3 + x] * o[23 + 3 * p + 0] + R[1 * 3 + x] * o[23 + 3 * p + 1] +
-                           R[2 * 3 + x] * o[23 + 3 * p + 2];
+          const double v = R[0 * 3 + x] * o(23 + 3 * p + 0) + R[1 * 3 + x] * o(23 + 3 * p + 1) +
+                           R[2 * 3 + x] * o(23 + 3 * p + 2);
           if (in_G) b[3 * p + x] += v;
           if (a.eval_mode && a.slot_b6) a.slot_b6[so * 6 + 3 * p + x] = (float)v;
         }
@@ -265,6 +269,7 @@ void launch_combine(mcs_ctx* c, int S, int mode, double* slot_l, float* slot_H21
   CombineArgs a;
   a.items = c->d_items;
   a.part = c->d_part;
+  a.pstride = (size_t)c->cfg.neighbor_count * c->capN;
   a.meta = c->d_meta;
   a.pose = c->d_pose;
   a.L = c->d_L;
