@@ -1,0 +1,106 @@
+"""Edge cases of the CUDA path against the oracle: scan sizes at and around the 256-point
+shared-memory stage and the 4-point probe batch (1, 2, 3, 5, 255, 256, 257, 513), every
+neighbour count 1..MCS_MAX_NEIGHBORS, GN over all slots, a voxel size of 2 m, and one-point
+keyframes."""
+import dataclasses
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_2504_18056_b200 as mcs
+import synth
+from test_gpu_parity import (G_RTOL, L_RTOL, ROT_TOL, T_TOL, check_slots, make_ctx, orc_cfg,
+                             pose_err, rel_err)
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def c2s():
+    return synth.subset(synth.c2(N=2000), 1500)
+
+
+# The north-star tolerances are for whole scans.  With a handful of points the fp32 rounding of
+# q (~1e-6 m at 10-20 m) against centimetre residuals is ~1e-4 of e per point and nothing
+# averages it out: l is then compared at 2e-3 relative and the (rank-deficient, damping-
+# dominated) pose step is not compared.
+FEW = 64
+
+
+def _eval_parity(s, **kw):
+    with make_ctx(s, **kw) as ctx:
+        g = ctx.eval(s.scan_mean3, s.scan_cov6)
+    o = oracle.particles(orc_cfg(s, **kw), oracle.Keyframes(s.keyframes, s.D, s.r), s.D_now,
+                         s.pose12.copy(), s.kf_pose12.copy(), s.scan_mean3, s.scan_cov6,
+                         apply_update=False, slots=True)
+    if s.S >= FEW:
+        check_slots(g, o, s.S)
+    else:
+        np.testing.assert_array_equal(g["slot_kf"], o["slot_kf"])
+        np.testing.assert_array_equal(g["slot_n"], o["slot_n"])
+        assert np.all(np.abs(g["slot_loglik"] - o["slot_l"]) <= 2e-3 * np.abs(o["slot_l"]) + 1e-6)
+    return g, o
+
+
+def _update_parity(s, **kw):
+    nd = dict(posterior_floor=0.0, loglik_rel_floor=-np.inf)
+    with make_ctx(s, **kw, **nd) as ctx:
+        g = ctx.update(s.scan_mean3, s.scan_cov6, s.D_now, s.U)
+        st = ctx.get_particles()
+    pose, kp, L = s.pose12.copy(), s.kf_pose12.copy(), np.zeros(s.N)
+    o = oracle.update(orc_cfg(s, **kw, **nd), oracle.Keyframes(s.keyframes, s.D, s.r),
+                      s.D_now, pose, kp, L, s.scan_mean3, s.scan_cov6, s.U)
+    rt = L_RTOL if s.S >= FEW else 2e-3
+    assert np.all(np.abs(g["loglik"] - o["loglik"]) <= rt * np.abs(o["loglik"]) + 1e-6)
+    np.testing.assert_array_equal(g["flags"] & 1, o["flags"] & 1)
+    if s.S < FEW:
+        return g, o
+    gn = np.linalg.norm(o["grad6"], axis=1) > 0
+    assert np.all(rel_err(g["grad6"][gn], o["grad6"][gn], axis=1) <= G_RTOL)
+    np.testing.assert_array_equal(g["flags"], o["flags"])
+    ang, dt = pose_err(st["pose12"], pose)
+    assert ang.max() <= ROT_TOL and dt.max() <= T_TOL, (ang.max(), dt.max())
+    ak, dk = pose_err(st["kf_pose12"].reshape(-1, 12), kp.reshape(-1, 12))
+    assert ak.max() <= ROT_TOL and dk.max() <= T_TOL
+    return g, o
+
+
+@pytest.mark.parametrize("S", [1, 2, 3, 5, 255, 256, 257, 513])
+def test_scan_sizes_around_stage_and_batch(c2s, S):
+    s = dataclasses.replace(c2s, scan_mean3=np.ascontiguousarray(c2s.scan_mean3[:S]),
+                            scan_cov6=np.ascontiguousarray(c2s.scan_cov6[:S]))
+    _eval_parity(s)
+    _update_parity(s)
+
+
+@pytest.mark.parametrize("nb", [1, 2, 3, 4])  # 1..MCS_MAX_NEIGHBORS
+def test_every_neighbour_count(c2s, nb):
+    _eval_parity(c2s, neighbor_count=nb)
+    _update_parity(c2s, neighbor_count=nb)
+
+
+def test_gn_over_all_slots(c2s):
+    g, o = _update_parity(c2s, gn_slots=1)
+    assert (o["flags"] & 2).mean() > 0.5
+
+
+def test_voxel_size_two_metres():
+    s = synth.c1()
+    m3, c6 = s.keyframes[0]
+    s2 = dataclasses.replace(s, r=2.0, pose12=np.ascontiguousarray(s.pose12[:400]),
+                             kf_pose12=np.ascontiguousarray(s.kf_pose12[:400]))
+    _eval_parity(s2)
+    _update_parity(s2)
+
+
+def test_one_point_keyframes():
+    """Keyframes of a single Gaussian: a one-cell table; most points miss, the rest match it."""
+    s = synth.c1()
+    m3, c6 = s.keyframes[0]
+    kfs = [(m3[i:i + 1].copy(), c6[i:i + 1].copy()) for i in (0, 100, 900)]
+    kp = np.ascontiguousarray(np.repeat(s.kf_pose12[:300], 3, axis=1))
+    s2 = dataclasses.replace(s, keyframes=kfs, D=np.array([0.0, 1.0, 2.0]),
+                             pose12=np.ascontiguousarray(s.pose12[:300]), kf_pose12=kp)
+    g, o = _eval_parity(s2)
+    assert g["slot_n"].max() <= s2.S
