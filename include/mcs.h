@@ -132,10 +132,17 @@ typedef struct mcs_config {
                                     processes) when every rank's state is reachable, else (and
                                     with 0) packed and exchanged by NCCL send/recv or the
                                     transport's alltoallv                                     */
+  int32_t  point_splits;         /* scan-point ranges per work item in the sweep, 1..8; 0 (default)
+                                    = auto: more splits when the particles alone cannot fill the
+                                    GPU (results differ only in fp rounding; bitwise equality of
+                                    runs holds for a fixed value)                               */
   int32_t  graph_replay;         /* 1 (default): a single-rank update body is captured once into
                                     a CUDA graph and replayed while the scan size, particle and
                                     keyframe counts stay the same; 0: launched kernel by kernel */
 } mcs_config;
+
+/* sizeof(mcs_config) of this build: bindings check their mirror of the struct against it. */
+MCS_API size_t mcs_config_size(void);
 
 /* Fills *cfg with the defaults above (capacities 0: caller sets them). */
 MCS_API void mcs_config_default(mcs_config* cfg);

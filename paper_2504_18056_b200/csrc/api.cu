@@ -234,6 +234,8 @@ static cudaError_t to_device(void* dst, const void* src, size_t bytes, cudaStrea
 // ------------------------------------------------------------------ ABI
 extern "C" {
 
+size_t mcs_config_size(void) { return sizeof(mcs_config); }
+
 void mcs_config_default(mcs_config* cfg) {
   if (!cfg) return;
   memset(cfg, 0, sizeof(*cfg));
@@ -255,6 +257,7 @@ void mcs_config_default(mcs_config* cfg) {
   cfg->clone_split = 0;
   cfg->peer_migration = 1;
   cfg->graph_replay = 1;
+  cfg->point_splits = 0;
   cfg->rank = 0;
   cfg->world_size = 1;
   cfg->nccl_unique_id = nullptr;
@@ -305,9 +308,10 @@ mcs_status mcs_create(const mcs_config* cfg, mcs_ctx** out) {
        !(cfg->nn_radius > 0.0f && cfg->nn_radius <= cfg->voxel_resolution)) ||
       (cfg->clone_split != 0 && cfg->clone_split != 1) ||
       (cfg->peer_migration != 0 && cfg->peer_migration != 1) ||
-      (cfg->graph_replay != 0 && cfg->graph_replay != 1)) {
+      (cfg->graph_replay != 0 && cfg->graph_replay != 1) ||
+      cfg->point_splits < 0 || cfg->point_splits > 8) {
     g_create_error = "corr_mode must be CELL or NN27 (with 0 < nn_radius <= voxel_resolution), "
-                     "clone_split, peer_migration and graph_replay 0 or 1";
+                     "clone_split, peer_migration and graph_replay 0 or 1; point_splits 0..8";
     return MCS_E_INVALID_ARG;
   }
   if (cfg->world_size < 1 || cfg->rank < 0 || cfg->rank >= cfg->world_size) {
@@ -371,7 +375,8 @@ mcs_status mcs_create(const mcs_config* cfg, mcs_ctx** out) {
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     }
   }
-  if (e == cudaSuccess) e = dalloc(c, &c->d_part, (size_t)kSlotWords * nb * N);
+  c->part_splits = cfg->point_splits > 0 ? cfg->point_splits : 1;
+  if (e == cudaSuccess) e = dalloc(c, &c->d_part, (size_t)kSlotWords * nb * N * c->part_splits);
   if (e == cudaSuccess) e = dalloc(c, &c->d_meta, N);
   if (e == cudaSuccess) e = dalloc(c, &c->d_to, N);
   if (e == cudaSuccess) e = dalloc(c, &c->d_l, N);
@@ -572,6 +577,17 @@ mcs_status mcs_set_particles(mcs_ctx* ctx, int32_t n, const float* pose12,
   mem_free_async(ctx, bad, st);
   CUDA_TRY(ctx, cudaStreamSynchronize(st));
   ctx->N = n;
+  {  // sweep partials for the point splits this particle count will use (outside any capture)
+    const int P = sweep_splits_for(ctx, n);
+    if (P > ctx->part_splits) {
+      double* np = nullptr;
+      CUDA_TRY(ctx, mem_alloc(ctx, (void**)&np,
+                              sizeof(double) * kSlotWords * ctx->nbcap * ctx->capN * P));
+      mem_free(ctx, ctx->d_part);
+      ctx->d_part = np;
+      ctx->part_splits = P;
+    }
+  }
   // global index base of this shard (collective over ranks)
   ctx->n_per_rank.assign(ctx->world, 0);
   const long long mine = n;

@@ -177,6 +177,10 @@ struct mcs_ctx {
   void* d_cub_temp = nullptr;
   size_t cub_temp_bytes = 0;
   int32_t capN = 0, capK = 0, capS = 0, nbcap = 0;
+  // sweep point splits (cfg.point_splits): splits the partial buffer holds, splits in use by
+  // the current update (set by launch_sweep, read by combine)
+  int part_splits = 1;
+  int cur_splits = 1;
 
   // multi-rank (world > 1): particle shards with global index = gbase + local index
   int world = 1, rank = 0;
@@ -222,6 +226,8 @@ enum { kSelectUpdate = 0, kSelectEval = 1, kSelectWeight = 2 };
 void launch_select(mcs_ctx* c, int mode);
 // a2
 void launch_sweep(mcs_ctx* c, int S);
+// point splits the sweep would use for n local particles (cfg.point_splits, or auto)
+int sweep_splits_for(const mcs_ctx* c, int n);
 
 // device memory through the allocator hook (include/mcs.h): persistent buffers (context
 // lifetime) and stream-ordered temporaries

@@ -124,6 +124,12 @@ __global__ void __launch_bounds__(kSweepThreads, MCS_SWEEP_MINBLOCKS)
       reinterpret_cast<double(*)[kSweepThreads]>(smem_dyn + kBufs * kStage);
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   const int item = t < n_items ? order[t] : -1;
+  // point splits (gridDim.y): this CTA's run of whole stages, and its own partial records
+  const int stages_all = (S + kChunk - 1) / kChunk;
+  const int st_per = (stages_all + gridDim.y - 1) / gridDim.y;
+  const int st_lo = min((int)blockIdx.y * st_per, stages_all);
+  const int st_hi = min(st_lo + st_per, stages_all);
+  part += (size_t)blockIdx.y * kSlotWords * pstride;
   // this item's partial record, SoA: word k at part[k * pstride + item] (coalesced per warp)
   auto rec = [&](int k) -> double& { return part[(size_t)k * pstride + item]; };
   float4 r0 = make_float4(0, 0, 0, 0), r1 = r0, r2 = r0, inf = r0;
@@ -454,12 +460,12 @@ __global__ void __launch_bounds__(kSweepThreads, MCS_SWEEP_MINBLOCKS)
   // warps run up to a stage ahead of slow ones.
   uint64_t* full = reinterpret_cast<uint64_t*>(&s_acc[28][0]);  // [2] mbarriers
   int* done = reinterpret_cast<int*>(full + 2);                   // [2] warps done with stage
-  const int n_stages = (S + kChunk - 1) / kChunk;
+  const int n_stages = st_hi - st_lo;  // stages k of this CTA: st_lo + k
   constexpr int kWarps = kSweepThreads / 32;
-  auto refill = [&](int k) {  // one thread: stage k into buffer k & 1
-    const int cnt = min(kChunk, S - k * kChunk);
-    bulk_stage(smem_dyn + (k & 1) * kStage, scan + 3 * (size_t)k * kChunk, 48u * cnt,
-               &full[k & 1]);
+  auto refill = [&](int k) {  // one thread: stage st_lo + k into buffer k & 1
+    const int base = (st_lo + k) * kChunk;
+    const int cnt = min(kChunk, S - base);
+    bulk_stage(smem_dyn + (k & 1) * kStage, scan + 3 * (size_t)base, 48u * cnt, &full[k & 1]);
   };
   if (threadIdx.x < 12)
     smem_dyn[(threadIdx.x / 6) * kStage + 3 * kChunk + threadIdx.x % 6] =
@@ -479,7 +485,7 @@ __global__ void __launch_bounds__(kSweepThreads, MCS_SWEEP_MINBLOCKS)
     s_pt = smem_dyn + (k & 1) * kStage;
     mbar_wait(&full[k & 1], (k >> 1) & 1);
     if (active) {
-      stage(min(kChunk, S - k * kChunk));
+      stage(min(kChunk, S - (st_lo + k) * kChunk));
       flush();
     }
     __syncwarp();
@@ -497,7 +503,7 @@ __global__ void __launch_bounds__(kSweepThreads, MCS_SWEEP_MINBLOCKS)
   }
 #else
   if (threadIdx.x < 6) s_pt[3 * kChunk + threadIdx.x] = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (int base = 0; base < S; base += kChunk) {
+  for (int base = st_lo * kChunk; base < st_hi * kChunk; base += kChunk) {
     const int cnt = min(kChunk, S - base);
     __syncthreads();
     for (int k = threadIdx.x; k < cnt * 3; k += kSweepThreads) s_pt[k] = scan[3 * base + k];
@@ -578,9 +584,25 @@ void launch_prepare_scan(const float* mean3, const float* cov6, int S, float4* o
   prepare_scan_kernel<<<(S + 127) / 128, 128, 0, st>>>(mean3, cov6, S, out);
 }
 
+#ifndef MCS_SPLIT_TARGET_CTAS
+#define MCS_SPLIT_TARGET_CTAS 1184  // auto point splits aim for two waves of 148 x 4 CTAs
+#endif
+
+int sweep_splits_for(const mcs_ctx* c, int n) {
+  if (c->cfg.point_splits > 0) return c->cfg.point_splits;
+  const long long ctas = ((long long)c->cfg.neighbor_count * n + kSweepThreads - 1) / kSweepThreads;
+  const long long p = (MCS_SPLIT_TARGET_CTAS + ctas - 1) / (ctas > 0 ? ctas : 1);
+  return (int)(p < 1 ? 1 : (p > 8 ? 8 : p));
+}
+
 void launch_sweep(mcs_ctx* c, int S) {
   const int n_items = c->cfg.neighbor_count * c->N;
-  const int grid = (n_items + kSweepThreads - 1) / kSweepThreads;
+  const int stages = (S + kChunk - 1) / kChunk;
+  int P = sweep_splits_for(c, c->N);
+  P = P > c->part_splits ? c->part_splits : P;
+  P = P > stages ? stages : P;
+  c->cur_splits = P;
+  const dim3 grid((n_items + kSweepThreads - 1) / kSweepThreads, P);
   const float inv_r = 1.0f / c->cfg.voxel_resolution;
   static_assert(!(MCS_SWEEP_TMA && MCS_SWEEP_GACC), "the TMA mbarriers follow s_acc");
   constexpr size_t smem = sizeof(float4) * (kChunk + 2) * 3 * (MCS_SWEEP_TMA ? 2 : 1) +

@@ -25,6 +25,7 @@ struct CombineArgs {
   const float4* items;
   const double* part;    // sweep partials, SoA [kSlotWords][pstride]
   size_t pstride;
+  int splits;            // point splits of the sweep (records [splits][kSlotWords][pstride])
   const uint8_t* meta;
   float* pose;
   double* L;
@@ -78,9 +79,14 @@ __global__ void __launch_bounds__(128) combine_kernel(CombineArgs a) {
       const int kf = __float_as_int(inf.x);
       const double R[9] = {r0.x, r0.y, r0.z, r1.x, r1.y, r1.z, r2.x, r2.y, r2.z};
       // sweep partials, SoA: word k of item at part[k * pstride + item] (coalesced across i)
+      // point splits: the same word of every split record, summed in split order (fp64)
       const double* pi = a.part + item;
       const size_t ps = a.pstride;
-      auto o = [&](int k) { return pi[(size_t)k * ps]; };
+      auto o = [&](int k) {
+        double v = pi[(size_t)k * ps];
+        for (int q = 1; q < a.splits; ++q) v += pi[((size_t)q * kSlotWords + k) * ps];
+        return v;
+      };
       const double ls = o(0);
       const int ns = (int)o(1);
       const bool in_G = a.gn_all ? true : (kf <= latest - a.gap);
@@ -270,6 +276,7 @@ void launch_combine(mcs_ctx* c, int S, int mode, double* slot_l, float* slot_H21
   a.items = c->d_items;
   a.part = c->d_part;
   a.pstride = (size_t)c->cfg.neighbor_count * c->capN;
+  a.splits = c->cur_splits;
   a.meta = c->d_meta;
   a.pose = c->d_pose;
   a.L = c->d_L;

@@ -60,6 +60,7 @@ class Config(C.Structure):
         ("clone_split", C.c_int32),
         ("allocator", C.c_void_p),
         ("peer_migration", C.c_int32),
+        ("point_splits", C.c_int32),
         ("graph_replay", C.c_int32),
     ]
 
@@ -150,6 +151,7 @@ def load() -> C.CDLL:
         "mcs_plan_migration": (st, [i32, vp, vp, vp]),
         "mcs_peer_migration_state": (i32, [vp]),
         "mcs_get_pose": (st, [vp, i32, vp]),
+        "mcs_config_size": (C.c_size_t, []),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -166,6 +168,10 @@ def header_symbols() -> list[str]:
 
 
 def default_config(**kw) -> Config:
+    n = load().mcs_config_size()
+    if C.sizeof(Config) != n:  # the ctypes mirror must match include/mcs.h exactly
+        raise RuntimeError(f"mcs_config is {n} bytes in libmcs but {C.sizeof(Config)} in the "
+                           "binding: rebuild libmcs or update mcs.Config")
     cfg = Config()
     load().mcs_config_default(C.byref(cfg))
     for k, v in kw.items():

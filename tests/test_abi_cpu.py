@@ -2,11 +2,14 @@
 declares, and behaves on host-only logic (no compute calls without a GPU)."""
 import ctypes as C
 import math
+import os
 
 import numpy as np
 import pytest
 
 import paper_2504_18056_b200 as mcs
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def test_library_exports_every_header_symbol():
@@ -74,3 +77,22 @@ def test_unpack_h21_roundtrip():
     iu = np.triu_indices(6)
     h21 = A[:, iu[0], iu[1]]
     np.testing.assert_array_equal(mcs.unpack_h21(h21), A)
+
+
+def test_config_mirror_matches_the_header():
+    """The ctypes mirror of mcs_config has the header's fields in the header's order and the
+    library's size (a mismatch once let mcs_config_default write past the Python struct)."""
+    import ctypes as C
+    import re
+    src = open(os.path.join(ROOT, "include", "mcs.h")).read()
+    body = src[src.index("typedef struct mcs_config {"):src.index("} mcs_config;")]
+    body = re.sub(r"/\*.*?\*/", "", body, flags=re.S)
+    names = []
+    for decl in body.split("{", 1)[1].split(";"):
+        decl = decl.strip()
+        if not decl:
+            continue
+        for part in decl.split(","):
+            names.append(re.findall(r"[A-Za-z_]\w*", part)[-1])
+    assert [f for f, _ in mcs.Config._fields_] == names
+    assert C.sizeof(mcs.Config) == mcs.load().mcs_config_size()
