@@ -96,3 +96,34 @@ def test_config_mirror_matches_the_header():
             names.append(re.findall(r"[A-Za-z_]\w*", part)[-1])
     assert [f for f, _ in mcs.Config._fields_] == names
     assert C.sizeof(mcs.Config) == mcs.load().mcs_config_size()
+
+
+def _header_fields(closing):
+    """Member names of the struct typedef that ends with `closing` in include/mcs.h."""
+    import re
+    src = open(os.path.join(ROOT, "include", "mcs.h")).read()
+    end = src.index(closing)
+    body = src[src.rindex("typedef struct", 0, end):end]
+    body = re.sub(r"/\*.*?\*/", "", body, flags=re.S).split("{", 1)[1]
+    names = []
+    for decl in body.split(";"):
+        decl = decl.strip()
+        if not decl:
+            continue
+        if "(" in decl:  # function pointer: int (*name)(...)
+            names.append(re.search(r"\(\s*\*\s*(\w+)\s*\)", decl).group(1))
+            continue
+        for part in decl.split(","):
+            names.append(re.findall(r"[A-Za-z_]\w*", part)[-1])
+    return names
+
+
+def test_other_struct_mirrors_match_the_header():
+    import ctypes as C
+    assert [f for f, _ in mcs.mcs.UpdateOut._fields_] == _header_fields("} mcs_update_out;")
+    assert [f for f, _ in mcs.mcs.Transport._fields_] == _header_fields("} mcs_transport;")
+    assert [f for f, _ in mcs.mcs.Allocator._fields_] == _header_fields("} mcs_allocator;")
+    assert [f for f, _ in mcs.Config._fields_] == _header_fields("} mcs_config;")
+    # all pointer-sized members
+    assert C.sizeof(mcs.mcs.UpdateOut) == 8 * len(mcs.mcs.UpdateOut._fields_)
+    assert C.sizeof(mcs.mcs.Transport) == 32 and C.sizeof(mcs.mcs.Allocator) == 24
