@@ -164,6 +164,8 @@ def cpu_baseline(s, budget_s: float = 12.0):
     oracle.set_num_threads(cores)
     return {"value": n * s.S / t, "unit": UNIT, "cores": cores, "kind": "oracle",
             "cpu_model": cpu_model(), "single_thread_value": n1 * s.S / t1,
+            "extrapolated_full_update_s": t * s.N / n,
+            "triple_evals_per_s": n * s.S * 3 / t,
             "sample": f"{n} of {s.N} particles (strided), full 4096-pt scan, 20 keyframes, "
                       f"whole update a1-a7 on the sample; {t:.2f} s on {cores} threads "
                       f"(+ {n1} particles on 1 thread, {t1:.2f} s)"}, t
