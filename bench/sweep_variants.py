@@ -10,7 +10,6 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 VARIANTS = {
     "base": [],
-    "gacc": ["MCS_SWEEP_GACC=1"],
 }
 OUT = os.path.join(ROOT, "bench", "_variants")
 
