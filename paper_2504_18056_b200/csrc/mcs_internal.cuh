@@ -5,7 +5,8 @@
 //   keyframe poses T_k^i   : fp32 [Ncap][Kcap][12]          (a particle's map is contiguous:
 //                                                            clone = one memcpy)
 //   cumulative log-lik L   : fp64 [Ncap]                    (R22)
-//   keyframe hash tables   : per keyframe, keys u64 [cap] + payload float4 [cap][3]
+//   keyframe hash tables   : per keyframe, 64-B slots float4 [cap + 1][4] (key in the first
+//                            word, then mu', Sigma'; slot cap = always-empty sentinel)
 //   work items (a1 -> a2)  : float4 [3*Ncap][4]  = (kR|kt rows, {kf, particle, flags, 0})
 //   sweep partials (a2->a3): fp64 SoA [32][3*Ncap] = {l, n, H~21, b~6, pad} per item
 #pragma once

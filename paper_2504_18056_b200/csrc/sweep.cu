@@ -12,10 +12,11 @@
 //   H~ += K^T Omega K,  b~ += K^T Omega e,   K = [-I, [m]x],  m = R mu_j = q - t
 // K is the Jacobian in the rotated frame: J = de/d(delta) = [-R, R[mu]x] = K blockdiag(R, R)
 // (R2), so the per-slot rotation back to the body frame happens once in a3, not per point.
-// The table probe of point j+1 (key + payload, one 48-byte slot) is issued before the math of
-// point j, so the L2 gather latency hides behind ~140 FP32 instructions.
-// R Sigma_j R^T uses the per-scan spectral form of Sigma_j (prepare_scan_kernel below).
-// Accumulators are fp32 registers in a fixed point order: bitwise reproducible.
+// Table probes (key + 40 B of payload from one 64-byte slot) are issued in batches of two
+// points, two points ahead of the math, so the L2 gather latency hides behind it; the (y, z)
+// halves of the 3-vector / 3x3 math run as packed FFMA2.  R Sigma_j R^T uses the per-scan
+// spectral form of Sigma_j (prepare_scan_kernel below).  Accumulation is two-level (fp32 within
+// a 256-point stage, fp64 across stages) in a fixed order: bitwise reproducible.  DESIGN.md §5.
 #include "mcs_internal.cuh"
 
 namespace mcs {
