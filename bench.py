@@ -217,16 +217,22 @@ def run_gpu(args):
 
     import paper_2504_18056_b200 as mcs
     rank, world, local = dist_env()
+    local = local % max(torch.cuda.device_count(), 1)  # --dist-backend gloo may share a GPU
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist = None
     extra = {}
-    if world > 1:  # one process per GPU; the library owns its own NCCL communicator
+    if world > 1 and args.dist_backend == "nccl":
+        # one process per GPU; the library owns its own NCCL communicator
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
         obj = [mcs.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         extra = dict(world_size=world, rank=rank, nccl_unique_id=obj[0])
+    elif world > 1:  # check of the multi-rank script path: host collectives over gloo
+        import torch.distributed as dist
+        dist.init_process_group("gloo")
+        extra = dict(world_size=world, rank=rank, transport=mcs.TorchDistTransport())
     s = make_scene(args.particles)  # every rank: the same keyframes and scan, its own shard
     N, S, K = s.N, s.S, s.K
     stream = torch.cuda.Stream(device=dev)
@@ -315,7 +321,8 @@ def run_gpu(args):
         ctx.set_profiling(False)
     total_ms = float(np.sum(step_ms))
     if dist:  # the job's time is the slowest rank's
-        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        t = torch.tensor([total_ms], dtype=torch.float64,
+                         device=dev if args.dist_backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
     ms = total_ms / args.steps
@@ -339,7 +346,8 @@ def run_gpu(args):
             e2e_t.append(t2 - t1)
     e2e_mean = float(np.mean(e2e_t))
     if dist:
-        t = torch.tensor([e2e_mean], dtype=torch.float64, device=dev)
+        t = torch.tensor([e2e_mean], dtype=torch.float64,
+                         device=dev if args.dist_backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_mean = float(t.item())
     e2e_value = world * N * S / e2e_mean
@@ -359,7 +367,7 @@ def run_gpu(args):
         "config": {"workload": "C2: 100k particles x 4096-pt LiDAR-like scan vs 20 keyframes "
                                "(loop corridor, r = 0.5 m, 3 neighbours, every particle loops)",
                    "particles": N * world, "particles_per_gpu": N, "scan_points": S,
-                   "keyframes": K, "parallelism": f"particle shards x{world} (NCCL)",
+                   "keyframes": K, "parallelism": f"particle shards x{world} ({args.dist_backend})",
                    "keyframe_cells": int(sum(len(k[0]) for k in s.keyframes)),
                    "l2": "particle state restored from a device snapshot and 256 MiB L2 flush "
                          "before every timed step (untimed)",
@@ -408,6 +416,9 @@ def main():
     ap.add_argument("--ref-step-s", type=float, default=4.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="eager updates in the timed loop")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="N > 1: library NCCL communicator (default) or host collectives over "
+                         "gloo (a script-path check; ranks may share one GPU, times meaningless)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
