@@ -104,3 +104,26 @@ def test_one_point_keyframes():
                              pose12=np.ascontiguousarray(s.pose12[:300]), kf_pose12=kp)
     g, o = _eval_parity(s2)
     assert g["slot_n"].max() <= s2.S
+
+
+def test_far_from_origin_correspondences_stay_exact():
+    """R27 pins the fp32 key path (relative pose entries, transform, floor), so even 400 km
+    from the origin, where fp32 poses carry ~3 cm of rounding and l is no longer comparable
+    (the tolerances assume scenes within +-50 m), the GPU and the oracle pick the same cells:
+    slot keyframes and match counts agree exactly."""
+    s = synth.c1()
+    off = np.array([4.0e5, -3.0e5, 120.0], np.float32)
+    P = s.pose12.reshape(-1, 3, 4).copy()
+    P[:, :, 3] += off
+    K = s.kf_pose12.reshape(s.N, -1, 3, 4).copy()
+    K[:, :, :, 3] += off
+    s2 = dataclasses.replace(s, pose12=np.ascontiguousarray(P.reshape(-1, 12)),
+                             kf_pose12=np.ascontiguousarray(K.reshape(s.N, -1, 12)))
+    with make_ctx(s2) as ctx:
+        g = ctx.eval(s2.scan_mean3, s2.scan_cov6)
+    o = oracle.particles(orc_cfg(s2), oracle.Keyframes(s2.keyframes, s2.D, s2.r), s2.D_now,
+                         s2.pose12.copy(), s2.kf_pose12.copy(), s2.scan_mean3, s2.scan_cov6,
+                         apply_update=False, slots=True)
+    np.testing.assert_array_equal(g["slot_kf"], o["slot_kf"])
+    np.testing.assert_array_equal(g["slot_n"], o["slot_n"])
+    assert g["slot_n"].sum() > 0
