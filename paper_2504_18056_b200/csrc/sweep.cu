@@ -36,6 +36,13 @@ namespace mcs {
 #ifndef MCS_SWEEP_GACC
 #define MCS_SWEEP_GACC 0  // 1: fp64 stage totals in the (SoA) partial records, not shared memory
 #endif
+#ifndef MCS_SWEEP_STATIC_SMEM  // static shared arrays when they fit in 48 KB (default build)
+#if MCS_SWEEP_TMA || MCS_SWEEP_GACC || (MCS_SWEEP_CHUNK + 2) * 48 + 224 * MCS_SWEEP_THREADS > 49152
+#define MCS_SWEEP_STATIC_SMEM 0
+#else
+#define MCS_SWEEP_STATIC_SMEM 1
+#endif
+#endif
 #ifndef MCS_SWEEP_MINBLOCKS
 #define MCS_SWEEP_MINBLOCKS 4
 #endif
@@ -73,6 +80,15 @@ __device__ __forceinline__ void ld_slot(const float4* sl, float4& s0, float4& s1
   asm volatile("ld.global.nc.v2.f32 {%0, %1}, [%2];" : "=f"(s2.x), "=f"(s2.y) : "l"(sl + 2));
   s2.z = 0.f;
   s2.w = 0.f;
+}
+
+// shared-memory load through a 32-bit shared-window address (kept in one register; a generic
+// pointer would make ptxas re-derive the window base from %cgactaid at every use)
+__device__ __forceinline__ float4 lds4(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+  return v;
 }
 
 // ---- TMA bulk-copy staging (MCS_SWEEP_TMA): mbarrier + cp.async.bulk wrappers ----
@@ -114,15 +130,24 @@ __global__ void __launch_bounds__(kSweepThreads, MCS_SWEEP_MINBLOCKS)
                  const KfMeta* __restrict__ kmeta, float inv_r, float nn_r2,
                  double* __restrict__ part, size_t pstride) {
   // dynamic shared memory: [(kChunk + 2) * 3] float4 scan stage, then [28][threads] fp64 totals
-  extern __shared__ float4 smem_dyn[];
-  float4* s_pt = smem_dyn;  // the current stage (MCS_SWEEP_TMA: one of two buffers)
   constexpr int kStage = (kChunk + 2) * 3;  // float4 per stage buffer (2 spare points)
   constexpr int kBufs = MCS_SWEEP_TMA ? 2 : 1;
+#if MCS_SWEEP_STATIC_SMEM
+  // static shared memory: link-time addresses, nothing to rematerialise per point
+  __shared__ float4 smem_dyn[kBufs * kStage];
+  __shared__ double s_acc_st[28][kSweepThreads];
+  double(*s_acc)[kSweepThreads] = s_acc_st;
+#else
+  extern __shared__ float4 smem_dyn[];
   // two-level accumulation: fp32 registers within a stage, fp64 totals per thread in shared
   // memory across stages (the fp32 running sums over a whole 4,096-point scan lose ~1e-5
   // relative, which an ill-conditioned H turns into >1e-5 m of pose error)
   double(*s_acc)[kSweepThreads] =
       reinterpret_cast<double(*)[kSweepThreads]>(smem_dyn + kBufs * kStage);
+#endif
+  float4* s_pt = smem_dyn;  // the current stage (MCS_SWEEP_TMA: one of two buffers)
+  uint32_t s_pt_u32 = (uint32_t)__cvta_generic_to_shared(smem_dyn);  // same, shared window
+  auto pt = [&](int j, int w) { return lds4(s_pt_u32 + 48u * j + 16u * w); };  // word w of point j
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   const int item = t < n_items ? order[t] : -1;
   // point splits (gridDim.y): this CTA's run of whole stages, and its own partial records
@@ -166,7 +191,7 @@ __global__ void __launch_bounds__(kSweepThreads, MCS_SWEEP_MINBLOCKS)
   // transform, cell and key of point j (pinned, R27) and its first probe slot
   auto locate = [&](int j) {
     Probe p;
-    const float4 A = s_pt[3 * j];
+    const float4 A = pt(j, 0);
     // q = kR mu + kt with the pinned chain fma(R2, z, fma(R1, y, fma(R0, x, t))) per lane (R27)
     p.qx = __fmaf_rn(R02, A.z, __fmaf_rn(R01, A.y, __fmaf_rn(R00, A.x, tx)));
     p.qyz = fma2(Ryz2, bc(A.z), fma2(Ryz1, bc(A.y), fma2(Ryz0, bc(A.x), tyz)));
@@ -235,9 +260,9 @@ __global__ void __launch_bounds__(kSweepThreads, MCS_SWEEP_MINBLOCKS)
   // Eqs.3-4 and Eq.6 for one matched (item, point); the (y, z) halves of the 3-vectors and of
   // the symmetric 3x3 matrices travel as register pairs (packed FFMA2/FMUL2/FADD2)
   auto accumulate = [&](int j, const Probe& p) {
-    const float4 A = s_pt[3 * j];      // {mu, lambda3}
-    const float4 U = s_pt[3 * j + 1];  // {u, 0}
-    const float4 V = s_pt[3 * j + 2];  // {v, 0}   Sigma_j = lambda3 I + u u^T + v v^T
+    const float4 A = pt(j, 0);  // {mu, lambda3}
+    const float4 U = pt(j, 1);  // {u, 0}
+    const float4 V = pt(j, 2);  // {v, 0}   Sigma_j = lambda3 I + u u^T + v v^T
     // payload {key, mu'} {S'yy, S'zz, S'xy, S'xz} {S'xx, S'yz}
     const float4 P0 = p.s0, P1 = p.s1, P2 = p.s2;
     // e = mu' - kT mu   (Eq.4);  m = R mu = q - t
@@ -484,6 +509,7 @@ __global__ void __launch_bounds__(kSweepThreads, MCS_SWEEP_MINBLOCKS)
   }
   for (int k = 0; k < n_stages; ++k) {
     s_pt = smem_dyn + (k & 1) * kStage;
+    s_pt_u32 = (uint32_t)__cvta_generic_to_shared(s_pt);
     mbar_wait(&full[k & 1], (k >> 1) & 1);
     if (active) {
       stage(min(kChunk, S - (st_lo + k) * kChunk));
@@ -606,7 +632,8 @@ void launch_sweep(mcs_ctx* c, int S) {
   const dim3 grid((n_items + kSweepThreads - 1) / kSweepThreads, P);
   const float inv_r = 1.0f / c->cfg.voxel_resolution;
   static_assert(!(MCS_SWEEP_TMA && MCS_SWEEP_GACC), "the TMA mbarriers follow s_acc");
-  constexpr size_t smem = sizeof(float4) * (kChunk + 2) * 3 * (MCS_SWEEP_TMA ? 2 : 1) +
+  constexpr size_t smem = MCS_SWEEP_STATIC_SMEM ? 0 :
+                          sizeof(float4) * (kChunk + 2) * 3 * (MCS_SWEEP_TMA ? 2 : 1) +
                           (MCS_SWEEP_GACC ? 0 : sizeof(double) * 28 * kSweepThreads) +
                           (MCS_SWEEP_TMA ? 32 : 0);
   const size_t pstride = (size_t)c->cfg.neighbor_count * c->capN;
