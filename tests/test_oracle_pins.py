@@ -517,3 +517,36 @@ def test_resample_exact_ladder_boundaries():
         dead[dead_idx] = 1
         ref, *_ = _systematic_brute_force(e, dead, U)
         assert list(oracle.resample(e, dead, U)) == ref
+
+
+def test_sandwich_rotates_the_scan_covariance_eigenvectors():
+    """C = Sigma' + R Sigma R^T (Eq.4): with Sigma' = eps I and a residual along the rotated
+    eigenvector R u_i of Sigma, l = -s^2 / (eps + lambda_i) for every rotation R — a transposed
+    or missing R in the sandwich gives another value (spectral theorem; not the oracle's own
+    formula)."""
+    g = np.random.default_rng(7)
+    eps, s = 0.01, 0.05
+    lam = np.array([0.09, 0.04, 0.002])
+    U = Rotation.from_rotvec(g.normal(size=3)).as_matrix()
+    Sig = U @ np.diag(lam) @ U.T
+    c6 = np.array([[Sig[0, 0], Sig[0, 1], Sig[0, 2], Sig[1, 1], Sig[1, 2], Sig[2, 2]]],
+                  np.float32)
+    Sig = np.array([[c6[0, 0], c6[0, 1], c6[0, 2]], [c6[0, 1], c6[0, 3], c6[0, 4]],
+                    [c6[0, 2], c6[0, 4], c6[0, 5]]], np.float64)  # the fp32-rounded input
+    lam, U = np.linalg.eigh(Sig)
+    mu_p = np.array([[1.0, 1.0, 1.0]], np.float32)  # middle of voxel (0, 0, 0) at r = 2
+    m = oracle.Map(mu_p, np.array([[eps, 0, 0, eps, 0, eps]], np.float32), 2.0)
+    mu = np.array([[0.3, -0.2, 0.1]], np.float32)
+    for trial in range(4):
+        R = Rotation.from_rotvec(g.normal(size=3) * 0.7).as_matrix()
+        for i in range(3):
+            v = s * (R @ U[:, i])              # wanted residual e = mu' - (R mu + t)
+            t = mu_p[0] - R @ mu[0] - v
+            T = np.eye(4)
+            T[:3, :3], T[:3, 3] = R, t
+            rel32 = np.asarray(T[:3, :4], np.float32)
+            res = oracle.pair_linearize(m, mu, c6, rel32, T[:3, :4])
+            assert res.n == 1
+            e = mu_p[0].astype(np.float64) - (R @ mu[0].astype(np.float64) + t)
+            expect = -(e @ e) / (eps + lam[i])  # e is v up to fp32 input rounding
+            assert res.l == pytest.approx(expect, rel=1e-6), (trial, i)
