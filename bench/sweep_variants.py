@@ -10,7 +10,6 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 VARIANTS = {
     "base": [],
-    "dynamic_smem": ["MCS_SWEEP_STATIC_SMEM=0"],
 }
 OUT = os.path.join(ROOT, "bench", "_variants")
 

@@ -17,13 +17,17 @@
 namespace mcs {
 
 // Lane-coherence sort key of a work item: the keyframe id in the top bits, then
-// a 6-D Morton code of where the item's relative pose sends two reference points 8 m out on
-// the x and y axes, at 1/8 m steps (5 bits per coordinate, wrapping every 4 m: one radix pass
-// fewer than 6 bits at 1/16 m, same sweep time).  Items that
+// a 6-D Morton code of where the item's relative pose sends two reference points 16 m out on
+// the x and y axes (a typical LiDAR range, which weighs rotation against translation the way
+// the scan's own points do; 4 m / 8 m / 24 m / 32 m measured slower), at 1/8 m steps (5 bits
+// per coordinate, wrapping every 4 m: one radix pass fewer than 6 bits at 1/16 m).  Items that
 // are adjacent in this order probe the same cells for the same scan point, so a warp's
 // gathers coalesce and its hit/miss branches agree.
 #ifndef MCS_MORTON_BITS
 #define MCS_MORTON_BITS 5
+#endif
+#ifndef MCS_MORTON_REF
+#define MCS_MORTON_REF 16.0f  // distance of the two reference points (m): a typical LiDAR range
 #endif
 #ifndef MCS_MORTON_SCALE
 #define MCS_MORTON_SCALE 8.0f
@@ -32,7 +36,7 @@ constexpr int kMortonBitsPerDim = MCS_MORTON_BITS;
 constexpr int kMortonBits = 6 * kMortonBitsPerDim;
 
 __device__ __forceinline__ unsigned long long coherence_key(int kf, const float* rel) {
-  const float d = 8.0f;
+  const float d = MCS_MORTON_REF;
   float q[6];
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
