@@ -32,26 +32,29 @@ namespace mcs {
 #ifndef MCS_MORTON_SCALE
 #define MCS_MORTON_SCALE 8.0f
 #endif
+#ifndef MCS_MORTON_PTS
+#define MCS_MORTON_PTS 2  // reference points on the x, y (, z) axes
+#endif
 constexpr int kMortonBitsPerDim = MCS_MORTON_BITS;
-constexpr int kMortonBits = 6 * kMortonBitsPerDim;
+constexpr int kMortonDims = 3 * MCS_MORTON_PTS;
+constexpr int kMortonBits = kMortonDims * kMortonBitsPerDim;
 
 __device__ __forceinline__ unsigned long long coherence_key(int kf, const float* rel) {
   const float d = MCS_MORTON_REF;
-  float q[6];
+  float q[kMortonDims];
 #pragma unroll
-  for (int a = 0; a < 3; ++a) {
-    q[a] = d * rel[4 * a + 0] + rel[4 * a + 3];
-    q[3 + a] = d * rel[4 * a + 1] + rel[4 * a + 3];
-  }
-  unsigned int c[6];
+  for (int p = 0; p < MCS_MORTON_PTS; ++p)
 #pragma unroll
-  for (int k = 0; k < 6; ++k)
+    for (int a = 0; a < 3; ++a) q[3 * p + a] = d * rel[4 * a + p] + rel[4 * a + 3];
+  unsigned int c[kMortonDims];
+#pragma unroll
+  for (int k = 0; k < kMortonDims; ++k)
     c[k] = (unsigned int)__float2int_rd(q[k] * MCS_MORTON_SCALE) & ((1u << kMortonBitsPerDim) - 1u);
   unsigned long long m = 0ull;
 #pragma unroll
   for (int b = kMortonBitsPerDim - 1; b >= 0; --b)
 #pragma unroll
-    for (int k = 0; k < 6; ++k) m = (m << 1) | ((c[k] >> b) & 1u);
+    for (int k = 0; k < kMortonDims; ++k) m = (m << 1) | ((c[k] >> b) & 1u);
   return ((unsigned long long)kf << kMortonBits) | m;
 }
 
