@@ -109,6 +109,26 @@ def own_peaks():
         return {}
 
 
+def committed_ncu_context():
+    """FMA-pipe and issue activity of the sweep from the committed ncu summary (context for the
+    roofline: the kernel is issue/FMA-pipe limited, not memory limited)."""
+    import glob
+    out = {}
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_sweep_v*_ncu.txt")),
+                   key=lambda f: int(f.rsplit("_v", 1)[1].split("_")[0]))
+    if not files:
+        return None
+    for line in open(files[-1]):
+        parts = line.split()
+        if len(parts) >= 2 and parts[0] in (
+                "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
+                "smsp__issue_active.avg.pct_of_peak_sustained_active",
+                "l1tex__t_sector_hit_rate.pct", "lts__t_sector_hit_rate.pct"):
+            out[parts[0].split(".")[0]] = float(parts[1]) / 100.0
+    out["source"] = os.path.relpath(files[-1], ROOT)
+    return out
+
+
 def committed_traffic():
     p = os.path.join(ROOT, "profiles", "sweep_traffic.json")
     if os.path.exists(p):
@@ -382,7 +402,8 @@ def run_gpu(args):
                                     f"({peak_src} sm_max_mhz)",
                      "flops_per_launch": flops, "sweep_ms": sweep_avg,
                      "l2_gather_GBps": gather / (sweep_avg * 1e-3) / 1e9,
-                     "gather": gather_roofline(gather, sweep_avg)},
+                     "gather": gather_roofline(gather, sweep_avg),
+                     "ncu": committed_ncu_context()},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(36 * S),
                 "d2h_bytes_per_step": int(16 * N + 4 + 8), "ms_per_step": 1e3 * e2e_mean},
         "gpu_launches": LAUNCHES_PER_UPDATE * args.steps,
