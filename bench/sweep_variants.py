@@ -10,6 +10,12 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 VARIANTS = {
     "base": [],
+    "chunk128": ["MCS_SWEEP_CHUNK=128"],
+    "chunk512": ["MCS_SWEEP_CHUNK=512"],
+    "mscale6": ["MCS_MORTON_SCALE=6.0f"],
+    "mscale12": ["MCS_MORTON_SCALE=12.0f"],
+    "mbits4": ["MCS_MORTON_BITS=4"],
+    "mbits4s4": ["MCS_MORTON_BITS=4", "MCS_MORTON_SCALE=4.0f"],
 }
 OUT = os.path.join(ROOT, "bench", "_variants")
 
@@ -33,7 +39,7 @@ def run_one(name):
     ctx.set_particles(s.pose12, s.kf_pose12)
     ctx.snapshot()
     ctx.set_profiling(True)
-    sw, sel = [], []
+    sw, sel, tot = [], [], []
     for k in range(8):
         ctx.restore()
         ctx.update(s.scan_mean3, s.scan_cov6, s.D_now, s.U, outputs=("loglik",))
@@ -41,7 +47,9 @@ def run_one(name):
             ph = ctx.phase_ms()
             sw.append(ph["sweep"])
             sel.append(ph["select"])
-    print(json.dumps({"select_ms": float(np.median(sel))}), file=sys.stderr)
+            tot.append(ph["total"])
+    print(json.dumps({"select_ms": float(np.median(sel)), "total_ms": float(np.median(tot))}),
+          file=sys.stderr)
     return float(np.median(sw))
 
 
