@@ -64,6 +64,9 @@ class ClockSampler:
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            t0 = time.time()  # nvidia-smi takes a moment to start: wait for its first sample
+            while not self.rows and time.time() - t0 < 5.0 and self.proc.poll() is None:
+                time.sleep(0.02)
         except FileNotFoundError:
             self.proc = None
         return self
@@ -260,9 +263,11 @@ def run_gpu(args):
                       device=local, **extra)
     ctx.set_stream(stream)
     t0 = time.perf_counter()
-    for (m3, c6), d in zip(s.keyframes, s.D):
+    for k, ((m3, c6), d) in enumerate(zip(s.keyframes, s.D)):
+        if k == 1:  # the first insertion also pays the lazy loading of the library's kernels
+            t0 = time.perf_counter()
         ctx.add_keyframe(m3, c6, d)
-    a0_ms = 1e3 * (time.perf_counter() - t0) / K
+    a0_ms = 1e3 * (time.perf_counter() - t0) / max(K - 1, 1)
     ctx.set_particles(s.pose12, s.kf_pose12)
     # match statistics (algorithmic work per launch), untimed
     ev = ctx.eval(s.scan_mean3, s.scan_cov6)
@@ -310,26 +315,43 @@ def run_gpu(args):
             e1.record(stream)
         return e0, e1
 
-    step_ms, sweep_ms, phases = [], [], []
-    with ClockSampler(local) as clocks:
-        for _ in range(args.warmup):
-            one_step()
-        torch.cuda.synchronize()
-        if dist:
-            dist.barrier()
-        torch.cuda.synchronize()
-        for _ in range(args.steps):
-            e0, e1 = one_step()
-            e1.synchronize()
-            step_ms.append(e0.elapsed_time(e1))
-            if graph is None:
-                ph = ctx.phase_ms()
-                phases.append(ph)
-                sweep_ms.append(ph["sweep"])
-        torch.cuda.synchronize()
-        if dist:
-            dist.barrier()
-        torch.cuda.synchronize()
+    def timed_region():
+        step_ms, sweep_ms, phases = [], [], []
+        with ClockSampler(local) as clocks:
+            for _ in range(args.warmup):
+                one_step()
+            torch.cuda.synchronize()
+            if dist:
+                dist.barrier()
+            torch.cuda.synchronize()
+            for _ in range(args.steps):
+                e0, e1 = one_step()
+                e1.synchronize()
+                step_ms.append(e0.elapsed_time(e1))
+                if graph is None:
+                    ph = ctx.phase_ms()
+                    phases.append(ph)
+                    sweep_ms.append(ph["sweep"])
+            torch.cuda.synchronize()
+            if dist:
+                dist.barrier()
+            torch.cuda.synchronize()
+        return step_ms, sweep_ms, phases, clocks
+
+    step_ms, sweep_ms, phases, clocks = timed_region()
+    # a run that saw a hardware / thermal slowdown is re-measured once (the decision is the
+    # same on every rank: a MAX over ranks of the flag)
+    bad = {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"}
+    flag = float(bool(bad & set(clocks.summary()["reasons"])))
+    if dist:
+        t = torch.tensor([flag], dtype=torch.float64,
+                         device=dev if args.dist_backend == "nccl" else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        flag = float(t.item())
+    remeasured = None
+    if flag > 0:
+        remeasured = clocks.summary()["reasons"]
+        step_ms, sweep_ms, phases, clocks = timed_region()
     if graph is not None:  # phase breakdown (roofline) from profiled eager updates, untimed
         ctx.set_profiling(True)
         for k in range(max(3, min(args.steps, 10))):
@@ -407,7 +429,8 @@ def run_gpu(args):
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(36 * S),
                 "d2h_bytes_per_step": int(16 * N + 4 + 8), "ms_per_step": 1e3 * e2e_mean},
         "gpu_launches": LAUNCHES_PER_UPDATE * args.steps,
-        "clocks": clocks.summary(),
+        "clocks": dict(clocks.summary(), **({"remeasured_after": remeasured} if remeasured
+                                             else {})),
         "ms_p10_p50_p90": [float(np.percentile(step_ms, q)) for q in (10, 50, 90)],
         "phase_ms": ph_mean,
         "triple_evals_per_s": triples * args.steps / (total_ms * 1e-3),
