@@ -10,12 +10,6 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 VARIANTS = {
     "base": [],
-    "chunk128": ["MCS_SWEEP_CHUNK=128"],
-    "chunk512": ["MCS_SWEEP_CHUNK=512"],
-    "mscale6": ["MCS_MORTON_SCALE=6.0f"],
-    "mscale12": ["MCS_MORTON_SCALE=12.0f"],
-    "mbits4": ["MCS_MORTON_BITS=4"],
-    "mbits4s4": ["MCS_MORTON_BITS=4", "MCS_MORTON_SCALE=4.0f"],
 }
 OUT = os.path.join(ROOT, "bench", "_variants")
 
@@ -33,7 +27,8 @@ def run_one(name):
     import paper_2504_18056_b200 as mcs
     import synth
     s = synth.c2()
-    ctx = mcs.Context(s.N, s.K, s.S, loop_recency_gap=s.gap, voxel_resolution=s.r)
+    kw = dict(corr_mode=mcs.CORR_NN27, nn_radius=s.r) if name.startswith("nn27") else {}
+    ctx = mcs.Context(s.N, s.K, s.S, loop_recency_gap=s.gap, voxel_resolution=s.r, **kw)
     for (m3, c6), d in zip(s.keyframes, s.D):
         ctx.add_keyframe(m3, c6, d)
     ctx.set_particles(s.pose12, s.kf_pose12)

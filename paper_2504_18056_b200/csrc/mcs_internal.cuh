@@ -59,7 +59,8 @@ constexpr int kMaxNb = MCS_MAX_NEIGHBORS;
 //   float4 {key, mu'x, mu'y, mu'z}  {S'yy, S'zz, S'xy, S'xz}  {S'xx, S'yz, count, 0}  {0,0,0,0}
 // (the key shares the first 16 bytes with the mean, so the first-probe payload loads are
 // issued together with the key; the (y, z) pairs (mu'y, mu'z), (S'yy, S'zz), (S'xy, S'xz) land
-// in aligned register pairs, the operands of the sweep's packed FFMA2 math).  Load factor <= 1/4.
+// in aligned register pairs, the operands of the sweep's packed FFMA2 math).  Load factor <= 1/4
+// (down to 1/64 within a 64 MiB table, kf_store.cu).
 constexpr unsigned int kEmptyKey32 = 0xFFFFFFFFu;  // dx = 2047 never occurs (ex <= 2047)
 constexpr unsigned int kNoKey32 = 0xFFFFFFFEu;     // query key of an out-of-bbox point (dx = 2047)
 constexpr int kMaxEx = 2047, kMaxEy = 2048, kMaxEz = 1024;

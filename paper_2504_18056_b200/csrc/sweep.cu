@@ -46,6 +46,12 @@ namespace mcs {
 #ifndef MCS_SWEEP_MINBLOCKS
 #define MCS_SWEEP_MINBLOCKS 4
 #endif
+#ifndef MCS_NN27_MINBLOCKS
+#define MCS_NN27_MINBLOCKS 4
+#endif
+#ifndef MCS_NN27_BATCH
+#define MCS_NN27_BATCH 9  // NN27: cells whose first-probe loads are issued together (1, 3, 9, 27)
+#endif
 constexpr int kSweepThreads = MCS_SWEEP_THREADS;
 constexpr int kChunk = MCS_SWEEP_CHUNK;  // scan points per shared-memory stage (48 B each)
 
@@ -124,7 +130,8 @@ constexpr float kMagic = 12582912.0f;
 
 // kCorr: MCS_CORR_CELL (one probe of the containing voxel, R7) or MCS_CORR_NN27 (R33)
 template <int kCorr>
-__global__ void __launch_bounds__(kSweepThreads, MCS_SWEEP_MINBLOCKS)
+__global__ void __launch_bounds__(kSweepThreads, kCorr == MCS_CORR_NN27 ? MCS_NN27_MINBLOCKS
+                                                                       : MCS_SWEEP_MINBLOCKS)
     sweep_kernel(const float4* __restrict__ items, const int32_t* __restrict__ order,
                  int n_items, const float4* __restrict__ scan, int S,
                  const KfMeta* __restrict__ kmeta, float inv_r, float nn_r2,
@@ -339,52 +346,75 @@ __global__ void __launch_bounds__(kSweepThreads, MCS_SWEEP_MINBLOCKS)
 
   // NN27 (R33): the nearest cell representative within nn_radius among the 27 voxels around
   // q's voxel, d = mu'32 - q32, d2 = fma(dz, dz, fma(dy, dy, dx * dx)) (pinned fp32), ties ->
-  // lower (oz, oy, ox) index.  Plain loop: a flagged variant, not the timed path.
+  // lower (oz, oy, ox) index.
+  // Per cell (ox, oy, oz) the key and hash follow from the centre's by one add each: with the
+  // key taken as the modular sum kc = (bx << 21) + (by << 10) + bz, the key of an in-bbox
+  // neighbour is kc + (ox << 21) + (oy << 10) + oz (mod 2^32, equal to local_key's OR form
+  // there), and its hash product (kc + off) * M = kc * M + off * M; the bbox test is the AND
+  // of three per-axis flags computed once per point.
+  const float nn_r2_up = __int_as_float(__float_as_int(nn_r2) + 1);  // next float above nn_r2
   auto nn27_point = [&](int j) {
     Probe p = locate(j);
     const unsigned int bx = (unsigned)__float_as_int(__fmaf_rd(p.qx, inv_r, kMagic)) - offx;
     const float2 fyz = __ffma2_rd(p.qyz, bc(inv_r), bc(kMagic));
     const unsigned int by = (unsigned)__float_as_int(fyz.x) - offy;
     const unsigned int bz = (unsigned)__float_as_int(fyz.y) - offz;
+    const unsigned int kc = (bx << 21) + (by << 10) + bz;
+    const unsigned int hc = kc * kHashMul32;
+    bool fx[3], fy[3], fz[3];
+#pragma unroll
+    for (int o = 0; o < 3; ++o) {
+      fx[o] = bx + (unsigned)(o - 1) < m.ex;
+      fy[o] = by + (unsigned)(o - 1) < m.ey;
+      fz[o] = bz + (unsigned)(o - 1) < m.ez;
+    }
     int best = -1;
-    float best_d2 = 0.f;
-    // candidate: keep the nearest within the radius; strict < keeps the lower enumeration
-    // index on ties (cells are visited in (oz, oy, ox) order)
+    // d2 <= nn_r2 and strictly below the best so far (ties keep the lower enumeration index;
+    // cells are visited in (oz, oy, ox) order) is one compare against a running bound that
+    // starts just above nn_r2
+    float best_d2 = nn_r2_up;
     auto consider = [&](unsigned int h, const float4 t0) {  // t0 = {key, mu'} of slot h
       const float dx = __fsub_rn(t0.y, p.qx);
       const float dy = __fsub_rn(t0.z, p.qyz.x);
       const float dz = __fsub_rn(t0.w, p.qyz.y);
       const float d2 = __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, __fmul_rn(dx, dx)));
-      if (d2 <= nn_r2 && (best < 0 || d2 < best_d2)) {
+      if (d2 < best_d2) {
         best = (int)h;
         best_d2 = d2;
       }
     };
+    // the first-probe loads (key + mu', 16 B) of kB cells at a time issue together, then are
+    // consumed in (oz, oy, ox) order
+    constexpr int kB = MCS_NN27_BATCH;
+    static_assert(27 % kB == 0, "MCS_NN27_BATCH: 1, 3, 9 or 27");
 #pragma unroll
-    for (int oz = -1; oz <= 1; ++oz) {
-      // one z-layer at a time: the nine first-probe loads (key + mu', 16 B) issue together
-      unsigned int key[9], h[9];
-      float4 t[9];
+    for (int c0 = 0; c0 < 27; c0 += kB) {
+      unsigned int key[kB], h[kB];
+      float4 t[kB];
 #pragma unroll
-      for (int c = 0; c < 9; ++c) {
-        const unsigned int cx = bx + (c % 3 - 1), cy = by + (c / 3 - 1), cz = bz + oz;
-        const bool in = (cx < m.ex) & (cy < m.ey) & (cz < m.ez);
-        key[c] = in ? local_key(cx, cy, cz) : kNoKey32;
-        h[c] = in ? slot_hash(key[c], m.shift) : m.mask + 1;  // sentinel: always empty
-        t[c] = __ldg(m.slots + 4 * (size_t)h[c]);
+      for (int u = 0; u < kB; ++u) {
+        const int c = c0 + u;
+        const int ox = c % 3 - 1, oy = (c / 3) % 3 - 1, oz = c / 9 - 1;
+        const unsigned int off = (unsigned)(ox * (1 << 21) + oy * (1 << 10) + oz);
+        const bool in = fx[ox + 1] & fy[oy + 1] & fz[oz + 1];
+        key[u] = in ? kc + off : kNoKey32;
+        h[u] = in ? (hc + off * kHashMul32) >> m.shift : m.mask + 1;  // sentinel: always empty
+        MCS_DCHECK(!in || (key[u] == local_key(bx + ox, by + oy, bz + oz) &&
+                           h[u] == slot_hash(key[u], m.shift)));
+        t[u] = __ldg(m.slots + 4 * (size_t)h[u]);
       }
 #pragma unroll
-      for (int c = 0; c < 9; ++c) {
-        const unsigned int k0 = __float_as_uint(t[c].x);
-        if (k0 == key[c]) {
-          consider(h[c], t[c]);
+      for (int u = 0; u < kB; ++u) {
+        const unsigned int k0 = __float_as_uint(t[u].x);
+        if (k0 == key[u]) {
+          consider(h[u], t[u]);
         } else if (k0 != kEmptyKey32) {  // rare: continue linear probing
-          unsigned int hh = h[c];
+          unsigned int hh = h[u];
           while (true) {
             hh = (hh + 1) & m.mask;
             const float4 tt = __ldg(m.slots + 4 * (size_t)hh);
             const unsigned int kk = __float_as_uint(tt.x);
-            if (kk == key[c]) {
+            if (kk == key[u]) {
               consider(hh, tt);
               break;
             }
