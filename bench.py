@@ -126,7 +126,8 @@ def committed_ncu_context():
         if len(parts) >= 2 and parts[0] in (
                 "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
                 "smsp__issue_active.avg.pct_of_peak_sustained_active",
-                "l1tex__t_sector_hit_rate.pct", "lts__t_sector_hit_rate.pct"):
+                "l1tex__t_sector_hit_rate.pct", "lts__t_sector_hit_rate.pct",
+                "l1tex__throughput.avg.pct_of_peak_sustained_active"):
             out[parts[0].split(".")[0]] = float(parts[1]) / 100.0
     out["source"] = os.path.relpath(files[-1], ROOT)
     return out
