@@ -78,11 +78,24 @@ __device__ __forceinline__ float2 mul2(float2 a, float2 b) { return __fmul2_rn(a
 __device__ __forceinline__ float2 add2(float2 a, float2 b) { return __fadd2_rn(a, b); }
 __device__ __forceinline__ float2 neg2(float2 a) { return make_float2(-a.x, -a.y); }
 
+#ifndef MCS_SWEEP_LDG256
+#define MCS_SWEEP_LDG256 1  // 1: the slot's first sector (key, mu', 4 of Sigma') as one 256-bit load
+#endif
+// the 40 used bytes of a 64-byte slot: sector 0 {key, mu'} {S'yy, S'zz, S'xy, S'xz} and the
+// first 8 bytes of sector 1 {S'xx, S'yz}.  sm_100 loads a whole 32-byte sector per lane in one
+// instruction (LDG.256): one request and its L1 wavefronts instead of two
 __device__ __forceinline__ void ld_slot(const float4* sl, float4& s0, float4& s1, float4& s2) {
+#if MCS_SWEEP_LDG256
+  asm volatile("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=f"(s0.x), "=f"(s0.y), "=f"(s0.z), "=f"(s0.w), "=f"(s1.x), "=f"(s1.y),
+                 "=f"(s1.z), "=f"(s1.w)
+               : "l"(sl));
+#else
   asm volatile("ld.global.nc.v4.f32 {%0, %1, %2, %3}, [%4];"
                : "=f"(s0.x), "=f"(s0.y), "=f"(s0.z), "=f"(s0.w) : "l"(sl));
   asm volatile("ld.global.nc.v4.f32 {%0, %1, %2, %3}, [%4];"
                : "=f"(s1.x), "=f"(s1.y), "=f"(s1.z), "=f"(s1.w) : "l"(sl + 1));
+#endif
   asm volatile("ld.global.nc.v2.f32 {%0, %1}, [%2];" : "=f"(s2.x), "=f"(s2.y) : "l"(sl + 2));
   s2.z = 0.f;
   s2.w = 0.f;
