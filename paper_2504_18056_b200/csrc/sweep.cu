@@ -167,7 +167,11 @@ __global__ void __launch_bounds__(kSweepThreads, kCorr == MCS_CORR_NN27 ? MCS_NN
 #endif
   float4* s_pt = smem_dyn;  // the current stage (MCS_SWEEP_TMA: one of two buffers)
   uint32_t s_pt_u32 = (uint32_t)__cvta_generic_to_shared(smem_dyn);  // same, shared window
-  auto pt = [&](int j, int w) { return lds4(s_pt_u32 + 48u * j + 16u * w); };  // word w of point j
+  // a point is named by its shared-window address (48 B per point): a loop-carried register
+  // that ptxas cannot rematerialise from %cgactaid at every use, as it does for a stage-constant
+  // base plus an index
+  constexpr uint32_t kPt = 48u;
+  auto pt = [&](uint32_t j, int w) { return lds4(j + 16u * w); };  // word w of point j
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   const int item = t < n_items ? order[t] : -1;
   // point splits (gridDim.y): this CTA's run of whole stages, and its own partial records
@@ -209,7 +213,7 @@ __global__ void __launch_bounds__(kSweepThreads, kCorr == MCS_CORR_NN27 ? MCS_NN
   const float2 ntyz = neg2(tyz);
 
   // transform, cell and key of point j (pinned, R27) and its first probe slot
-  auto locate = [&](int j) {
+  auto locate = [&](uint32_t j) {
     Probe p;
     const float4 A = pt(j, 0);
     // q = kR mu + kt with the pinned chain fma(R2, z, fma(R1, y, fma(R0, x, t))) per lane (R27)
@@ -234,7 +238,7 @@ __global__ void __launch_bounds__(kSweepThreads, kCorr == MCS_CORR_NN27 ? MCS_NN
   auto load = [&](Probe& p) {
     if (active) ld_slot(m.slots + 4 * (size_t)p.h, p.s0, p.s1, p.s2);
   };
-  auto issue = [&](int j) {
+  auto issue = [&](uint32_t j) {
     Probe p = locate(j);
     load(p);
     return p;
@@ -242,7 +246,7 @@ __global__ void __launch_bounds__(kSweepThreads, kCorr == MCS_CORR_NN27 ? MCS_NN
   // issue whose loads are predicated on a key already loaded (never 0xFFFFFFFD: dx = 2047):
   // ptxas must then drain the earlier probe loads before it issues these (all probe loads
   // share one scoreboard, so a later wait would also drain the new ones)
-  auto issue_after = [&](int j, unsigned int kdep) {
+  auto issue_after = [&](uint32_t j, unsigned int kdep) {
     Probe p = locate(j);
     if (active & (kdep != 0xFFFFFFFDu)) ld_slot(m.slots + 4 * (size_t)p.h, p.s0, p.s1, p.s2);
     return p;
@@ -279,7 +283,7 @@ __global__ void __launch_bounds__(kSweepThreads, kCorr == MCS_CORR_NN27 ? MCS_NN
 
   // Eqs.3-4 and Eq.6 for one matched (item, point); the (y, z) halves of the 3-vectors and of
   // the symmetric 3x3 matrices travel as register pairs (packed FFMA2/FMUL2/FADD2)
-  auto accumulate = [&](int j, const Probe& p) {
+  auto accumulate = [&](uint32_t j, const Probe& p) {
     const float4 A = pt(j, 0);  // {mu, lambda3}
     const float4 U = pt(j, 1);  // {u, 0}
     const float4 V = pt(j, 2);  // {v, 0}   Sigma_j = lambda3 I + u u^T + v v^T
@@ -346,7 +350,7 @@ __global__ void __launch_bounds__(kSweepThreads, kCorr == MCS_CORR_NN27 ? MCS_NN
   };
 
   // first probe: hit -> accumulate; empty slot (or the sentinel) -> miss; else keep probing
-  auto act = [&](int j, const Probe& p, unsigned int k0) {
+  auto act = [&](uint32_t j, const Probe& p, unsigned int k0) {
     if (k0 == p.key) {
       accumulate(j, p);
     } else if (k0 != kEmptyKey32) {
@@ -355,7 +359,7 @@ __global__ void __launch_bounds__(kSweepThreads, kCorr == MCS_CORR_NN27 ? MCS_NN
       if (probe_on(q)) accumulate(j, q);
     }
   };
-  auto consume = [&](int j, const Probe& p) { act(j, p, __float_as_uint(p.s0.x)); };
+  auto consume = [&](uint32_t j, const Probe& p) { act(j, p, __float_as_uint(p.s0.x)); };
 
   // NN27 (R33): the nearest cell representative within nn_radius among the 27 voxels around
   // q's voxel, d = mu'32 - q32, d2 = fma(dz, dz, fma(dy, dy, dx * dx)) (pinned fp32), ties ->
@@ -366,7 +370,7 @@ __global__ void __launch_bounds__(kSweepThreads, kCorr == MCS_CORR_NN27 ? MCS_NN
   // there), and its hash product (kc + off) * M = kc * M + off * M; the bbox test is the AND
   // of three per-axis flags computed once per point.
   const float nn_r2_up = __int_as_float(__float_as_int(nn_r2) + 1);  // next float above nn_r2
-  auto nn27_point = [&](int j) {
+  auto nn27_point = [&](uint32_t j) {
     Probe p = locate(j);
     const unsigned int bx = (unsigned)__float_as_int(__fmaf_rd(p.qx, inv_r, kMagic)) - offx;
     const float2 fyz = __ffma2_rd(p.qyz, bc(inv_r), bc(kMagic));
@@ -478,8 +482,9 @@ __global__ void __launch_bounds__(kSweepThreads, kCorr == MCS_CORR_NN27 ? MCS_NN
 
   // the math of one stage of cnt points in s_pt (active threads)
   auto stage = [&](const int cnt) {
+    const uint32_t e = s_pt_u32 + kPt * (uint32_t)cnt;  // one past the last point
     if (kCorr == MCS_CORR_NN27) {
-      for (int j = 0; j < cnt; ++j) nn27_point(j);
+      for (uint32_t j = s_pt_u32; j < e; j += kPt) nn27_point(j);
       return;
     }
     // Probe buffers in rotation, no register copies between iterations.  Every probe load
@@ -489,36 +494,36 @@ __global__ void __launch_bounds__(kSweepThreads, kCorr == MCS_CORR_NN27 ? MCS_NN
     // n+1 is in flight.  s_pt has two spare points, so the look-ahead issues past the stage end
     // need no guard (their stale key probes a real slot or the sentinel, and is never consumed)
 #if MCS_SWEEP_AHEAD == 4
-    Probe pa = issue(0), pb = issue(1), pc, pd;
-    int j = 0;
-    for (; j + 3 < cnt; j += 4) {
+    Probe pa = issue(s_pt_u32), pb = issue(s_pt_u32 + kPt), pc, pd;
+    uint32_t j = s_pt_u32;
+    for (; j + 3 * kPt < e; j += 4 * kPt) {
       const unsigned int ka = __float_as_uint(pa.s0.x), kb = __float_as_uint(pb.s0.x);
-      pc = issue_after(j + 2, ka);
-      pd = issue_after(j + 3, kb);
+      pc = issue_after(j + 2 * kPt, ka);
+      pd = issue_after(j + 3 * kPt, kb);
       act(j, pa, ka);
-      act(j + 1, pb, kb);
+      act(j + kPt, pb, kb);
       const unsigned int kc = __float_as_uint(pc.s0.x), kd = __float_as_uint(pd.s0.x);
-      pa = issue_after(j + 4, kc);
-      pb = issue_after(j + 5, kd);
-      act(j + 2, pc, kc);
-      act(j + 3, pd, kd);
+      pa = issue_after(j + 4 * kPt, kc);
+      pb = issue_after(j + 5 * kPt, kd);
+      act(j + 2 * kPt, pc, kc);
+      act(j + 3 * kPt, pd, kd);
     }
-    if (j < cnt) consume(j, pa);
-    if (j + 1 < cnt) consume(j + 1, pb);
-    if (j + 2 < cnt) {
-      pc = issue(j + 2);
-      consume(j + 2, pc);
+    if (j < e) consume(j, pa);
+    if (j + kPt < e) consume(j + kPt, pb);
+    if (j + 2 * kPt < e) {
+      pc = issue(j + 2 * kPt);
+      consume(j + 2 * kPt, pc);
     }
 #else
-    Probe pa = issue(0), pb;
-    int j = 0;
-    for (; j + 1 < cnt; j += 2) {
-      pb = issue(j + 1);
+    Probe pa = issue(s_pt_u32), pb;
+    uint32_t j = s_pt_u32;
+    for (; j + kPt < e; j += 2 * kPt) {
+      pb = issue(j + kPt);
       consume(j, pa);
-      pa = issue(j + 2);
-      consume(j + 1, pb);
+      pa = issue(j + 2 * kPt);
+      consume(j + kPt, pb);
     }
-    if (j < cnt) consume(j, pa);
+    if (j < e) consume(j, pa);
 #endif
   };
 
