@@ -114,6 +114,7 @@ def main():
     out["rows"]["driver_frame"] = {
         "ms_median_host_inclusive": float(np.median(frame_ms[2:])), "particles": N,
         "scan_points": S, "frames": tr.F, "keyframes_at_end": K_end,
+        "frame_ms": [round(x, 3) for x in frame_ms],
         "note": "includes the read-back of every current pose, L and w each frame (6.4 MB); "
                 "context: the paper reports ~50-60 ms per frame on an RTX 4090 (P:240)"}
     print(json.dumps(out))

@@ -194,7 +194,7 @@ static bool is_pow2_float(float r) {
 }
 
 static void free_all(mcs_ctx* c) {
-  for (auto& k : c->kf) mem_free(c, k.slots);
+  for (auto& k : c->kf) mem_free_async(c, k.slots, c->stream);
   void* ptrs[] = {c->d_kf_meta, c->d_D,       c->d_pose,     c->d_kfpose,   c->d_L,
                   c->d_snapshot, c->d_scan_raw, c->d_scan,    c->d_items,    c->d_order,
                   c->d_part,    c->d_meta,    c->d_to,       c->d_l,        c->d_psi,
@@ -486,7 +486,7 @@ mcs_status mcs_add_keyframe(mcs_ctx* ctx, const float* mean3, const float* cov6,
   if (bad_cell)
     FAIL(ctx, MCS_E_INVALID_ARG, "%d keyframe points outside the 21-bit cell range", bad_cell);
   if (bad_extent) {
-    if (kh.slots) mem_free(ctx, kh.slots);
+    if (kh.slots) mem_free_async(ctx, kh.slots, st);
     FAIL(ctx, MCS_E_INVALID_ARG,
          "keyframe occupied extent exceeds 2047 x 2048 x 1024 cells at r = %g m",
          (double)ctx->cfg.voxel_resolution);

@@ -185,7 +185,9 @@ cudaError_t kf_build(mcs_ctx* c, const float* d_mean3, const float* d_cov6, int 
     out.n_cells = n_cells;
     out.n_points = n;
     // cap probe slots + one always-empty sentinel slot (index cap) that out-of-bbox queries read
-    CK(mem_alloc(c, (void**)&out.slots, sizeof(float4) * 4 * (size_t)(cap + 1)));
+    // stream-ordered from the pool the context keeps mapped (a sparse table is tens of MiB: a
+    // plain cudaMalloc of that size synchronises the device and maps pages on every insertion)
+    CK(mem_alloc_async(c, (void**)&out.slots, sizeof(float4) * 4 * (size_t)(cap + 1), st));
     m.slots = out.slots;
     out.meta = m;
     init_slots_kernel<<<(cap + 1 + 255) / 256, 256, 0, st>>>(out.slots, cap + 1);
