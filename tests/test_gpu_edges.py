@@ -127,3 +127,19 @@ def test_far_from_origin_correspondences_stay_exact():
     np.testing.assert_array_equal(g["slot_kf"], o["slot_kf"])
     np.testing.assert_array_equal(g["slot_n"], o["slot_n"])
     assert g["slot_n"].sum() > 0
+
+
+def test_keyframe_larger_than_the_sparse_table_budget():
+    """A keyframe of ~300k occupied cells: 4 x cells already exceeds the 64 MiB table budget, so
+    its table stays at the minimum capacity (load up to 1/4, linear-probing chains common)
+    instead of the sparse 1/64; correspondences and l still match the oracle."""
+    s = synth.c1()
+    m3, c6 = s.keyframes[0]
+    g = np.stack(np.meshgrid(np.arange(70), np.arange(70), np.arange(62), indexing="ij"), -1)
+    fill = (g.reshape(-1, 3) * 0.5 + 0.25 + np.array([40.0, -20.0, -10.0])).astype(np.float32)
+    fc = np.tile(np.array([1e-2, 0, 0, 1e-2, 0, 1e-2], np.float32), (len(fill), 1))
+    big = (np.concatenate([m3, fill]), np.concatenate([c6, fc]))
+    s2 = dataclasses.replace(s, keyframes=[big], pose12=np.ascontiguousarray(s.pose12[:300]),
+                             kf_pose12=np.ascontiguousarray(s.kf_pose12[:300]))
+    assert len(big[0]) > 300_000
+    _eval_parity(s2)
