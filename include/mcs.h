@@ -139,6 +139,12 @@ typedef struct mcs_config {
   int32_t  graph_replay;         /* 1 (default): a single-rank update body is captured once into
                                     a CUDA graph and replayed while the scan size, particle and
                                     keyframe counts stay the same; 0: launched kernel by kernel */
+  int32_t  kf_table_mib;         /* per-keyframe hash-table budget (MiB): the table's power-of-two
+                                    capacity is >= 4 x the occupied cells and is doubled up to 64 x
+                                    the cells while it stays within this budget (a sparse table:
+                                    first probes almost never walk a linear-probing chain; C2: 32
+                                    MiB per keyframe); 64 (default); 0 = minimum capacity (load up
+                                    to 1/4, least memory).  Results do not depend on it.        */
 } mcs_config;
 
 /* sizeof(mcs_config) of this build: bindings check their mirror of the struct against it. */

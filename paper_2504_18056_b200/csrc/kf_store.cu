@@ -14,17 +14,14 @@
 #include "mcs_internal.cuh"
 
 // Table capacity: the smallest power of two >= 4 x the occupied cells (load <= 1/4), then
-// doubled up to MCS_HASH_SLOTS_PER_CELL x the cells while the table stays within
-// MCS_HASH_TABLE_MAX_BYTES.  A sparse table costs HBM (64 B per slot; C2: 32 MiB per
-// keyframe) and buys first probes that almost never meet another key: at load 1/4, about a
-// quarter of the probes for empty cells (36 % of the sweep's probes at C2) and a sixth of
-// those for occupied cells continue down a dependent linear-probing chain; at 1/64 the C2
-// sweep runs 7.5 % faster and NN27 12 %.
+// doubled up to MCS_HASH_SLOTS_PER_CELL x the cells while the table stays within the
+// context's budget (mcs_config.kf_table_mib, 64 MiB by default).  A sparse table costs HBM
+// (64 B per slot; C2: 32 MiB per keyframe) and buys first probes that almost never meet
+// another key: at load 1/4, about a quarter of the probes for empty cells (36 % of the
+// sweep's probes at C2) and a sixth of those for occupied cells continue down a dependent
+// linear-probing chain; at 1/64 the C2 sweep runs 7.5 % faster and NN27 12 %.
 #ifndef MCS_HASH_SLOTS_PER_CELL
 #define MCS_HASH_SLOTS_PER_CELL 64
-#endif
-#ifndef MCS_HASH_TABLE_MAX_BYTES
-#define MCS_HASH_TABLE_MAX_BYTES (64ll << 20)
 #endif
 
 namespace mcs {
@@ -175,7 +172,7 @@ cudaError_t kf_build(mcs_ctx* c, const float* d_mean3, const float* d_cov6, int 
     int cap = 64, lg = 6;
     while (cap < 4 * n_cells) { cap <<= 1; ++lg; }
     while ((long long)cap < (long long)MCS_HASH_SLOTS_PER_CELL * n_cells &&
-           2ll * cap * 64 <= (long long)MCS_HASH_TABLE_MAX_BYTES && lg < 30) {
+           2ll * cap * 64 <= ((long long)c->cfg.kf_table_mib << 20) && lg < 30) {
       cap <<= 1;
       ++lg;
     }

@@ -62,6 +62,7 @@ class Config(C.Structure):
         ("peer_migration", C.c_int32),
         ("point_splits", C.c_int32),
         ("graph_replay", C.c_int32),
+        ("kf_table_mib", C.c_int32),
     ]
 
 

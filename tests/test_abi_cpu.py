@@ -32,6 +32,7 @@ def test_config_defaults_follow_the_paper_readings():
     assert cfg.loglik_rel_floor == math.log(1e-16)      # P:190, R17
     assert cfg.posterior_floor == 1e-8
     assert cfg.world_size == 1 and cfg.rank == 0
+    assert cfg.kf_table_mib == 64 and cfg.graph_replay == 1 and cfg.point_splits == 0
 
 
 def test_state_bytes_linear_in_keyframes_and_paper_memory_figure():

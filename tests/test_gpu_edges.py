@@ -143,3 +143,23 @@ def test_keyframe_larger_than_the_sparse_table_budget():
                              kf_pose12=np.ascontiguousarray(s.kf_pose12[:300]))
     assert len(big[0]) > 300_000
     _eval_parity(s2)
+
+
+@pytest.mark.parametrize("corr", ["cell", "nn27"])
+def test_table_budget_does_not_change_results(c2s, corr):
+    """mcs_config.kf_table_mib only changes where cells sit in the table (minimum load-1/4
+    capacity with 0, up to 64 slots per cell by default): every output is bitwise equal."""
+    kw = dict(corr_mode=mcs.CORR_NN27, nn_radius=c2s.r) if corr == "nn27" else {}
+    s = synth.subset(c2s, 300) if corr == "nn27" else c2s
+    outs = []
+    for mib in (0, 64):
+        with make_ctx(s, kf_table_mib=mib, **kw) as ctx:
+            ev = ctx.eval(s.scan_mean3, s.scan_cov6)
+            up = ctx.update(s.scan_mean3, s.scan_cov6, s.D_now, s.U)
+        outs.append((ev, up))
+    (e0, u0), (e1, u1) = outs
+    for k in e0:
+        np.testing.assert_array_equal(e0[k], e1[k], err_msg=k)
+    for k in ("loglik", "grad6", "hess21", "psi6", "weight", "donor", "flags"):
+        np.testing.assert_array_equal(u0[k], u1[k], err_msg=k)
+    assert u0["representative"] == u1["representative"]
