@@ -124,13 +124,13 @@ struct NcclApi {
   const char* (*GetErrorString)(int) = nullptr;
 };
 
-NcclApi* nccl() {
-  static NcclApi api;
-  static bool tried = false;
-  if (!tried) {
-    tried = true;
+// resolved once per process (a function-local static: thread-safe initialisation, so contexts
+// created concurrently from several threads see one fully filled table)
+static NcclApi load_nccl() {
+  NcclApi api;
+  {
     void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
-    if (!h) return nullptr;
+    if (!h) return api;
     api.h = h;
 #define SYM(f, n) api.f = reinterpret_cast<decltype(api.f)>(dlsym(h, n))
     SYM(GetUniqueId, "ncclGetUniqueId");
@@ -148,6 +148,11 @@ NcclApi* nccl() {
         !api.Recv || !api.GroupStart || !api.GroupEnd)
       api.h = nullptr;
   }
+  return api;
+}
+
+NcclApi* nccl() {
+  static NcclApi api = load_nccl();
   return api.h ? &api : nullptr;
 }
 

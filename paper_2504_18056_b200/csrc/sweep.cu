@@ -17,6 +17,8 @@
 // halves of the 3-vector / 3x3 math run as packed FFMA2.  R Sigma_j R^T uses the per-scan
 // spectral form of Sigma_j (prepare_scan_kernel below).  Accumulation is two-level (fp32 within
 // a 256-point stage, fp64 across stages) in a fixed order: bitwise reproducible.  DESIGN.md §5.
+#include <atomic>
+
 #include "mcs_internal.cuh"
 
 namespace mcs {
@@ -685,13 +687,15 @@ void launch_sweep(mcs_ctx* c, int S) {
                           (MCS_SWEEP_GACC ? 0 : sizeof(double) * 28 * kSweepThreads) +
                           (MCS_SWEEP_TMA ? 32 : 0);
   const size_t pstride = (size_t)c->cfg.neighbor_count * c->capN;
-  static bool attr_set[128] = {};  // opt in beyond 48 KB once per device (both instantiations)
-  if (c->dev < 0 || c->dev >= 128 || !attr_set[c->dev]) {
+  // opt in beyond 48 KB once per device (both instantiations); atomic flags: contexts may be
+  // driven from several host threads (repeating the idempotent call is harmless)
+  static std::atomic<bool> attr_set[128];
+  if (c->dev < 0 || c->dev >= 128 || !attr_set[c->dev].load(std::memory_order_acquire)) {
     cudaFuncSetAttribute(sweep_kernel<MCS_CORR_CELL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
     cudaFuncSetAttribute(sweep_kernel<MCS_CORR_NN27>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
-    if (c->dev >= 0 && c->dev < 128) attr_set[c->dev] = true;
+    if (c->dev >= 0 && c->dev < 128) attr_set[c->dev].store(true, std::memory_order_release);
   }
   if (c->cfg.corr_mode == MCS_CORR_NN27) {
     const float nn_r2 = c->cfg.nn_radius * c->cfg.nn_radius;
