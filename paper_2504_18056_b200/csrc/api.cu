@@ -350,7 +350,7 @@ mcs_status mcs_create(const mcs_config* cfg, mcs_ctx** out) {
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
   c->own_stream = (e == cudaSuccess);
   const size_t N = c->capN, K = c->capK, S = c->capS, nb = c->nbcap;
-  const size_t maxb = (N + 127) / 128 + 64;
+  const size_t maxb = (N + 31) / 32 + 64;  // block partials: combine runs 32 particles per block
   if (e == cudaSuccess) e = dalloc(c, &c->d_kf_meta, K);
   if (e == cudaSuccess) e = dalloc(c, &c->d_D, K);
   if (e == cudaSuccess) e = dalloc(c, &c->d_pose, 12 * N);

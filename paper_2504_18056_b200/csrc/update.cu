@@ -48,7 +48,9 @@ struct CombineArgs {
   uint8_t* loop_out;
 };
 
-__global__ void __launch_bounds__(128) combine_kernel(CombineArgs a) {
+// One thread per particle, the slots in a loop: the better shape when the particles fill the
+// GPU (the solve keeps every resident warp busy).
+__global__ void __launch_bounds__(128) combine_serial_kernel(CombineArgs a) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   double l = -INFINITY, Lnew = -INFINITY;
   if (i < a.N) {
@@ -269,6 +271,262 @@ __global__ void __launch_bounds__(128) combine_kernel(CombineArgs a) {
   }
 }
 
+// One block per kCombP particles and one thread per (slot, particle), for small shards where
+// one thread per particle leaves the GPU mostly idle and a3 is latency-bound: the slot threads
+// rotate their slot's H~, b~ back to the body frame (the bulk of a3's fp64 work) in parallel,
+// the slot-0 threads then sum the slots in slot order (the same additions as the serial loop,
+// so the result is bitwise that of combine_serial_kernel) and run the solve.
+constexpr int kCombP = 32;
+#ifndef MCS_COMBINE_SLOTS_BELOW
+#define MCS_COMBINE_SLOTS_BELOW 40000  // particles per device below which a3 runs per slot
+#endif  // (measured: a3 + a4 at 12.5k 0.118 -> 0.069 ms, 25k 0.122 -> 0.112; 50k 0.135 -> 0.156)
+
+__global__ void __launch_bounds__(kCombP * kMaxNb) combine_slots_kernel(CombineArgs a) {
+  const int il = threadIdx.x % kCombP, s = threadIdx.x / kCombP;  // particle lane, slot
+  const int i = blockIdx.x * kCombP + il;
+  __shared__ double sh_hb[kMaxNb][27][kCombP];  // rotated H_s (21) and b_s (6) per slot
+  __shared__ double sh_ls[kMaxNb][kCombP];
+  __shared__ int sh_ns[kMaxNb][kCombP];
+  __shared__ unsigned char sh_g[kMaxNb][kCombP];  // bit0: in G, bit1: H_s / b_s present
+  double l = -INFINITY, Lnew = -INFINITY;
+  const int nb = a.K < a.nb_max ? a.K : a.nb_max;
+  const int latest = a.K - 1;
+  // ---- phase 1: slot s of particle i
+  if (i < a.N && s < a.nb_max) {
+    const size_t item = (size_t)s * a.capN + i;
+    unsigned char g = 0;
+    double ls = 0.0;
+    int ns = 0;
+    if (s >= nb) {
+      if (a.eval_mode) {
+        const size_t o = (size_t)i * a.nb_max + s;
+        if (a.slot_l) a.slot_l[o] = 0.0;
+        if (a.slot_n) a.slot_n[o] = 0;
+        if (a.slot_kf) a.slot_kf[o] = -1;
+        if (a.slot_H21) for (int k = 0; k < 21; ++k) a.slot_H21[o * 21 + k] = 0.f;
+        if (a.slot_b6) for (int k = 0; k < 6; ++k) a.slot_b6[o * 6 + k] = 0.f;
+      }
+    } else {
+      const float4 r0 = a.items[4 * item + 0], r1 = a.items[4 * item + 1],
+                   r2 = a.items[4 * item + 2], inf = a.items[4 * item + 3];
+      const int kf = __float_as_int(inf.x);
+      const double R[9] = {r0.x, r0.y, r0.z, r1.x, r1.y, r1.z, r2.x, r2.y, r2.z};
+      // sweep partials, SoA: word k of item at part[k * pstride + item] (coalesced across i)
+      // point splits: the same word of every split record, summed in split order (fp64)
+      const double* pi = a.part + item;
+      const size_t ps = a.pstride;
+      auto o = [&](int k) {
+        double v = pi[(size_t)k * ps];
+        for (int q = 1; q < a.splits; ++q) v += pi[((size_t)q * kSlotWords + k) * ps];
+        return v;
+      };
+      ls = o(0);
+      ns = (int)o(1);
+      const bool in_G = a.gn_all ? true : (kf <= latest - a.gap);
+      g = in_G ? 1 : 0;
+      if ((a.eval_mode || a.do_gn) && (in_G || a.eval_mode)) {
+        g |= 2;
+        const size_t so = (size_t)i * a.nb_max + s;
+        float* hs_out = (a.eval_mode && a.slot_H21) ? a.slot_H21 + so * 21 : nullptr;
+        // H_s = B^T H~ B with B = blockdiag(R, R), block by block on the upper triangle only
+        // (blocks (0,0), (0,1), (1,1); block (1,0) lies below the diagonal): T = H~_pq R,
+        // H_s,pq = R^T T
+#pragma unroll
+        for (int p = 0; p < 2; ++p)
+#pragma unroll
+          for (int q = p; q < 2; ++q) {
+            double Hb[9];
+#pragma unroll
+            for (int x = 0; x < 3; ++x)
+#pragma unroll
+              for (int y = 0; y < 3; ++y) {
+                const int r = 3 * p + x, c = 3 * q + y;
+                Hb[3 * x + y] = o(2 + (r <= c ? up_idx(r, c) : up_idx(c, r)));
+              }
+            double T[9];
+#pragma unroll
+            for (int x = 0; x < 3; ++x)
+#pragma unroll
+              for (int y = 0; y < 3; ++y)
+                T[3 * x + y] = Hb[3 * x + 0] * R[0 * 3 + y] + Hb[3 * x + 1] * R[1 * 3 + y] +
+                               Hb[3 * x + 2] * R[2 * 3 + y];
+#pragma unroll
+            for (int x = 0; x < 3; ++x)
+#pragma unroll
+              for (int y = 0; y < 3; ++y) {
+                if (p == q && y < x) continue;
+                const double v = R[0 * 3 + x] * T[0 * 3 + y] + R[1 * 3 + x] * T[1 * 3 + y] +
+                                 R[2 * 3 + x] * T[2 * 3 + y];
+                const int u = up_idx(3 * p + x, 3 * q + y);
+                sh_hb[s][u][il] = v;
+                if (hs_out) hs_out[u] = (float)v;
+              }
+          }
+        // b_s = B^T b~
+#pragma unroll
+        for (int p = 0; p < 2; ++p)
+#pragma unroll
+          for (int x = 0; x < 3; ++x) {
+            const double v = R[0 * 3 + x] * o(23 + 3 * p + 0) + R[1 * 3 + x] * o(23 + 3 * p + 1) +
+                             R[2 * 3 + x] * o(23 + 3 * p + 2);
+            sh_hb[s][21 + 3 * p + x][il] = v;
+            if (a.eval_mode && a.slot_b6) a.slot_b6[so * 6 + 3 * p + x] = (float)v;
+          }
+      }
+      if (a.eval_mode) {
+        const size_t so = (size_t)i * a.nb_max + s;
+        if (a.slot_l) a.slot_l[so] = ls;
+        if (a.slot_n) a.slot_n[so] = ns;
+        if (a.slot_kf) a.slot_kf[so] = kf;
+      }
+    }
+    sh_ls[s][il] = ls;
+    sh_ns[s][il] = ns;
+    sh_g[s][il] = g;
+  }
+  __syncthreads();
+  // ---- phase 2: the slot-0 thread of particle i sums the slots in slot order and solves
+  if (s == 0 && i < a.N) {
+    double H[21], b[6];
+#pragma unroll
+    for (int k = 0; k < 21; ++k) H[k] = 0.0;
+#pragma unroll
+    for (int k = 0; k < 6; ++k) b[k] = 0.0;
+    double lsum = 0.0;
+    long long unmatched = 0;
+    for (int t = 0; t < nb; ++t) {
+      lsum += sh_ls[t][il];
+      unmatched += a.S - sh_ns[t][il];
+      if ((sh_g[t][il] & 3) == 3) {  // in G, rotated
+#pragma unroll
+        for (int k = 0; k < 21; ++k) H[k] += sh_hb[t][k][il];
+#pragma unroll
+        for (int k = 0; k < 6; ++k) b[k] += sh_hb[t][21 + k][il];
+      }
+    }
+    l = lsum - a.kappa * (double)unmatched;
+    const uint8_t loop = a.meta[i] & 1;
+    if (a.eval_mode) {
+      if (a.loop_out) a.loop_out[i] = loop;
+    } else if (a.do_gn) {
+      uint8_t flags = loop;
+      double psi[6] = {0, 0, 0, 0, 0, 0};
+      // outputs that do not depend on the solve first (frees H's registers for it)
+#pragma unroll
+      for (int k = 0; k < 6; ++k) a.grad[(size_t)k * a.capN + i] = (float)(-2.0 * b[k]);
+#pragma unroll
+      for (int k = 0; k < 21; ++k) a.hess[(size_t)k * a.capN + i] = (float)H[k];
+      if (loop) {
+        // Eq.5 with Levenberg damping (R11): (H + lambda I) psi = -b via Cholesky, in place on
+        // the packed lower triangle Lc[r(r+1)/2 + c] (fully unrolled: register-resident); a
+        // non-positive pivot marks the system singular, the rest runs on a stand-in value
+        const double tr = H[up_idx(0, 0)] + H[up_idx(1, 1)] + H[up_idx(2, 2)] +
+                          H[up_idx(3, 3)] + H[up_idx(4, 4)] + H[up_idx(5, 5)];
+        const double lam = a.damping * tr / 6.0;
+        double Lc[21];
+#pragma unroll
+        for (int r = 0; r < 6; ++r)
+#pragma unroll
+          for (int c = 0; c <= r; ++c) Lc[r * (r + 1) / 2 + c] = H[up_idx(c, r)] + (r == c ? lam : 0.0);
+        // (inner loops have constant trip counts with index guards so that every loop unrolls
+        // and Lc stays in registers)
+        bool ok = true;
+#pragma unroll
+        for (int j = 0; j < 6; ++j) {
+          double d = Lc[j * (j + 1) / 2 + j];
+#pragma unroll
+          for (int k = 0; k < 6; ++k)
+            if (k < j) d -= Lc[j * (j + 1) / 2 + k] * Lc[j * (j + 1) / 2 + k];
+          ok = ok && (d > 0.0);
+          const double ljj = sqrt(d > 0.0 ? d : 1.0);
+          Lc[j * (j + 1) / 2 + j] = ljj;
+#pragma unroll
+          for (int r = 0; r < 6; ++r) {
+            if (r <= j) continue;
+            double t = Lc[r * (r + 1) / 2 + j];
+#pragma unroll
+            for (int k = 0; k < 6; ++k)
+              if (k < j) t -= Lc[r * (r + 1) / 2 + k] * Lc[j * (j + 1) / 2 + k];
+            Lc[r * (r + 1) / 2 + j] = t / ljj;
+          }
+        }
+        if (!ok) {
+          flags |= 4;
+        } else {
+          double z[6];
+#pragma unroll
+          for (int r = 0; r < 6; ++r) {
+            double t = -b[r];
+#pragma unroll
+            for (int k = 0; k < 6; ++k)
+              if (k < r) t -= Lc[r * (r + 1) / 2 + k] * z[k];
+            z[r] = t / Lc[r * (r + 1) / 2 + r];
+          }
+#pragma unroll
+          for (int rr = 0; rr < 6; ++rr) {
+            const int r = 5 - rr;
+            double t = z[r];
+#pragma unroll
+            for (int k = 0; k < 6; ++k)
+              if (k > r) t -= Lc[k * (k + 1) / 2 + r] * psi[k];
+            psi[r] = t / Lc[r * (r + 1) / 2 + r];
+          }
+          double nrm = 0.0;
+#pragma unroll
+          for (int k = 0; k < 6; ++k) nrm += psi[k] * psi[k];
+          nrm = sqrt(nrm);
+          if (nrm > a.clamp) {
+#pragma unroll
+            for (int k = 0; k < 6; ++k) psi[k] *= a.clamp / nrm;
+            flags |= 16;
+          }
+          flags |= 2;
+          bool nz = false;
+#pragma unroll
+          for (int k = 0; k < 6; ++k) nz |= (psi[k] != 0.0);
+          if (nz) {
+            float T[12];
+#pragma unroll
+            for (int e = 0; e < 12; ++e) T[e] = a.pose[(size_t)e * a.capN + i];
+            pose_right_update(T, psi);
+#pragma unroll
+            for (int e = 0; e < 12; ++e) a.pose[(size_t)e * a.capN + i] = T[e];
+          }
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 6; ++k) a.psi[(size_t)k * a.capN + i] = psi[k];
+      a.flags[i] = flags;
+    }
+    if (!a.eval_mode && a.do_weight) {
+      a.l_out[i] = l;
+      Lnew = a.L[i] + l;  // Eq.11 in log space (R22)
+      a.L[i] = Lnew;
+    }
+  }
+  if (a.eval_mode || !a.do_weight) return;
+  // first weight reduction: max L, max l  (a5)
+  const double bm = block_reduce(Lnew, MaxOp(), -INFINITY);
+  const double bl = block_reduce(l, MaxOp(), -INFINITY);
+  if (threadIdx.x == 0) {
+    a.partials[blockIdx.x] = bm;
+    a.partials[gridDim.x + blockIdx.x] = bl;
+  }
+  if (last_block(&a.scal->counter[0])) {
+    double m = -INFINITY, ls = -INFINITY;
+    for (int k = threadIdx.x; k < (int)gridDim.x; k += blockDim.x) {
+      m = fmax(m, a.partials[k]);
+      ls = fmax(ls, a.partials[gridDim.x + k]);
+    }
+    m = block_reduce(m, MaxOp(), -INFINITY);
+    ls = block_reduce(ls, MaxOp(), -INFINITY);
+    if (threadIdx.x == 0) {
+      a.scal->m = m;
+      a.scal->lstar = ls;
+    }
+  }
+}
+
 void launch_combine(mcs_ctx* c, int S, int mode, double* slot_l, float* slot_H21,
                     float* slot_b6, int32_t* slot_n, int32_t* slot_kf, uint8_t* loop_out) {
   const bool eval_mode = mode == kCombineEval;
@@ -306,8 +564,11 @@ void launch_combine(mcs_ctx* c, int S, int mode, double* slot_l, float* slot_H21
   a.slot_n = slot_n;
   a.slot_kf = slot_kf;
   a.loop_out = loop_out;
-  const int grid = (c->N + 127) / 128;
-  combine_kernel<<<grid, 128, 0, c->stream>>>(a);
+  if (c->N >= MCS_COMBINE_SLOTS_BELOW) {
+    combine_serial_kernel<<<(c->N + 127) / 128, 128, 0, c->stream>>>(a);
+  } else {
+    combine_slots_kernel<<<(c->N + kCombP - 1) / kCombP, kCombP * a.nb_max, 0, c->stream>>>(a);
+  }
 }
 
 __global__ void propagate_kernel(float* __restrict__ kfpose, int capK, int K, int N,

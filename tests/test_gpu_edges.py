@@ -163,3 +163,23 @@ def test_table_budget_does_not_change_results(c2s, corr):
     for k in ("loglik", "grad6", "hess21", "psi6", "weight", "donor", "flags"):
         np.testing.assert_array_equal(u0[k], u1[k], err_msg=k)
     assert u0["representative"] == u1["representative"]
+
+
+def test_combine_shapes_agree_bitwise():
+    """a3 runs one thread per particle from 40,000 particles up and one thread per (slot,
+    particle) below (MCS_COMBINE_SLOTS_BELOW): both sum the slots in the same order, so the
+    per-particle outputs of the same particles agree bitwise across the two shapes."""
+    s = synth.c2(N=40000)
+    nd = dict(posterior_floor=0.0, loglik_rel_floor=-np.inf)
+    res = []
+    for n in (40000, 39999):
+        sub = synth.subset(s, n)
+        with make_ctx(sub, **nd) as ctx:
+            g = ctx.update(sub.scan_mean3, sub.scan_cov6, sub.D_now, sub.U)
+            st = ctx.get_particles()
+        res.append((g, st))
+    (g0, s0), (g1, s1) = res
+    for k in ("loglik", "grad6", "hess21", "psi6", "flags"):
+        np.testing.assert_array_equal(g0[k][:39999], g1[k], err_msg=k)
+    np.testing.assert_array_equal(s0["pose12"][:39999], s1["pose12"])
+    np.testing.assert_array_equal(s0["kf_pose12"][:39999], s1["kf_pose12"])
