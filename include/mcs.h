@@ -93,8 +93,11 @@ typedef struct mcs_transport {
 /* Device-memory hook (e.g. PyTorch's caching allocator).  Every device buffer of a context is
  * taken from alloc(bytes, stream, user) and returned through free(ptr, stream, user), with the
  * context's stream at the time of the call (persistent buffers: the stream current at create).
- * alloc returns NULL on failure (-> MCS_E_OUT_OF_MEMORY).  Both must be thread-compatible with
- * the caller; the struct is copied at mcs_create. */
+ * alloc returns NULL on failure (-> MCS_E_OUT_OF_MEMORY) and must return 256-byte aligned
+ * memory, like cudaMalloc (the sweep reads table slots with 32-byte vector loads); a misaligned
+ * block is handed back through free and the call fails (MCS_E_INVALID_ARG from mcs_create,
+ * MCS_E_CUDA with cudaErrorMisalignedAddress in mcs_last_error later).  Both must be
+ * thread-compatible with the caller; the struct is copied at mcs_create. */
 typedef struct mcs_allocator {
   void* (*alloc)(size_t bytes, void* cuda_stream, void* user);
   void  (*free)(void* ptr, void* cuda_stream, void* user);

@@ -153,11 +153,23 @@ __global__ void gather_outputs_kernel(OutPtrs o, int N, int capN, const double* 
 
 // ------------------------------------------------------------------ helpers
 namespace mcs {
+// a user allocator's block must be 256-byte aligned like cudaMalloc's (vector loads of table
+// slots); a misaligned one is returned and reported as cudaErrorMisalignedAddress, which the
+// callers turn into MCS_E_INVALID_ARG
+static cudaError_t user_block(mcs_ctx* c, void** p, cudaStream_t st) {
+  if (!*p) return cudaErrorMemoryAllocation;
+  if (reinterpret_cast<uintptr_t>(*p) % 256 != 0) {
+    c->alloc.free(*p, (void*)st, c->alloc.user);
+    *p = nullptr;
+    return cudaErrorMisalignedAddress;
+  }
+  return cudaSuccess;
+}
 cudaError_t mem_alloc(mcs_ctx* c, void** p, size_t bytes) {
   if (!bytes) bytes = 1;
   if (c->alloc.alloc) {
     *p = c->alloc.alloc(bytes, (void*)c->stream, c->alloc.user);
-    return *p ? cudaSuccess : cudaErrorMemoryAllocation;
+    return user_block(c, p, c->stream);
   }
   return cudaMalloc(p, bytes);
 }
@@ -170,7 +182,7 @@ cudaError_t mem_alloc_async(mcs_ctx* c, void** p, size_t bytes, cudaStream_t st)
   if (!bytes) bytes = 1;
   if (c->alloc.alloc) {
     *p = c->alloc.alloc(bytes, (void*)st, c->alloc.user);
-    return *p ? cudaSuccess : cudaErrorMemoryAllocation;
+    return user_block(c, p, st);
   }
   return cudaMallocAsync(p, bytes, st);
 }
@@ -418,7 +430,10 @@ mcs_status mcs_create(const mcs_config* cfg, mcs_ctx** out) {
     g_create_error = std::string("CUDA: ") + cudaGetErrorString(e);
     free_all(c);
     delete c;
-    return (e == cudaErrorMemoryAllocation) ? MCS_E_OUT_OF_MEMORY : MCS_E_CUDA;
+    if (e == cudaErrorMisalignedAddress)
+      g_create_error = "the allocator hook returned memory that is not 256-byte aligned";
+    return e == cudaErrorMemoryAllocation ? MCS_E_OUT_OF_MEMORY
+           : e == cudaErrorMisalignedAddress ? MCS_E_INVALID_ARG : MCS_E_CUDA;
   }
   *out = c;
   return MCS_OK;

@@ -179,6 +179,29 @@ def test_torch_allocator_hook_gives_identical_results():
         np.testing.assert_array_equal(st0[k], st1[k])
 
 
+def test_misaligned_allocator_is_refused():
+    """The hook must return 256-byte aligned blocks (like cudaMalloc): a misaligned one is handed
+    back through free and mcs_create fails with MCS_E_INVALID_ARG; nothing leaks."""
+    import torch
+    live = {}
+
+    def _alloc(nbytes, stream, user):
+        base = torch.cuda.caching_allocator_alloc(int(nbytes) + 256, 0, int(stream or 0))
+        live[base + 16] = base
+        return base + 16
+
+    def _free(ptr, stream, user):
+        torch.cuda.caching_allocator_delete(live.pop(int(ptr)))
+
+    fns = (mcs.ALLOC_FN(_alloc), mcs.FREE_FN(_free))
+    hook = mcs.Allocator(fns[0], fns[1], None)
+    s = synth.c1()
+    with pytest.raises(mcs.MCSError) as ei:
+        mcs.Context(s.N, 1, s.S, voxel_resolution=s.r, allocator=hook)
+    assert ei.value.status == 1 and "256-byte" in str(ei.value)  # MCS_E_INVALID_ARG
+    assert not live
+
+
 def test_get_pose_equals_get_particles_row():
     s = synth.c1()
     with _ctx(s) as ctx:
