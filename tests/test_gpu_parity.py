@@ -48,12 +48,26 @@ def pose_err(P, Q):
     return ang, np.linalg.norm(P[:, :, 3] - Q[:, :, 3], axis=1)
 
 
+def check_grad_rows(g_grad, o_grad, g_h21, o_h36):
+    """Gradient rows at G_RTOL (vector norm) and H at H_RTOL (Frobenius) where the oracle's row
+    is nonzero; where it is exactly zero (G empty: no old slot, R4) the GPU row must be exactly
+    zero as well, so a leak of non-G slots into g or H cannot hide behind a mask."""
+    nz = np.linalg.norm(o_grad, axis=1) > 0
+    assert np.all(rel_err(g_grad[nz], o_grad[nz], axis=1) <= G_RTOL)
+    assert not np.asarray(g_grad)[~nz].any(), "nonzero GPU gradient where the oracle's is 0"
+    Hg = mcs.unpack_h21(g_h21).reshape(-1, 36).astype(float)
+    Ho = np.asarray(o_h36).reshape(-1, 36)
+    hz = np.linalg.norm(Ho, axis=1) > 0
+    assert np.all(rel_err(Hg[hz], Ho[hz], axis=1) <= H_RTOL)
+    assert not Hg[~hz].any(), "nonzero GPU H where the oracle's is 0"
+
+
 def check_slots(g, o, S):
     """g: mcs_eval outputs; o: oracle slot outputs for the same particles."""
     np.testing.assert_array_equal(g["slot_kf"], o["slot_kf"])
     np.testing.assert_array_equal(g["slot_n"], o["slot_n"])
     lg, lo = g["slot_loglik"], o["slot_l"]
-    assert np.all(np.abs(lg - lo) <= L_RTOL * np.abs(lo) + 1e-6)
+    assert np.all(np.abs(lg - lo) <= L_RTOL * np.abs(lo))
     Hg = mcs.unpack_h21(g["slot_H21"]).astype(float)
     Ho = o["slot_H36"]
     active = o["slot_n"] > 0
