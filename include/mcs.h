@@ -167,7 +167,9 @@ MCS_API mcs_status  mcs_set_stream(mcs_ctx* ctx, void* cuda_stream);
  * in the keyframe's own sensor frame, and D_k, the cumulative odometry path length at the
  * keyframe (Eq.9 reading R14).  Builds the keyframe's voxel hash once (off the update
  * clock).  Every particle's new keyframe pose is its current pose: T_k^i := T_t^i (R24).
- * MCS_E_INVALID_ARG if a point's cell lies outside the 21-bit range or n < 1. */
+ * MCS_E_INVALID_ARG if a point's cell lies outside the 21-bit range, if the occupied cells'
+ * bounding box is wider than 2047 x 2048 x 1024 cells (the 32-bit bbox-local table keys: at
+ * r = 0.5 m that is 1023.5 x 1024 x 512 m), or if n < 1. */
 MCS_API mcs_status mcs_add_keyframe(mcs_ctx* ctx, const float* mean3, const float* cov6, int32_t n,
                             double path_length, int32_t* out_kf_id);
 
@@ -183,6 +185,12 @@ MCS_API mcs_status mcs_get_sizes(const mcs_ctx* ctx, int32_t* n_local, int32_t* 
  * the representative's without reading back the whole set.  MCS_E_INVALID_ARG if
  * index is outside [0, n_local). */
 MCS_API mcs_status mcs_get_pose(mcs_ctx* ctx, int32_t index, float* pose12);
+/* Collective over the ranks of a multi-GPU job (every rank calls it with the same index): the
+ * current pose of the particle with GLOBAL index global_index (e.g. mcs_update_out's
+ * representative) on every rank — the owning rank's pose reaches the others through one fp64
+ * all-reduce of 12 values.  On one device it equals mcs_get_pose.  MCS_E_INVALID_ARG if the
+ * index is outside [0, N_total). */
+MCS_API mcs_status mcs_get_global_pose(mcs_ctx* ctx, int64_t global_index, float* pose12);
 
 /* Outputs of one update; every pointer optional (NULL = not produced).  Per-particle rows are
  * indexed by LOCAL particle index.  loglik = l_i over ALL neighbour slots (Eq.2) minus the kappa
@@ -208,12 +216,22 @@ typedef struct {
  * sensor frame): a1 neighbours/relative poses, a2 likelihood+gradient sweep, a3 GN update,
  * a4 keyframe propagation, a5 weights, a6 pruning/respawn, a7 representative.
  * D_now = current cumulative odometry path length (R14); resample_u = the respawn uniform
- * u0 = resample_u / 2^32 (R18).  Synchronous; host or device pointers. */
+ * u0 = resample_u / 2^32 (R18).  Synchronous; host or device pointers.
+ * MCS_E_INVALID_ARG (before any state change) for a null or non-finite scan, a non-SPD scan
+ * covariance, n_pts < 1, or D_now below the newest keyframe's path length (the cumulative path
+ * length never decreases, R14).
+ * Precision (fp32 sweep, fp64 combine/solve): loglik within 1e-4 relative of the exact value
+ * for scans of >= 64 points; below that a single point's fp32 transform rounding (~1e-6 m at
+ * 10-20 m against centimetre residuals, ~1e-4 of e) is not averaged out and the bound is 2e-3.
+ * grad6 within 1e-3 (vector norm), poses within 1e-5 rad / 1e-5 m after one step. */
 MCS_API mcs_status mcs_update(mcs_ctx* ctx, const float* scan_mean3, const float* scan_cov6,
                       int32_t n_pts, double D_now, uint32_t resample_u,
                       const mcs_update_out* out);
 /* Same, stream-ordered on cuda_stream (NULL = context stream); DEVICE pointers only; the
- * scan is not validated (caller guarantees finite SPD covariances). */
+ * scan is not validated (caller guarantees finite SPD covariances).  On one device, and across
+ * ranks joined by NCCL with peer-direct migration, no step waits on the host: the call can be
+ * captured into the caller's CUDA graph (a host transport or the pack/send/recv fallback
+ * synchronises). */
 MCS_API mcs_status mcs_update_async(mcs_ctx* ctx, const float* d_scan_mean3, const float* d_scan_cov6,
                             int32_t n_pts, double D_now, uint32_t resample_u,
                             const mcs_update_out* d_out, void* cuda_stream);
@@ -227,8 +245,11 @@ MCS_API mcs_status mcs_eval(mcs_ctx* ctx, const float* scan_mean3, const float* 
                     int32_t* slot_n, int32_t* slot_kf, uint8_t* loop);
 
 /* Isolated respawn (a6) on given inputs, no state change: e[n] (fp64 exp(L - max L)),
- * dead[n] (0/1), uniform u -> donor[n] (-1 or donor index).  Bit-exact contract with the
- * oracle's integer-ladder systematic resampler (R18).  Single-device only. */
+ * dead[n] (0 = survivor, nonzero = dead), uniform u -> donor[n] (-1 or donor index).
+ * Domain: every e_i finite in [0, 1] (e = exp(L - max L)); otherwise MCS_E_INVALID_ARG.  Within
+ * it the result is bit-exact with the oracle's integer-ladder systematic resampler (R18) for
+ * any e, including survivors whose rung floor(e 2^32) is 0 (they never donate);
+ * MCS_E_DEGENERATE when some particle is dead and every rung is 0.  Single-device. */
 MCS_API mcs_status mcs_resample(mcs_ctx* ctx, const double* e, const uint8_t* dead, int32_t n,
                         uint32_t u, int32_t* donor_out);
 
@@ -289,6 +310,9 @@ MCS_API mcs_status mcs_get_phase_ms(const mcs_ctx* ctx, float* ms5);
  * kernel writes clones into other ranks' memory), -1 packed + NCCL / transport exchange,
  * 0 not decided yet (no respawn so far, or world_size 1 without an exchange path). */
 MCS_API int32_t mcs_peer_migration_state(const mcs_ctx* ctx);
+/* 1 if the library holds a captured CUDA graph of the update body (mcs_config.graph_replay and
+ * a device-resident exchange path: one device, or NCCL with peer-direct migration), else 0. */
+MCS_API int32_t mcs_graph_state(const mcs_ctx* ctx);
 
 #ifdef __cplusplus
 }

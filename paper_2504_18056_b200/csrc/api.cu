@@ -109,6 +109,17 @@ __global__ void validate_gauss_kernel(const float* __restrict__ mean3,
   if (!ok) atomicAdd(bad, 1);
 }
 
+__global__ void pose_column_kernel(const float* __restrict__ pose, int capN, int i,
+                                   double* __restrict__ out) {
+  const int k = threadIdx.x;
+  if (k < 12) out[k] = i >= 0 ? (double)pose[(size_t)k * capN + i] : 0.0;
+}
+
+__global__ void validate_unit_kernel(const double* __restrict__ e, int n, int* bad) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n && !(e[i] >= 0.0 && e[i] <= 1.0)) atomicAdd(bad, 1);  // NaN fails both
+}
+
 __global__ void fill_double_kernel(double* __restrict__ p, int n, double v) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) p[i] = v;
@@ -130,7 +141,7 @@ __global__ void gather_outputs_kernel(OutPtrs o, int N, int capN, const double* 
                                       const float* __restrict__ grad,
                                       const float* __restrict__ hess,
                                       const double* __restrict__ psi,
-                                      const double* __restrict__ w,
+                                      const double* __restrict__ e,
                                       const int32_t* __restrict__ donor,
                                       const uint8_t* __restrict__ flags, const Scalars* sc) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -146,7 +157,7 @@ __global__ void gather_outputs_kernel(OutPtrs o, int N, int capN, const double* 
     for (int k = 0; k < 21; ++k) o.hess21[(size_t)i * 21 + k] = hess[(size_t)k * capN + i];
   if (o.psi6)
     for (int k = 0; k < 6; ++k) o.psi6[(size_t)i * 6 + k] = (float)psi[(size_t)k * capN + i];
-  if (o.weight) o.weight[i] = w[i];
+  if (o.weight) o.weight[i] = e[i] / sc->S2;  // w = e' / S' (weights.cu)
   if (o.donor) o.donor[i] = donor[i];
   if (o.flags) o.flags[i] = flags[i];
 }
@@ -210,8 +221,8 @@ static void free_all(mcs_ctx* c) {
   void* ptrs[] = {c->d_kf_meta, c->d_D,       c->d_pose,     c->d_kfpose,   c->d_L,
                   c->d_snapshot, c->d_scan_raw, c->d_scan,    c->d_items,    c->d_order,
                   c->d_part,    c->d_meta,    c->d_to,       c->d_l,        c->d_psi,
-                  c->d_grad,    c->d_hess,    c->d_flags,    c->d_e,        c->d_w,
-                  c->d_ladder,  c->d_ladder_scan, c->d_ncum, c->d_donor,    c->d_partials,
+                  c->d_grad,    c->d_hess,    c->d_flags,    c->d_e,        c->d_xg,
+                  c->d_ladder,  c->d_ladder_scan, c->d_donor,    c->d_partials,
                   c->d_ipartials, c->d_scal,  c->d_cub_temp, c->d_skeys, c->d_skeys_out,
                   c->d_sids,    c->d_stage,   c->d_bad,      c->d_dead_list, c->d_donor_g,
                   c->d_plan,    c->d_pack_src, c->d_send,    c->d_recv};
@@ -400,10 +411,11 @@ mcs_status mcs_create(const mcs_config* cfg, mcs_ctx** out) {
   if (e == cudaSuccess) e = dalloc(c, &c->d_hess, 21 * N);
   if (e == cudaSuccess) e = dalloc(c, &c->d_flags, N);
   if (e == cudaSuccess) e = dalloc(c, &c->d_e, N);
-  if (e == cudaSuccess) e = dalloc(c, &c->d_w, N);
+  if (e == cudaSuccess) e = dalloc(c, &c->d_xg, 32 * (size_t)(cfg->world_size + 1) + 96);
   if (e == cudaSuccess) e = mem_alloc(c, &c->d_ladder, 16 * N);
-  if (e == cudaSuccess) e = mem_alloc(c, &c->d_ladder_scan, 16 * N);
-  if (e == cudaSuccess) e = dalloc(c, &c->d_ncum, N);
+  // look-back tile flags carry a launch epoch; zero memory matches no published tile
+  if (e == cudaSuccess) e = cudaMemset(c->d_ladder, 0, 16 * N);
+  if (e == cudaSuccess) e = mem_alloc(c, &c->d_ladder_scan, 8 * N);
   if (e == cudaSuccess) e = dalloc(c, &c->d_donor, N);
   if (e == cudaSuccess) e = dalloc(c, &c->d_partials, 2 * maxb);
   if (e == cudaSuccess) e = dalloc(c, &c->d_ipartials, 2 * maxb);
@@ -411,7 +423,7 @@ mcs_status mcs_create(const mcs_config* cfg, mcs_ctx** out) {
   if (e == cudaSuccess) e = cudaMemset(c->d_scal, 0, sizeof(Scalars));
   if (e == cudaSuccess) e = cudaMallocHost((void**)&c->h_scal, sizeof(Scalars));
   if (e == cudaSuccess) {
-    c->cub_temp_bytes = std::max(cub_temp_needed((int)N), sort_temp_needed((int)(nb * N), (int)K));
+    c->cub_temp_bytes = sort_temp_needed((int)(nb * N), (int)K);
     e = mem_alloc(c, &c->d_cub_temp, c->cub_temp_bytes);
   }
   for (int k = 0; k < 6 && e == cudaSuccess; ++k) e = cudaEventCreate(&c->ev[k]);
@@ -587,7 +599,7 @@ mcs_status mcs_set_particles(mcs_ctx* ctx, int32_t n, const float* pose12,
   } else {
     CUDA_TRY(ctx, cudaMemsetAsync(ctx->d_L, 0, sizeof(double) * n, st));
   }
-  fill_double_kernel<<<(n + 255) / 256, 256, 0, st>>>(ctx->d_w, n, 1.0 / n);
+  fill_double_kernel<<<(n + 255) / 256, 256, 0, st>>>(ctx->d_e, n, 1.0);  // w = 1 / N_total
   CUDA_TRY(ctx, cudaGetLastError());
   mem_free_async(ctx, tp, st);
   if (tk) mem_free_async(ctx, tk, st);
@@ -616,6 +628,11 @@ mcs_status mcs_set_particles(mcs_ctx* ctx, int32_t n, const float* pose12,
   }
   ctx->gbase = 0;
   for (int g = 0; g < ctx->rank; ++g) ctx->gbase += ctx->n_per_rank[g];
+  double n_total = 0.0;  // uniform initial weights over the particles of every rank
+  for (int g = 0; g < ctx->world; ++g) n_total += (double)ctx->n_per_rank[g];
+  CUDA_TRY(ctx, cudaMemcpyAsync(&ctx->d_scal->S2, &n_total, sizeof(double),
+                                cudaMemcpyHostToDevice, st));
+  CUDA_TRY(ctx, cudaStreamSynchronize(st));
   return MCS_OK;
 }
 
@@ -638,8 +655,13 @@ mcs_status mcs_get_particles(mcs_ctx* ctx, float* pose12, float* kf_pose12, doub
                                     cudaMemcpyDefault, st));
   if (cum_loglik)
     CUDA_TRY(ctx, cudaMemcpyAsync(cum_loglik, ctx->d_L, sizeof(double) * n, cudaMemcpyDefault, st));
-  if (weight)
-    CUDA_TRY(ctx, cudaMemcpyAsync(weight, ctx->d_w, sizeof(double) * n, cudaMemcpyDefault, st));
+  if (weight) {
+    double* tw = nullptr;
+    CUDA_TRY(ctx, mem_alloc_async(ctx, (void**)&tw, sizeof(double) * n, st));
+    launch_weights_out(ctx, tw);
+    CUDA_TRY(ctx, cudaMemcpyAsync(weight, tw, sizeof(double) * n, cudaMemcpyDefault, st));
+    mem_free_async(ctx, tw, st);
+  }
   CUDA_TRY(ctx, cudaStreamSynchronize(st));
   return MCS_OK;
 }
@@ -653,6 +675,29 @@ mcs_status mcs_get_pose(mcs_ctx* ctx, int32_t index, float* pose12) {
                                   sizeof(float) * ctx->capN, sizeof(float), 12, cudaMemcpyDefault,
                                   ctx->stream));
   CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  return MCS_OK;
+}
+
+mcs_status mcs_get_global_pose(mcs_ctx* ctx, int64_t global_index, float* pose12) {
+  CHECK_CTX(ctx);
+  long long n_total = 0;
+  for (long long v : ctx->n_per_rank) n_total += v;
+  if (!pose12 || global_index < 0 || global_index >= n_total)
+    FAIL(ctx, MCS_E_INVALID_ARG, "mcs_get_global_pose: index %lld outside [0, %lld)",
+         (long long)global_index, n_total);
+  cudaStream_t st = ctx->stream;
+  double* d = reinterpret_cast<double*>(ctx->d_xg) + 4 * (ctx->world + 1);  // 12 doubles
+  const long long li = global_index - ctx->gbase;
+  const int owner = li >= 0 && li < ctx->N;
+  pose_column_kernel<<<1, 12, 0, st>>>(ctx->d_pose, ctx->capN, owner ? (int)li : -1, d);
+  const mcs_status s = dist_allreduce_f64(ctx, d, 12, 0);  // exactly one rank is nonzero
+  if (s != MCS_OK) FAIL(ctx, s, "mcs_get_global_pose: all-reduce failed");
+  double h[12];
+  CUDA_TRY(ctx, cudaMemcpyAsync(h, d, sizeof(h), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(ctx, cudaStreamSynchronize(st));
+  float f[12];
+  for (int k = 0; k < 12; ++k) f[k] = (float)h[k];  // fp32 values: exact round trip
+  CUDA_TRY(ctx, cudaMemcpy(pose12, f, sizeof(f), cudaMemcpyDefault));
   return MCS_OK;
 }
 
@@ -678,6 +723,9 @@ static mcs_status check_update_args(mcs_ctx* ctx, const void* m, const void* c, 
   if (n_pts < 1) FAIL(ctx, MCS_E_INVALID_ARG, "n_pts < 1");
   if (n_pts > ctx->capS) FAIL(ctx, MCS_E_CAPACITY, "n_pts > capacity_scan_points");
   if (!std::isfinite(D_now)) FAIL(ctx, MCS_E_INVALID_ARG, "D_now not finite");
+  if (!ctx->D.empty() && D_now < ctx->D.back())  // cumulative path length never decreases (R14)
+    FAIL(ctx, MCS_E_INVALID_ARG, "D_now (%g) < the newest keyframe's path length (%g)", D_now,
+         ctx->D.back());
   return MCS_OK;
 }
 
@@ -720,8 +768,13 @@ static mcs_status run_update(mcs_ctx* ctx, int n_pts, double D_now, uint32_t U) 
   launch_set_params(ctx, D_now, U);
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
   cudaStreamIsCapturing(ctx->stream, &cap);
+  // multi-rank: the peer views are exchanged (collectively, with host steps) before any capture
+  if (dist_active(ctx) && ctx->p2p == 0) {
+    const mcs_status ps = dist_peer_setup(ctx);
+    if (ps != MCS_OK) return ps;
+  }
   const bool graph = ctx->cfg.graph_replay && !ctx->graph_off && !ctx->profiling &&
-                     !dist_active(ctx) && cap == cudaStreamCaptureStatusNone;
+                     weights_device_resident(ctx) && cap == cudaStreamCaptureStatusNone;
   if (!graph) return run_update_body(ctx, n_pts, U);
   const long long key[4] = {n_pts, ctx->N, ctx->K, 0};
   if (!ctx->gexec || memcmp(key, ctx->gkey, sizeof(key)) != 0) {
@@ -783,7 +836,7 @@ mcs_status mcs_update(mcs_ctx* ctx, const float* scan_mean3, const float* scan_c
     if (out->donor) o.donor = (int32_t*)(stage + lay.d);
     if (out->flags) o.flags = (uint8_t*)(stage + lay.f);
     gather_outputs_kernel<<<(N + 255) / 256, 256, 0, st>>>(
-        o, N, ctx->capN, ctx->d_l, ctx->d_grad, ctx->d_hess, ctx->d_psi, ctx->d_w, ctx->d_donor_g,
+        o, N, ctx->capN, ctx->d_l, ctx->d_grad, ctx->d_hess, ctx->d_psi, ctx->d_e, ctx->d_donor_g,
         ctx->d_flags, ctx->d_scal);
     if (out->loglik) CUDA_TRY(ctx, cudaMemcpyAsync(out->loglik, o.loglik, 8 * N, cudaMemcpyDefault, st));
     if (out->grad6) CUDA_TRY(ctx, cudaMemcpyAsync(out->grad6, o.grad6, 24 * N, cudaMemcpyDefault, st));
@@ -822,7 +875,7 @@ mcs_status mcs_update_async(mcs_ctx* ctx, const float* d_scan_mean3, const float
     OutPtrs o{d_out->loglik, d_out->grad6,  d_out->hess21,         d_out->psi6,  d_out->weight,
               d_out->donor,  d_out->flags,  d_out->representative, d_out->n_dead};
     gather_outputs_kernel<<<(ctx->N + 255) / 256, 256, 0, ctx->stream>>>(
-        o, ctx->N, ctx->capN, ctx->d_l, ctx->d_grad, ctx->d_hess, ctx->d_psi, ctx->d_w,
+        o, ctx->N, ctx->capN, ctx->d_l, ctx->d_grad, ctx->d_hess, ctx->d_psi, ctx->d_e,
         ctx->d_donor_g, ctx->d_flags, ctx->d_scal);
   }
   cudaError_t e = cudaGetLastError();
@@ -835,7 +888,8 @@ mcs_status mcs_eval(mcs_ctx* ctx, const float* scan_mean3, const float* scan_cov
                     double* slot_loglik, float* slot_H21, float* slot_b6, int32_t* slot_n,
                     int32_t* slot_kf, uint8_t* loop) {
   CHECK_CTX(ctx);
-  mcs_status s = check_update_args(ctx, scan_mean3, scan_cov6, n_pts, 0.0);
+  mcs_status s = check_update_args(ctx, scan_mean3, scan_cov6, n_pts,
+                                   ctx->D.empty() ? 0.0 : ctx->D.back());  // no D_now in eval
   if (s != MCS_OK) return s;
   cudaStream_t st = ctx->stream;
   float* raw_m = ctx->d_scan_raw;
@@ -884,6 +938,19 @@ mcs_status mcs_resample(mcs_ctx* ctx, const double* e, const uint8_t* dead, int3
   CUDA_TRY(ctx, mem_alloc_async(ctx, (void**)&de, 8 * (size_t)n, st));
   CUDA_TRY(ctx, to_device(dd, dead, n, st));
   CUDA_TRY(ctx, to_device(de, e, 8 * (size_t)n, st));
+  // domain of the exact ladder (R18): 0 <= e_i <= 1 (e = exp(L - max L)), so every rung
+  // floor(e 2^32) and the N-term prefix sums are exact uint64
+  CUDA_TRY(ctx, cudaMemsetAsync(ctx->d_bad, 0, sizeof(int), st));
+  validate_unit_kernel<<<(n + 255) / 256, 256, 0, st>>>(de, n, ctx->d_bad);
+  CUDA_TRY(ctx, cudaMemcpyAsync(&ctx->h_scal->status, ctx->d_bad, sizeof(int),
+                                cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(ctx, cudaStreamSynchronize(st));
+  if (ctx->h_scal->status) {
+    const int nb = ctx->h_scal->status;
+    mem_free_async(ctx, dd, st);
+    mem_free_async(ctx, de, st);
+    FAIL(ctx, MCS_E_INVALID_ARG, "mcs_resample: %d values of e outside [0, 1] or not finite", nb);
+  }
   int32_t* ddon = nullptr;
   CUDA_TRY(ctx, mem_alloc_async(ctx, (void**)&ddon, 4 * (size_t)n, st));
   if (launch_resample_only(ctx, de, dd, n, u, ddon) != MCS_OK) CUDA_TRY(ctx, cudaGetLastError());
@@ -939,7 +1006,7 @@ mcs_status mcs_overlap(mcs_ctx* ctx, const float* scan_mean3, int32_t n_pts, con
   char* d = nullptr;
   const size_t bm = (sizeof(float) * 3 * (size_t)n_pts + 255) & ~(size_t)255;  // keep alignment
   CUDA_TRY(ctx, mem_alloc_async(ctx, (void**)&d, bm + 64 + 8, st));
-  CUDA_TRY(ctx, to_device(d, scan_mean3, bm, st));
+  CUDA_TRY(ctx, to_device(d, scan_mean3, sizeof(float) * 3 * (size_t)n_pts, st));
   CUDA_TRY(ctx, to_device(d + bm, rel12, 48, st));
   unsigned long long cnt = 0;
   const mcs_status s = launch_overlap(ctx, (const float*)d, n_pts, (const float*)(d + bm), kf,
@@ -986,6 +1053,7 @@ mcs_status mcs_set_profiling(mcs_ctx* ctx, int32_t enable) {
 }
 
 int32_t mcs_peer_migration_state(const mcs_ctx* ctx) { return ctx ? ctx->p2p : 0; }
+int32_t mcs_graph_state(const mcs_ctx* ctx) { return ctx && ctx->gexec ? 1 : 0; }
 
 mcs_status mcs_get_phase_ms(const mcs_ctx* ctx, float* ms5) {
   if (!ctx || !ms5) return MCS_E_INVALID_ARG;

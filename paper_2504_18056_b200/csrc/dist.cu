@@ -365,6 +365,30 @@ mcs_status dist_allgather_host(mcs_ctx* c, const void* send, void* recv, size_t 
   return c->tr->allgather(c->tr->user, c->rank, send, recv, bytes) ? MCS_E_NCCL : MCS_OK;
 }
 
+mcs_status dist_allgather_dev(mcs_ctx* c, const void* d_send, void* d_recv, size_t bytes) {
+  if (!dist_active(c)) {
+    return cudaMemcpyAsync(d_recv, d_send, bytes, cudaMemcpyDeviceToDevice, c->stream) ==
+                   cudaSuccess ? MCS_OK : MCS_E_CUDA;
+  }
+  if (c->nccl_comm) {
+    NcclApi* a = nccl();
+    return a->AllGather(d_send, d_recv, bytes, kNcclUint8, c->nccl_comm, c->stream) == 0
+               ? MCS_OK : MCS_E_NCCL;
+  }
+  const size_t tot = bytes * (c->world + 1);
+  if (stage(c, tot) != MCS_OK) return MCS_E_OUT_OF_MEMORY;
+  char* h = (char*)c->h_stage;
+  if (cudaMemcpyAsync(h, d_send, bytes, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess ||
+      cudaStreamSynchronize(c->stream) != cudaSuccess)
+    return MCS_E_CUDA;
+  if (c->tr->allgather(c->tr->user, c->rank, h, h + bytes, bytes)) return MCS_E_NCCL;
+  if (cudaMemcpyAsync(d_recv, h + bytes, bytes * c->world, cudaMemcpyHostToDevice, c->stream) !=
+          cudaSuccess ||
+      cudaStreamSynchronize(c->stream) != cudaSuccess)
+    return MCS_E_CUDA;
+  return MCS_OK;
+}
+
 mcs_status dist_barrier(mcs_ctx* c) {
   if (!dist_active(c)) return MCS_OK;
   if (c->nccl_comm) {  // a 1-element allreduce: later work on this stream waits for every rank

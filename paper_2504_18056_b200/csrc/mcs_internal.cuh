@@ -116,6 +116,8 @@ struct Scalars {                // device-side reduction results of one update
   unsigned int counter[8];      // last-block counters (reset by the last block)
   double D_now;                 // per-update parameters, written by set_params_kernel before
   unsigned int U;               // the update body (so a captured CUDA graph can be replayed)
+  unsigned int tile_ctr;        // ladder scan: next tile to hand out (reset by the last block)
+  unsigned int epoch;           // ladder scan: launch epoch tagging the look-back tile flags
 };
 
 }  // namespace mcs
@@ -163,11 +165,11 @@ struct mcs_ctx {
   float* d_grad = nullptr;      // [6][Ncap]
   float* d_hess = nullptr;      // [21][Ncap]
   uint8_t* d_flags = nullptr;   // [Ncap]
-  double* d_e = nullptr;        // [Ncap]
-  double* d_w = nullptr;        // [Ncap]
-  void* d_ladder = nullptr;     // [Ncap] {u64 C, u32 dead}
-  void* d_ladder_scan = nullptr;
-  long long* d_ncum = nullptr;  // [Ncap]
+  double* d_e = nullptr;        // [Ncap] e_i, then e'_i after the respawn: w_i = e'_i / S'
+  char* d_xg = nullptr;         // [4][world+1] x 8 B: device allgathers (Q_g, D_g), (e'_g, rep_g),
+                                // then 12 doubles: the all-reduced pose of mcs_get_global_pose
+  void* d_ladder = nullptr;     // [Ncap] 16-B look-back tile states of the ladder scan (zeroed)
+  void* d_ladder_scan = nullptr;  // [Ncap] u64 inclusive survivor ladder C_i
   int32_t* d_donor = nullptr;   // [Ncap]
   double* d_partials = nullptr; // [4][max_blocks]
   int32_t* d_ipartials = nullptr;
@@ -250,7 +252,11 @@ mcs_status launch_weights_resample(mcs_ctx* c, uint32_t U);
 // isolated respawn on caller arrays (single device)
 mcs_status launch_resample_only(mcs_ctx* c, const double* d_e, const uint8_t* d_dead, int n,
                                 uint32_t U, int32_t* d_donor);
-size_t cub_temp_needed(int n);
+// true when a5-a7 need no host round trip (one device, or NCCL with peer-direct migration):
+// the update body can then be captured into a CUDA graph
+bool weights_device_resident(const mcs_ctx* c);
+// w = e' / S' into d_w (N doubles)
+void launch_weights_out(mcs_ctx* c, double* d_w);
 
 // A rank's particle state as another rank writes it (peer-direct migration).
 struct PeerView {
@@ -273,6 +279,8 @@ mcs_status dist_peer_setup(mcs_ctx* c);
 void dist_destroy(mcs_ctx* c);
 // in place on device doubles; op 0 = sum, 1 = max (stream-ordered; host transport syncs)
 mcs_status dist_allreduce_f64(mcs_ctx* c, double* d_buf, int n, int op);
+// device buffers gathered on the device (NCCL: stream-ordered; host transport: staged, syncs)
+mcs_status dist_allgather_dev(mcs_ctx* c, const void* d_send, void* d_recv, size_t bytes);
 // host values gathered to host (small, synchronous)
 mcs_status dist_allgather_host(mcs_ctx* c, const void* send, void* recv, size_t bytes);
 // device buffers; byte counts per peer on the host

@@ -151,6 +151,8 @@ def load() -> C.CDLL:
         "mcs_inproc_transport_destroy": (None, [vp]),
         "mcs_plan_migration": (st, [i32, vp, vp, vp]),
         "mcs_peer_migration_state": (i32, [vp]),
+        "mcs_graph_state": (i32, [vp]),
+        "mcs_get_global_pose": (i32, [vp, C.c_int64, vp]),
         "mcs_get_pose": (st, [vp, i32, vp]),
         "mcs_config_size": (C.c_size_t, []),
     }
@@ -292,6 +294,18 @@ class Context:
     def peer_migration_state(self) -> int:
         """1 peer-direct migration, -1 packed exchange, 0 not decided yet."""
         return int(self._lib.mcs_peer_migration_state(self._ctx))
+
+    def get_global_pose(self, global_index: int) -> np.ndarray:
+        """Collective over ranks: the pose (12,) of the particle with this GLOBAL index, e.g.
+        the update's representative, on every rank (mcs_get_global_pose)."""
+        p = np.zeros(12, np.float32)
+        self._check(self._lib.mcs_get_global_pose(self._ctx, int(global_index), p.ctypes.data))
+        return p
+
+    @property
+    def graph_captured(self) -> bool:
+        """True when the library replays a captured CUDA graph of the update body."""
+        return bool(self._lib.mcs_graph_state(self._ctx))
 
     def get_pose(self, index: int) -> np.ndarray:
         """One local particle's current pose (12,) fp32 [R|t] row-major (mcs_get_pose)."""

@@ -113,9 +113,10 @@ class MonteCarloSLAM:
             self.K += 1
             out["inserted"] = True
         # (4) representative
+        # the representative is a GLOBAL index: its owner's pose reaches every rank (collective)
         rep = out["update"]["representative"] if out["update"] is not None else 0
         out["representative"] = int(rep)
-        out["pose"] = _to44(self.ctx.get_pose(rep)) if 0 <= rep < self.N else None
+        out["pose"] = _to44(self.ctx.get_global_pose(rep))
         if state:
             out["state"] = self.ctx.get_particles()
         return out

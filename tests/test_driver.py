@@ -109,3 +109,52 @@ def test_driver_closes_the_loop_of_a_drifting_lap():
     print(f"keyframes {K}, odometry error {odo:.2f} m, representative error {errs[-1]:.2f} m")
     assert odo > 0.8                    # the odometry drifted (1.10 m with these seeds)
     assert errs[-1] < 0.5 * odo and errs[-1] < 0.5
+
+
+@pytest.mark.gpu
+def test_two_rank_driver_equals_one_rank():
+    """The driver on two particle shards (two contexts joined by the in-process transport, one
+    host thread per rank): the representative is a GLOBAL index and every rank reads its pose
+    through the collective mcs_get_global_pose; frame by frame it equals the one-rank driver."""
+    import threading
+
+    import paper_2504_18056_b200 as mcs
+    tr = _traj(8, 512, 0.02, 0.002)
+    N = 256
+    init_cov = np.diag([0.1 ** 2] * 3 + [0.01 ** 2] * 3)
+
+    def run(world, rank, n, transport, sink):
+        kw = dict(voxel_resolution=tr.r, loop_recency_gap=tr.gap)
+        if world > 1:
+            kw.update(world_size=world, rank=rank, transport=transport)
+        out = []
+        with mcs.MonteCarloSLAM(n, 16, 512, init_pose=tr.gt[0], init_cov=init_cov, seed=7,
+                                **kw) as g:
+            for k in range(tr.F):
+                r = g.step(*tr.scans[k], tr.odom[k], tr.odom_cov, tr.D[k], U=int(tr.U[k]),
+                           cloud=tr.clouds[k])
+                out.append((r["inserted"], r["representative"], r["pose"]))
+        sink[rank] = out
+
+    one = {}
+    run(1, 0, N, None, one)
+    tp = mcs.InprocTransport(2)
+    two, errors = {}, []
+
+    def worker(rank):
+        try:
+            run(2, rank, N // 2, tp, two)
+        except Exception as e:  # pragma: no cover - surfaced below
+            errors.append(repr(e))
+
+    th = [threading.Thread(target=worker, args=(r,)) for r in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(600)
+    assert not errors, errors
+    for k in range(tr.F):
+        for rank in range(2):
+            ins, rep, pose = two[rank][k]
+            assert ins == one[0][k][0] and rep == one[0][k][1], (k, rank)
+            np.testing.assert_array_equal(pose, one[0][k][2])

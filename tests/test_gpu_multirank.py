@@ -123,3 +123,71 @@ def test_exchange_path_with_one_rank_matches_plain():
         b.update(ctx.get_particles())
     for k in ("loglik", "weight", "donor", "flags", "pose12", "kf_pose12", "L"):
         assert np.array_equal(b[k], plain[k]), k
+
+
+def test_nccl_exchange_path_is_graph_captured():
+    """With NCCL (here a 1-rank communicator: gpurun gives one GPU) and peer-direct migration
+    the exchange steps are device-resident: the library captures the whole update, the
+    collectives included, into its CUDA graph, and the caller can capture mcs_update_async into
+    its own graph; both replay bitwise equal to kernel-by-kernel updates."""
+    import torch
+    s = synth.c1()
+    try:
+        nid = mcs.nccl_unique_id()
+    except mcs.MCSError:
+        pytest.skip("libnccl.so.2 not loadable")
+    runs = {}
+    for gr in (0, 1):
+        with mcs.Context(s.N, s.K, s.S, loop_recency_gap=s.gap, voxel_resolution=s.r,
+                         nccl_unique_id=mcs.nccl_unique_id(), graph_replay=gr) as ctx:
+            for (m3, c6), d in zip(s.keyframes, s.D):
+                ctx.add_keyframe(m3, c6, d)
+            ctx.set_particles(s.pose12, s.kf_pose12)
+            outs = [ctx.update(s.scan_mean3, s.scan_cov6, s.D_now + 0.1 * k,
+                               (s.U + 977 * k) & 0xFFFFFFFF) for k in range(3)]
+            outs.append(ctx.get_particles())
+            assert ctx.peer_migration_state == 1
+            assert ctx.graph_captured == bool(gr)
+        runs[gr] = outs
+    for a, b in zip(runs[0], runs[1]):
+        for k in a:
+            assert np.array_equal(np.asarray(a[k]), np.asarray(b[k])), k
+    dev = torch.device("cuda", 0)
+    ctx = mcs.Context(s.N, s.K, s.S, loop_recency_gap=s.gap, voxel_resolution=s.r,
+                      nccl_unique_id=nid, graph_replay=0)
+    for (m3, c6), d in zip(s.keyframes, s.D):
+        ctx.add_keyframe(m3, c6, d)
+    ctx.set_particles(s.pose12, s.kf_pose12)
+    ctx.snapshot()
+    d_m = torch.from_numpy(s.scan_mean3).to(dev)
+    d_c = torch.from_numpy(s.scan_cov6).to(dev)
+    out = {"loglik": torch.zeros(s.N, dtype=torch.float64, device=dev),
+           "weight": torch.zeros(s.N, dtype=torch.float64, device=dev),
+           "donor": torch.zeros(s.N, dtype=torch.int32, device=dev),
+           "representative": torch.zeros(1, dtype=torch.int32, device=dev),
+           "n_dead": torch.zeros(1, dtype=torch.int64, device=dev)}
+    stream = torch.cuda.Stream(device=dev)
+    ctx.set_stream(stream)
+    with torch.cuda.stream(stream):
+        ctx.update_async(d_m, d_c, s.D_now, s.U, out, stream=stream)
+    torch.cuda.synchronize()
+    eager = {k: v.clone() for k, v in out.items()}
+    eager_state = ctx.get_particles()
+    g = torch.cuda.CUDAGraph()
+    ctx.restore()
+    torch.cuda.synchronize()
+    with torch.cuda.graph(g, stream=stream, capture_error_mode="thread_local"):
+        ctx.update_async(d_m, d_c, s.D_now, s.U, out, stream=stream)
+    for _ in range(2):
+        ctx.restore()
+        torch.cuda.synchronize()
+        for v in out.values():
+            v.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        for k in out:
+            assert torch.equal(out[k], eager[k]), k
+        st = ctx.get_particles()
+        for k in ("pose12", "kf_pose12", "L"):
+            np.testing.assert_array_equal(st[k], eager_state[k])
+    ctx.close()

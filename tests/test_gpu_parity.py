@@ -197,10 +197,26 @@ def test_resample_bit_exact_random():
             e[g.integers(0, N)] = 1.0
             dead = (g.random(N) < g.uniform(0, 0.999)).astype(np.uint8)
             dead[np.argmax(e)] = 0
-            # domain of the respawn (R18): survivors have w >= 1e-8, hence e >= 1e-8
-            e[dead == 0] = np.maximum(e[dead == 0], 1e-8)
+            # the whole domain [0, 1]: zero rungs (e < 2^-32), exact zeros, tiny and unit e
+            k = g.integers(0, N, max(1, N // 10))
+            e[k] = g.choice([0.0, 2.0**-33, 1e-12, 2.0**-32, 1e-8, 1.0], len(k))
             U = int(g.integers(0, 2**32))
             np.testing.assert_array_equal(ctx.resample(e, dead, U), oracle.resample(e, dead, U))
+
+
+def test_resample_rejects_values_outside_the_domain():
+    """mcs_resample's domain is 0 <= e <= 1 (e = exp(L - max L)): anything else is refused
+    before any work, so the bit-exact contract holds wherever the call succeeds."""
+    with mcs.Context(16, 1, 1) as ctx:
+        dead = np.zeros(4, np.uint8)
+        dead[3] = 1
+        for bad in (1.5, -1e-300, np.nan, np.inf):
+            e = np.array([1.0, 0.5, bad, 0.25])
+            with pytest.raises(mcs.MCSError) as ei:
+                ctx.resample(e, dead, 7)
+            assert ei.value.status == 1
+        e = np.array([1.0, 0.0, 2.0**-40, 0.5])  # zero rungs are inside the domain
+        np.testing.assert_array_equal(ctx.resample(e, dead, 7), oracle.resample(e, dead, 7))
 
 
 def test_resample_exact_boundaries():
@@ -321,6 +337,20 @@ def test_errors_before_state_change(c1):
         assert ei.value.status == 1
         after = ctx.get_particles()
         assert np.array_equal(before["pose12"], after["pose12"])
+
+
+def test_path_length_below_newest_keyframe_is_rejected(c1):
+    """R14: D is a cumulative path length, so D_now below the newest keyframe's D_k is an
+    argument error, reported before any state change."""
+    s = c1
+    with make_ctx(s) as ctx:
+        before = ctx.get_particles()
+        with pytest.raises(mcs.MCSError) as ei:
+            ctx.update(s.scan_mean3, s.scan_cov6, float(s.D[-1]) - 0.5, s.U)
+        assert ei.value.status == 1
+        after = ctx.get_particles()
+        for k in ("pose12", "kf_pose12", "L"):
+            assert np.array_equal(before[k], after[k]), k
 
 
 def test_all_dead_is_degenerate(c1):
