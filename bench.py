@@ -35,7 +35,9 @@ FLOPS_MATCHED = 236.0    # FP32 flops per matched (particle, point, slot) with H
 FLOPS_UNMATCHED = 21.0   # transform + key for an unmatched triple
 GATHER_MATCHED = 56.0    # bytes: 8-B key probe + 48-B payload
 GATHER_UNMATCHED = 8.0
-LAUNCHES_PER_UPDATE = 26  # kernels per mcs_update_async incl. CUB sort/scan + set_params (profiles/r01_launches.csv)
+LAUNCHES_PER_UPDATE = 18  # kernels per mcs_update_async: set_params, prepare_scan, select, 7 CUB
+#                           sort kernels, sweep, combine, propagate, exp_sum, ladder, draws,
+#                           renorm, gather_outputs (profiles/r02_launches.csv)
 
 
 def dist_env():
@@ -143,9 +145,37 @@ def committed_traffic():
     return None
 
 
-def make_scene(particles: int, seed: int = 0):
+CONFIGS = {
+    # name: (generator, particles, workload text)
+    "c2": ("c2", 100_000, "C2: {N} particles x 4096-pt LiDAR-like scan vs 20 keyframes (loop "
+                          "corridor, r = 0.5 m, 3 neighbours, every particle loops)"),
+    "c4": ("c4", 1_000_000, "C4: {N} particles x 8192-pt LiDAR-like scan vs 20 keyframes (the C2 "
+                            "scene, r = 0.5 m, 3 neighbours)"),
+    # C2 with the particles 200x closer to the truth (1 mm, 0.1 mrad; per-particle keyframe
+    # drift 0.1 mm / 0.01 mrad per keyframe): their likelihoods differ by units, not thousands,
+    # so about a third die under P:190's floors and a6 clones a realistic share (the headline
+    # C2 collapses to one survivor)
+    "c2_survival": ("c2_survival", 100_000,
+                    "C2 survival variant: {N} particles at 1 mm / 0.1 mrad spread (keyframe "
+                    "drift 0.1 mm / 0.01 mrad) x 4096-pt scan vs 20 keyframes"),
+}
+
+
+def make_scene(config: str, particles: int, seed: int = 0):
     import synth
+    if config == "c4":
+        return synth.c4(seed=seed, N=particles)
+    if config == "c2_survival":
+        return synth.c2(seed=seed, N=particles, sig_t=1e-3, sig_r=1e-4, drift_t=1e-4,
+                        drift_r=1e-5)
     return synth.c2(seed=seed, N=particles)
+
+
+def shard(s, lo: int, hi: int):
+    """Particles [lo, hi) of a scene: this rank's contiguous slice of the global index range."""
+    import dataclasses
+    return dataclasses.replace(s, pose12=np.ascontiguousarray(s.pose12[lo:hi]),
+                               kf_pose12=np.ascontiguousarray(s.kf_pose12[lo:hi]))
 
 
 # ------------------------------------------------------------------ CPU oracle (reference arm)
@@ -190,7 +220,7 @@ def cpu_baseline(s, budget_s: float = 12.0):
             "cpu_model": cpu_model(), "single_thread_value": n1 * s.S / t1,
             "extrapolated_full_update_s": t * s.N / n,
             "triple_evals_per_s": n * s.S * 3 / t,
-            "sample": f"{n} of {s.N} particles (strided), full 4096-pt scan, 20 keyframes, "
+            "sample": f"{n} of {s.N} particles (strided), full {s.S}-pt scan, {s.K} keyframes, "
                       f"whole update a1-a7 on the sample; {t:.2f} s on {cores} threads "
                       f"(+ {n1} particles on 1 thread, {t1:.2f} s)"}, t
 
@@ -199,7 +229,7 @@ def run_reference(args):
     rank, world, local = dist_env()
     if rank != 0:
         return 0
-    s = make_scene(args.particles)
+    s = make_scene(args.config, args.particles or CONFIGS[args.config][1])
     import oracle
     oracle.build()
     oracle_step.kfs = oracle.Keyframes(s.keyframes, s.D, s.r)
@@ -214,8 +244,8 @@ def run_reference(args):
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "C2 bounded sample: strided particles of the 100k-particle "
-                                   "loop-corridor scene, 4096-pt scan, 20 keyframes",
+            "config": {"workload": f"{args.config} bounded sample: strided particles of the "
+                                   f"{s.N}-particle scene, {s.S}-pt scan, {s.K} keyframes",
                        "particles_per_step": n, "scan_points": s.S, "keyframes": s.K},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": oracle.num_threads(),
                              "kind": "oracle",
@@ -257,8 +287,16 @@ def run_gpu(args):
         import torch.distributed as dist
         dist.init_process_group("gloo")
         extra = dict(world_size=world, rank=rank, transport=mcs.TorchDistTransport())
-    s = make_scene(args.particles)  # every rank: the same keyframes and scan, its own shard
-    N, S, K = s.N, s.S, s.K
+    # every rank: the same keyframes and scan; particles sharded by contiguous global index.
+    # strong scaling: the config's particle count split over the ranks (the metric's
+    # "@100k particles, 1-8 GPU"); weak: every rank a full-size shard of its own (distinct
+    # particles of a world x larger draw)
+    n_cfg = args.particles or CONFIGS[args.config][1]
+    n_total = n_cfg if args.scaling == "strong" else n_cfg * world
+    s_all = make_scene(args.config, n_total)
+    lo, hi = rank * n_total // world, (rank + 1) * n_total // world
+    s = shard(s_all, lo, hi) if world > 1 else s_all
+    N, S, K = hi - lo, s.S, s.K
     stream = torch.cuda.Stream(device=dev)
     ctx = mcs.Context(N, K, S, neighbor_count=3, loop_recency_gap=s.gap, voxel_resolution=s.r,
                       device=local, **extra)
@@ -282,17 +320,20 @@ def run_gpu(args):
            "representative": torch.zeros(1, dtype=torch.int32, device=dev),
            "n_dead": torch.zeros(1, dtype=torch.int64, device=dev)}
     flush = torch.empty(64 * 2**20, dtype=torch.float32, device=dev)  # 256 MiB > 126 MB L2
-    # single GPU: the whole update is captured once into a CUDA graph and replayed (the
-    # SURVEY 8(d) protocol); multi-rank updates have host-side exchange steps, so they run eagerly
-    use_graph = world == 1 and not args.no_graph
+    # The whole update is captured once into a CUDA graph and replayed (the SURVEY 8(d)
+    # protocol): on one GPU, and across ranks joined by the library's NCCL communicator with
+    # peer-direct migration (every exchange step device-resident); the gloo script-path check
+    # runs eagerly (host collectives)
+    ctx.set_profiling(False)
+    ctx.restore()
+    torch.cuda.synchronize()
+    with torch.cuda.stream(stream):  # one eager update first (pools, peer views, NCCL setup)
+        ctx.update_async(d_m, d_c, s.D_now, s.U, out, stream=stream)
+    torch.cuda.synchronize()
+    use_graph = not args.no_graph and (world == 1 or (args.dist_backend == "nccl" and
+                                                      ctx.peer_migration_state == 1))
     graph = None
     if use_graph:
-        ctx.set_profiling(False)
-        ctx.restore()
-        torch.cuda.synchronize()
-        with torch.cuda.stream(stream):  # one eager update first (allocator pools, CUB temp)
-            ctx.update_async(d_m, d_c, s.D_now, s.U, out, stream=stream)
-        torch.cuda.synchronize()
         graph = torch.cuda.CUDAGraph()
         ctx.restore()
         torch.cuda.synchronize()
@@ -369,7 +410,7 @@ def run_gpu(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
     ms = total_ms / args.steps
-    value = world * N * S * args.steps / (total_ms * 1e-3)
+    value = n_total * S * args.steps / (total_ms * 1e-3)  # every rank's particles / max time
 
     # e2e: the public synchronous call with pinned host buffers (H2D scan, D2H results)
     h_m = torch.from_numpy(s.scan_mean3).pin_memory()
@@ -393,7 +434,7 @@ def run_gpu(args):
                          device=dev if args.dist_backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_mean = float(t.item())
-    e2e_value = world * N * S / e2e_mean
+    e2e_value = n_total * S / e2e_mean
 
     peaks, peak_src = measured_peaks()
     sm_mhz = peaks.get("sm_max_mhz", 1965.0)
@@ -405,17 +446,18 @@ def run_gpu(args):
     ph_mean = {k: float(np.mean([p[k] for p in phases])) for k in phases[0]}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": "C2: 100k particles x 4096-pt LiDAR-like scan vs 20 keyframes "
-                               "(loop corridor, r = 0.5 m, 3 neighbours, every particle loops)",
-                   "particles": N * world, "particles_per_gpu": N, "scan_points": S,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": CONFIGS[args.config][2].format(N=n_total),
+                   "particles": n_total, "particles_per_gpu": N, "scan_points": S,
                    "keyframes": K, "parallelism": f"particle shards x{world} ({args.dist_backend})",
                    "keyframe_cells": int(sum(len(k[0]) for k in s.keyframes)),
                    "l2": "particle state restored from a device snapshot and 256 MiB L2 flush "
                          "before every timed step (untimed)",
-                   "timed": ("CUDA-graph replay of the whole update (a1-a7)" if use_graph
-                             else "eager mcs_update_async (multi-rank exchange steps)"),
+                   "timed": ("CUDA-graph replay of the whole update (a1-a7"
+                             + (", NCCL exchange steps and peer-direct migration included)"
+                                if world > 1 else ")") if use_graph
+                             else "eager mcs_update_async (host-transport exchange steps)"),
                    "phases": ("from separate profiled eager updates" if use_graph
                               else "library phase events of the timed updates")},
         "roofline": {"kernel": "sweep (a2)", "bound": "alu", "achieved": achieved,
@@ -456,7 +498,12 @@ def main():
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
-    ap.add_argument("--particles", type=int, default=100_000)
+    ap.add_argument("--particles", type=int, default=0,
+                    help="total particles (default: the config's; --scaling weak: per rank)")
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="N > 1: the config's particles split over the ranks (strong, default) "
+                         "or a full-size shard per rank (weak)")
     ap.add_argument("--cpu-budget-s", type=float, default=12.0)
     ap.add_argument("--ref-step-s", type=float, default=4.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")

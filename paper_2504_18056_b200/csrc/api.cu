@@ -400,6 +400,19 @@ mcs_status mcs_create(const mcs_config* cfg, mcs_ctx** out) {
       uint64_t thr = ~0ull;
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     }
+    // Reserve the keyframe tables' share of the pool now (capacity_keyframes tables at the
+    // per-keyframe budget, at most 16 GiB): the pool keeps the block mapped after the free, so
+    // a later insertion (a0) takes its table without growing the pool (page mapping: ms).
+    if (!c->alloc.alloc && K > 0) {
+      const size_t tab = (size_t)std::max(cfg->kf_table_mib, 1) << 20;
+      const size_t want = std::min((size_t)K * (tab + 4096), (size_t)16 << 30);
+      void* p = nullptr;
+      if (cudaMallocAsync(&p, want, c->stream) == cudaSuccess) {
+        cudaFreeAsync(p, c->stream);
+      } else {
+        cudaGetLastError();  // not enough memory to reserve: insertions grow the pool instead
+      }
+    }
   }
   c->part_splits = cfg->point_splits > 0 ? cfg->point_splits : 1;
   if (e == cudaSuccess) e = dalloc(c, &c->d_part, (size_t)kSlotWords * nb * N * c->part_splits);

@@ -79,7 +79,19 @@ def test_iterations_and_post_update_parity(iters, post):
                                          gn_iterations=iters, weight_after_update=post, **kw),
                       oracle.Keyframes(s.keyframes, s.D, s.r), s.D_now, pose, kp, L,
                       s.scan_mean3, s.scan_cov6, s.U)
-    assert np.all(np.abs(g["loglik"] - o["loglik"]) <= 1e-4 * np.abs(o["loglik"]))
+    if post:
+        # R13 variant: l is evaluated at the pose after the last GN step.  GPU and oracle poses
+        # agree to ~1e-6 m there, not bit for bit, so a scan point on a cell face can change
+        # its correspondence between the two final poses (R27 pins correspondences for equal
+        # fp32 poses only).  Parity of l is therefore checked at the SAME pose: the oracle
+        # evaluated at the GPU's final pose.
+        ref = oracle.particles(oracle.make_config(voxel_resolution=s.r, loop_recency_gap=s.gap),
+                               oracle.Keyframes(s.keyframes, s.D, s.r), s.D_now,
+                               st["pose12"].copy(), st["kf_pose12"].copy(), s.scan_mean3,
+                               s.scan_cov6, apply_update=False)["loglik"]
+    else:
+        ref = o["loglik"]  # pre-update l of the first linearisation: the input poses
+    assert np.all(np.abs(g["loglik"] - ref) <= 1e-4 * np.abs(ref))
     assert np.abs(st["pose12"] - pose).max() <= 2e-5
     np.testing.assert_array_equal(g["flags"], o["flags"])
 
