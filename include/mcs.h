@@ -148,6 +148,13 @@ typedef struct mcs_config {
                                     first probes almost never walk a linear-probing chain; C2: 32
                                     MiB per keyframe); 64 (default); 0 = minimum capacity (load up
                                     to 1/4, least memory).  Results do not depend on it.        */
+  double   diversity_weight;     /* eta (m^2) of the neighbour-particle diversity term (R35): after
+                                    the GN step(s) every translation moves by eta d_i in the world
+                                    frame, d_i = (2 / (h N)) sum_j (t_i - t_j) exp(-|t_i - t_j|^2
+                                    / h) over all N particles (every rank) at the translations the
+                                    update started from (SVGD's repulsive term; the paper cites it,
+                                    P:32, and defines none); 0 (default) = off           */
+  double   diversity_bandwidth;  /* h (m^2) of that RBF kernel, > 0; 1.0 (default)              */
 } mcs_config;
 
 /* sizeof(mcs_config) of this build: bindings check their mirror of the struct against it. */

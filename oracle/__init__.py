@@ -54,6 +54,8 @@ class Config(C.Structure):
         ("corr_mode", C.c_int32),
         ("nn_radius", C.c_float),
         ("clone_split", C.c_int32),
+        ("diversity_weight", C.c_double),
+        ("diversity_bandwidth", C.c_double),
     ]
 
 
@@ -64,10 +66,11 @@ def make_config(voxel_resolution=0.5, neighbor_count=3, loop_recency_gap=10, gn_
                 damping_rel=1e-6, step_clamp=1.0, unmatched_penalty=0.0,
                 loglik_rel_floor=LN_1E16, posterior_floor=1e-8, gn_iterations=1,
                 weight_after_update=0, corr_mode=CORR_CELL, nn_radius=0.0,
-                clone_split=0) -> Config:
+                clone_split=0, diversity_weight=0.0, diversity_bandwidth=1.0) -> Config:
     return Config(neighbor_count, loop_recency_gap, voxel_resolution, gn_slots, damping_rel,
                   step_clamp, unmatched_penalty, loglik_rel_floor, posterior_floor,
-                  gn_iterations, weight_after_update, corr_mode, nn_radius, clone_split)
+                  gn_iterations, weight_after_update, corr_mode, nn_radius, clone_split,
+                  diversity_weight, diversity_bandwidth)
 
 
 class ParticleOut(C.Structure):
@@ -127,6 +130,7 @@ def lib():
         L.orc_dead.restype = C.c_int64
         L.orc_resample.argtypes = [i32, vp, vp, u32, vp]
         L.orc_resample.restype = C.c_int
+        L.orc_diversity.argtypes = [i32, vp, f64, vp]
         L.orc_representative.argtypes = [i32, vp]
         L.orc_representative.restype = i32
         L.orc_update.argtypes = [vp, i32, vp, vp, f64, i32, vp, vp, i32, vp, vp, vp, i32, u32, vp]
@@ -333,6 +337,14 @@ def resample(e, dead_mask, U: int):
     if rc:
         raise RuntimeError("degenerate: every particle dead")
     return donor
+
+
+def diversity(t, h: float):
+    """R35: d_i = (2 / (h N)) sum_j (t_i - t_j) exp(-|t_i - t_j|^2 / h) for translations t (N, 3)."""
+    t = _c(np.asarray(t, np.float64).reshape(-1, 3), np.float64)
+    d = np.zeros_like(t)
+    lib().orc_diversity(len(t), _p(t), float(h), _p(d))
+    return d
 
 
 def representative(w) -> int:

@@ -816,6 +816,25 @@ int32_t orc_representative(int32_t N, const double* w) {
 /* the whole update: steps 2-11 in the paper's per-frame order          */
 /* ------------------------------------------------------------------------- */
 
+/* R35 (flag): the neighbour-particle diversity term — SVGD's kernel-gradient term with an RBF
+ * kernel k(x, y) = exp(-|x - y|^2 / h) on the current-pose translations (the paper cites SVGD /
+ * GN-SVGD for "preserving sample diversity through neighbor particle information", P:32, P:78,
+ * and defines no term of its own).  Written as the definition: a plain double loop. */
+void orc_diversity(int32_t N, const double* t, double h, double* d) {
+  for (int32_t i = 0; i < N; ++i) {
+    double acc[3] = {0.0, 0.0, 0.0};
+    for (int32_t j = 0; j < N; ++j) {
+      const double dx = t[3 * i] - t[3 * j], dy = t[3 * i + 1] - t[3 * j + 1],
+                   dz = t[3 * i + 2] - t[3 * j + 2];
+      const double k = exp(-(dx * dx + dy * dy + dz * dz) / h);
+      acc[0] += dx * k;
+      acc[1] += dy * k;
+      acc[2] += dz * k;
+    }
+    for (int c = 0; c < 3; ++c) d[3 * i + c] = 2.0 / (h * (double)N) * acc[c];
+  }
+}
+
 int orc_update(const orc_config* cfg, int32_t K, orc_map* const* maps, const double* D,
                double D_now, int32_t N, float* pose12, float* kf_pose12, int32_t kf_stride,
                double* L, const float* scan_mean3, const float* scan_cov6, int32_t S,
@@ -831,12 +850,32 @@ int orc_update(const orc_config* cfg, int32_t K, orc_map* const* maps, const dou
   /* steps 2-7, repeated gn_iterations times (R12); the weighting l is the pre-update l of the
    * first iteration (R13) unless weight_after_update asks for a re-evaluation */
   const int32_t iters = cfg->gn_iterations > 0 ? cfg->gn_iterations : 1;
+  /* R35: the translations the diversity term is taken at (the start of the update) */
+  double* t0 = NULL;
+  if (cfg->diversity_weight != 0.0) {
+    t0 = (double*)malloc(sizeof(double) * 3 * (N > 0 ? N : 1));
+    for (int32_t i = 0; i < N; ++i)
+      for (int c = 0; c < 3; ++c) t0[3 * i + c] = (double)pose12[12 * (size_t)i + 4 * c + 3];
+  }
   int rc = 0;
   for (int32_t it = 0; it < iters && rc == 0; ++it) {
     rc = orc_particles(cfg, K, maps, D, D_now, N, pose12, kf_pose12, kf_stride, scan_mean3,
                        scan_cov6, S, NULL, N, 1, &po);
     if (it == 0) memcpy(lw, out->loglik, sizeof(double) * N);
   }
+  if (rc == 0 && t0) {
+    /* after the GN step(s): t_i <- t_i + eta d_i in the world frame, rounded to fp32 (R35);
+     * rotations, keyframe poses and weights untouched */
+    double* d = (double*)malloc(sizeof(double) * 3 * (N > 0 ? N : 1));
+    orc_diversity(N, t0, cfg->diversity_bandwidth, d);
+    for (int32_t i = 0; i < N; ++i)
+      for (int c = 0; c < 3; ++c) {
+        float* tc = pose12 + 12 * (size_t)i + 4 * c + 3;
+        *tc = (float)((double)*tc + cfg->diversity_weight * d[3 * i + c]);
+      }
+    free(d);
+  }
+  free(t0);
   if (rc == 0 && cfg->weight_after_update) {
     orc_particle_out pe;
     memset(&pe, 0, sizeof(pe));

@@ -46,6 +46,8 @@ typedef struct {
   int32_t corr_mode;           /* 0: CELL, the containing voxel (R7); 1: NN27 (R33)       */
   float   nn_radius;           /* NN27 candidate radius, 0 < nn_radius <= r (R33)        */
   int32_t clone_split;         /* 0: a clone copies the donor's L (R19); 1: split (R34)  */
+  double  diversity_weight;    /* eta (m^2) of the neighbour-particle term (R35); 0: off  */
+  double  diversity_bandwidth; /* h (m^2) of its RBF kernel (R35)                        */
 } orc_config;
 
 /* ---- SE(3) (right-applied exp) ---- */
@@ -149,6 +151,10 @@ typedef struct {
   int32_t* representative; int64_t* n_dead;
 } orc_update_out;
 
+/* R35: SVGD's repulsive (diversity) term over the particles' translations t[N][3] (P:32,
+ * P:41, P:78 cite it; the paper defines none): d_i = (2 / (h N)) sum_j (t_i - t_j)
+ * exp(-|t_i - t_j|^2 / h), i.e. d_i = -grad_{t_i} (1/N) sum_j k(t_i, t_j), k the RBF kernel. */
+void orc_diversity(int32_t N, const double* t, double h, double* d);
 int orc_update(const orc_config* cfg,
                int32_t K, orc_map* const* maps, const double* D, double D_now,
                int32_t N, float* pose12, float* kf_pose12, int32_t kf_stride, double* L,

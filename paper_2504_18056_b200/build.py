@@ -15,7 +15,8 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libmcs.so")
-SOURCES = ["api.cu", "kf_store.cu", "select.cu", "sweep.cu", "update.cu", "weights.cu", "dist.cu", "predict.cu"]
+SOURCES = ["api.cu", "kf_store.cu", "select.cu", "sweep.cu", "update.cu", "weights.cu", "dist.cu",
+           "predict.cu", "diversity.cu"]
 HEADERS = ["mcs_internal.cuh", "reduce.cuh", "se3.cuh"]
 
 NVCC_FLAGS = [

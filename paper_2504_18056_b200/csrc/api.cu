@@ -225,7 +225,8 @@ static void free_all(mcs_ctx* c) {
                   c->d_ladder,  c->d_ladder_scan, c->d_donor,    c->d_partials,
                   c->d_ipartials, c->d_scal,  c->d_cub_temp, c->d_skeys, c->d_skeys_out,
                   c->d_sids,    c->d_stage,   c->d_bad,      c->d_dead_list, c->d_donor_g,
-                  c->d_plan,    c->d_pack_src, c->d_send,    c->d_recv};
+                  c->d_plan,    c->d_pack_src, c->d_send,    c->d_recv,     c->d_tall,
+                  c->d_divn};
   for (void* p : ptrs) mem_free(c, p);
   if (c->h_scal) cudaFreeHost(c->h_scal);
   if (c->h_stage) cudaFreeHost(c->h_stage);
@@ -281,6 +282,8 @@ void mcs_config_default(mcs_config* cfg) {
   cfg->peer_migration = 1;
   cfg->graph_replay = 1;
   cfg->kf_table_mib = 64;
+  cfg->diversity_weight = 0.0;
+  cfg->diversity_bandwidth = 1.0;
   cfg->point_splits = 0;
   cfg->rank = 0;
   cfg->world_size = 1;
@@ -320,6 +323,12 @@ mcs_status mcs_create(const mcs_config* cfg, mcs_ctx** out) {
       !(cfg->damping_rel >= 0) || !(cfg->step_clamp > 0) || !(cfg->unmatched_penalty >= 0) ||
       std::isnan(cfg->loglik_rel_floor) || std::isnan(cfg->posterior_floor)) {
     g_create_error = "invalid numeric configuration";
+    return MCS_E_INVALID_ARG;
+  }
+  if (!std::isfinite(cfg->diversity_weight) ||
+      (cfg->diversity_weight != 0.0 &&
+       !(cfg->diversity_bandwidth > 0.0 && std::isfinite(cfg->diversity_bandwidth)))) {
+    g_create_error = "diversity_weight must be finite, diversity_bandwidth > 0 and finite (R35)";
     return MCS_E_INVALID_ARG;
   }
   if (cfg->gn_iterations < 1 || cfg->gn_iterations > 64 ||
@@ -641,6 +650,24 @@ mcs_status mcs_set_particles(mcs_ctx* ctx, int32_t n, const float* pose12,
   }
   ctx->gbase = 0;
   for (int g = 0; g < ctx->rank; ++g) ctx->gbase += ctx->n_per_rank[g];
+  if (ctx->cfg.diversity_weight != 0.0) {  // R35: every rank's translations, padded
+    long long mx = 0;
+    for (long long v : ctx->n_per_rank) mx = v > mx ? v : mx;
+    if ((int)mx > ctx->div_maxn) {
+      mem_free(ctx, ctx->d_tall);
+      ctx->d_tall = nullptr;
+      ctx->div_maxn = 0;
+      CUDA_TRY(ctx, mem_alloc(ctx, (void**)&ctx->d_tall,
+                              sizeof(double) * 3 * (size_t)mx * ctx->world));
+      if (!ctx->d_divn) CUDA_TRY(ctx, mem_alloc(ctx, (void**)&ctx->d_divn, sizeof(int) * ctx->world));
+    }
+    ctx->div_maxn = (int)mx;
+    std::vector<int> nr(ctx->world);
+    for (int g = 0; g < ctx->world; ++g) nr[g] = (int)ctx->n_per_rank[g];
+    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->d_divn, nr.data(), sizeof(int) * ctx->world,
+                                  cudaMemcpyHostToDevice, st));
+    CUDA_TRY(ctx, cudaStreamSynchronize(st));
+  }
   double n_total = 0.0;  // uniform initial weights over the particles of every rank
   for (int g = 0; g < ctx->world; ++g) n_total += (double)ctx->n_per_rank[g];
   CUDA_TRY(ctx, cudaMemcpyAsync(&ctx->d_scal->S2, &n_total, sizeof(double),
@@ -750,9 +777,11 @@ static void record(mcs_ctx* ctx, int k) {
 static mcs_status run_update_body(mcs_ctx* ctx, int n_pts, uint32_t U) {
   const int iters = ctx->cfg.gn_iterations > 0 ? ctx->cfg.gn_iterations : 1;
   const bool post = ctx->cfg.weight_after_update != 0;
+  const bool div = ctx->cfg.diversity_weight != 0.0;
   record(ctx, 0);
+  if (div) MCS_TRY(launch_diversity_snapshot(ctx));  // R35: translations at the start
   for (int it = 0; it < iters; ++it) {  // R12: each iteration is a full a1-a4 pass
-    launch_select(ctx, kSelectUpdate);                                  // a1
+    MCS_TRY(launch_select(ctx, kSelectUpdate));                         // a1
     if (it == 0) record(ctx, 1);
     launch_sweep(ctx, n_pts);                                           // a2
     if (it == 0) record(ctx, 2);
@@ -760,8 +789,9 @@ static mcs_status run_update_body(mcs_ctx* ctx, int n_pts, uint32_t U) {
                    nullptr, nullptr, nullptr, nullptr, nullptr, nullptr);  // a3 (+ L += l)
     launch_propagate(ctx);                                              // a4
   }
+  if (div) MCS_TRY(launch_diversity_apply(ctx));  // R35: t_i += eta d_i after the GN step(s)
   if (post) {  // R13 variant: weight with l re-evaluated at the updated poses
-    launch_select(ctx, kSelectWeight);
+    MCS_TRY(launch_select(ctx, kSelectWeight));
     launch_sweep(ctx, n_pts);
     launch_combine(ctx, n_pts, kCombineWeight, nullptr, nullptr, nullptr, nullptr, nullptr,
                    nullptr);
@@ -789,7 +819,7 @@ static mcs_status run_update(mcs_ctx* ctx, int n_pts, double D_now, uint32_t U) 
   const bool graph = ctx->cfg.graph_replay && !ctx->graph_off && !ctx->profiling &&
                      weights_device_resident(ctx) && cap == cudaStreamCaptureStatusNone;
   if (!graph) return run_update_body(ctx, n_pts, U);
-  const long long key[4] = {n_pts, ctx->N, ctx->K, 0};
+  const long long key[4] = {n_pts, ctx->N, ctx->K, ctx->div_maxn};  // R35's gather shape
   if (!ctx->gexec || memcmp(key, ctx->gkey, sizeof(key)) != 0) {
     if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
     ctx->gexec = nullptr;
@@ -923,7 +953,7 @@ mcs_status mcs_eval(mcs_ctx* ctx, const float* scan_mean3, const float* scan_cov
   CUDA_TRY(ctx, mem_alloc_async(ctx, (void**)&dn, 4 * NS, st));
   CUDA_TRY(ctx, mem_alloc_async(ctx, (void**)&dk, 4 * NS, st));
   CUDA_TRY(ctx, mem_alloc_async(ctx, (void**)&dloop, ctx->N, st));
-  launch_select(ctx, kSelectEval);
+  if (launch_select(ctx, kSelectEval) != MCS_OK) CUDA_TRY(ctx, cudaErrorLaunchFailure);
   launch_sweep(ctx, n_pts);
   launch_combine(ctx, n_pts, kCombineEval, dl, dH, db, dn, dk, dloop);
   CUDA_TRY(ctx, cudaGetLastError());

@@ -209,6 +209,11 @@ struct mcs_ctx {
   cudaGraphExec_t gexec = nullptr;
   long long gkey[4] = {-1, -1, -1, -1};  // n_pts, N, K, flags
   bool graph_off = false;                // capture failed once: eager from then on
+  // neighbour-particle diversity term (R35, cfg.diversity_weight != 0): every rank's
+  // translations at the start of the update, padded to the largest shard
+  double* d_tall = nullptr;            // [world][div_maxn][3]
+  int* d_divn = nullptr;               // [world] shard sizes
+  int div_maxn = 0;
   mcs::PeerView* d_peers = nullptr;    // [world] device views of every rank's state
   std::vector<void*> ipc_opened;       // CUDA IPC mappings of other processes' buffers
 };
@@ -227,7 +232,7 @@ void launch_prepare_scan(const float* mean3, const float* cov6, int S, float4* o
                          cudaStream_t st);
 // a1; mode: kSelectUpdate (H~, b~ for slots in G), kSelectEval (all slots), kSelectWeight (none)
 enum { kSelectUpdate = 0, kSelectEval = 1, kSelectWeight = 2 };
-void launch_select(mcs_ctx* c, int mode);
+mcs_status launch_select(mcs_ctx* c, int mode);  // MCS_E_CUDA if a launch (or the sort) fails
 // a2
 void launch_sweep(mcs_ctx* c, int S);
 // point splits the sweep would use for n local particles (cfg.point_splits, or auto)
@@ -289,6 +294,9 @@ mcs_status dist_alltoallv(mcs_ctx* c, const float* d_send, const size_t* send_by
                           const size_t* recv_off);
 size_t sort_temp_needed(int n, int capK);
 // NEXT rows (predict.cu): Eq.1 prediction; keyframe-insertion overlap
+// R35: snapshot this rank's translations (+ the device allgather over ranks) / apply eta d_i
+mcs_status launch_diversity_snapshot(mcs_ctx* c);
+mcs_status launch_diversity_apply(mcs_ctx* c);
 mcs_status launch_predict(mcs_ctx* c, double* d_buf, int* d_bad, unsigned long long seed,
                           unsigned long long frame, double vsig);
 mcs_status launch_overlap(mcs_ctx* c, const float* d_mean3, int S, const float* d_rel, int kf,

@@ -153,7 +153,7 @@ size_t sort_temp_needed(int n, int capK) {
   return b;
 }
 
-void launch_select(mcs_ctx* c, int mode) {
+mcs_status launch_select(mcs_ctx* c, int mode) {
   const int N = c->N;
   const int nb_max = c->cfg.neighbor_count;
   const int end_bit = sort_end_bit(c->capK);
@@ -163,8 +163,11 @@ void launch_select(mcs_ctx* c, int mode) {
       c->cfg.gn_slots == MCS_GN_ALL_SLOTS, mode, c->d_items, c->d_meta, c->d_to,
       c->d_skeys, c->d_sids, inactive);
   size_t tb = c->cub_temp_bytes;
-  cub::DeviceRadixSort::SortPairs(c->d_cub_temp, tb, c->d_skeys, c->d_skeys_out, c->d_sids,
-                                  c->d_order, nb_max * N, 0, end_bit, c->stream);
+  if (cub::DeviceRadixSort::SortPairs(c->d_cub_temp, tb, c->d_skeys, c->d_skeys_out, c->d_sids,
+                                      c->d_order, nb_max * N, 0, end_bit, c->stream) !=
+      cudaSuccess)
+    return MCS_E_CUDA;
+  return cudaGetLastError() == cudaSuccess ? MCS_OK : MCS_E_CUDA;
 }
 
 }  // namespace mcs

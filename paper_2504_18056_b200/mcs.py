@@ -63,6 +63,8 @@ class Config(C.Structure):
         ("point_splits", C.c_int32),
         ("graph_replay", C.c_int32),
         ("kf_table_mib", C.c_int32),
+        ("diversity_weight", C.c_double),
+        ("diversity_bandwidth", C.c_double),
     ]
 
 

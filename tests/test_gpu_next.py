@@ -223,3 +223,57 @@ def test_get_pose_equals_get_particles_row():
             np.testing.assert_array_equal(ctx.get_pose(i), allp[i])
         with pytest.raises(mcs.MCSError):
             ctx.get_pose(s.N)
+
+
+# ------------------------------------------------------------------ diversity term (R35)
+def test_diversity_term_parity_c1():
+    """The neighbour-particle diversity term (flag, R35) on every particle of C1: poses after
+    the update against the oracle's (GN step, then t_i += eta d_i), and the term is really
+    applied (the poses differ from the plain update's by far more than the tolerance)."""
+    s = synth.c1()
+    kw = dict(posterior_floor=0.0, loglik_rel_floor=-np.inf)
+    eta, h = 0.02, 0.05
+    with _ctx(s, diversity_weight=eta, diversity_bandwidth=h, **kw) as ctx:
+        g = ctx.update(s.scan_mean3, s.scan_cov6, s.D_now, s.U)
+        st = ctx.get_particles()
+    with _ctx(s, **kw) as ctx:
+        ctx.update(s.scan_mean3, s.scan_cov6, s.D_now, s.U)
+        plain = ctx.get_particles()
+    pose, kp, L = s.pose12.copy(), s.kf_pose12.copy(), np.zeros(s.N)
+    o = oracle.update(oracle.make_config(voxel_resolution=s.r, loop_recency_gap=s.gap,
+                                         diversity_weight=eta, diversity_bandwidth=h, **kw),
+                      oracle.Keyframes(s.keyframes, s.D, s.r), s.D_now, pose, kp, L,
+                      s.scan_mean3, s.scan_cov6, s.U)
+    ang, dt = pose_err(st["pose12"], pose)
+    assert ang.max() <= 1e-5 and dt.max() <= 1e-5, (ang.max(), dt.max())
+    np.testing.assert_array_equal(st["kf_pose12"], plain["kf_pose12"])  # keyframes untouched
+    moved = np.abs(st["pose12"] - plain["pose12"]).max()
+    assert moved > 1e-3, moved
+    np.testing.assert_array_equal(g["flags"], o["flags"])
+    assert np.all(np.abs(g["loglik"] - o["loglik"]) <= 1e-4 * np.abs(o["loglik"]))
+
+
+def test_diversity_multirank_and_graph_bitwise():
+    """R35 needs every particle's translation: with G = 2 and 3 ranks (in-process transport,
+    the device allgather of the padded shards) the result equals the 1-rank result bit for
+    bit; the library's CUDA graph (snapshot + term inside) equals kernel-by-kernel updates."""
+    from test_gpu_multirank import _run_ranks
+    s = synth.c1()
+    kw = dict(diversity_weight=0.02, diversity_bandwidth=0.05)
+    one = _run_ranks(s, [np.arange(s.N)], **kw)
+    for G in (2, 3):
+        cuts = np.linspace(0, s.N, G + 1).astype(int)
+        cuts[1:-1] += 5
+        many = _run_ranks(s, [np.arange(cuts[r], cuts[r + 1]) for r in range(G)], **kw)
+        for k in ("loglik", "donor", "flags", "pose12", "kf_pose12", "L"):
+            assert np.array_equal(many[k], one[k]), (G, k)
+    runs = {}
+    for gr in (0, 1):
+        with _ctx(s, graph_replay=gr, **kw) as ctx:
+            outs = [ctx.update(s.scan_mean3, s.scan_cov6, s.D_now + 0.1 * k, s.U + k)
+                    for k in range(3)]
+            outs.append(ctx.get_particles())
+        runs[gr] = outs
+    for a, b in zip(runs[0], runs[1]):
+        for k in a:
+            assert np.array_equal(np.asarray(a[k]), np.asarray(b[k])), k
