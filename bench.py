@@ -33,8 +33,9 @@ METRIC = ("particle·point likelihood+grad evals/s; ms per update @100k particle
 UNIT = "particle·point evals/s"
 FLOPS_MATCHED = 236.0    # FP32 flops per matched (particle, point, slot) with H~, b~
 FLOPS_UNMATCHED = 21.0   # transform + key for an unmatched triple
-GATHER_MATCHED = 56.0    # bytes: 8-B key probe + 48-B payload
-GATHER_UNMATCHED = 8.0
+GATHER_MATCHED = 44.0    # algorithmic bytes per matched triple: 8-B key + 12-B mu'
+#                          + 24-B Sigma' (the slot layout moves 40 B + the 4-B key per first probe)
+GATHER_UNMATCHED = 8.0   # the key probe of an unmatched triple
 LAUNCHES_PER_UPDATE = 18  # kernels per mcs_update_async: set_params, prepare_scan, select, 7 CUB
 #                           sort kernels, sweep, combine, propagate, exp_sum, ladder, draws,
 #                           renorm, gather_outputs (profiles/r02_launches.csv)
@@ -257,12 +258,17 @@ def run_reference(args):
 
 
 def gather_roofline(gather_bytes, sweep_ms):
-    """The co-bound: algorithmic probe bytes (56 B per matched triple, 8 B per
-    unmatched) per sweep vs the L2 random 32-B gather bandwidth measured by bench/peaks.cu."""
+    """The co-bound: algorithmic probe bytes (44 B per matched triple, 8 B per
+    unmatched) per sweep over the L2 random 32-B sector-gather bandwidth bench/peaks.cu measures.
+    Context, not a bound: that benchmark reads independent random sectors, while the coherence
+    sort makes the 32 lanes of a warp share sectors (each L1 sector serves ~3 lanes), so the
+    algorithmic rate can exceed it; the sweep's bound is its FP32 arithmetic."""
     peak = own_peaks().get("l2_gather_32B_GBps")
     ach = gather_bytes / (sweep_ms * 1e-3) / 1e9
     return {"achieved_GBps": ach, "peak_GBps": peak, "frac": (ach / peak) if peak else None,
-            "peak_source": "profiles/r01_peaks.json (bench/peaks.cu, measured)" if peak else None}
+            "bytes_per_matched_triple": GATHER_MATCHED,
+            "peak_source": "profiles/r01_peaks.json (bench/peaks.cu: independent random 32-B "
+                           "sectors over an L2-resident table)" if peak else None}
 
 
 # ------------------------------------------------------------------ GPU arm
@@ -333,6 +339,9 @@ def run_gpu(args):
     use_graph = not args.no_graph and (world == 1 or (args.dist_backend == "nccl" and
                                                       ctx.peer_migration_state == 1))
     graph = None
+    # the library's phase events are recorded inside the captured update, so every timed
+    # replay also times its own phases (the sweep's CUDA-event time on its launch stream)
+    ctx.set_profiling(True)
     if use_graph:
         graph = torch.cuda.CUDAGraph()
         ctx.restore()
@@ -340,8 +349,6 @@ def run_gpu(args):
         with torch.cuda.graph(graph, stream=stream):
             ctx.update_async(d_m, d_c, s.D_now, s.U, out, stream=stream)
         torch.cuda.synchronize()
-    else:
-        ctx.set_profiling(True)
 
     def one_step(profiled=False):
         with torch.cuda.stream(stream):
@@ -370,10 +377,9 @@ def run_gpu(args):
                 e0, e1 = one_step()
                 e1.synchronize()
                 step_ms.append(e0.elapsed_time(e1))
-                if graph is None:
-                    ph = ctx.phase_ms()
-                    phases.append(ph)
-                    sweep_ms.append(ph["sweep"])
+                ph = ctx.phase_ms()  # events recorded by this very (replayed) update
+                phases.append(ph)
+                sweep_ms.append(ph["sweep"])
             torch.cuda.synchronize()
             if dist:
                 dist.barrier()
@@ -394,15 +400,7 @@ def run_gpu(args):
     if flag > 0:
         remeasured = clocks.summary()["reasons"]
         step_ms, sweep_ms, phases, clocks = timed_region()
-    if graph is not None:  # phase breakdown (roofline) from profiled eager updates, untimed
-        ctx.set_profiling(True)
-        for k in range(max(3, min(args.steps, 10))):
-            e0, e1 = one_step(profiled=True)
-            e1.synchronize()
-            ph = ctx.phase_ms()
-            phases.append(ph)
-            sweep_ms.append(ph["sweep"])
-        ctx.set_profiling(False)
+    ctx.set_profiling(False)
     total_ms = float(np.sum(step_ms))
     if dist:  # the job's time is the slowest rank's
         t = torch.tensor([total_ms], dtype=torch.float64,
@@ -458,8 +456,7 @@ def run_gpu(args):
                              + (", NCCL exchange steps and peer-direct migration included)"
                                 if world > 1 else ")") if use_graph
                              else "eager mcs_update_async (host-transport exchange steps)"),
-                   "phases": ("from separate profiled eager updates" if use_graph
-                              else "library phase events of the timed updates")},
+                   "phases": "library phase events recorded inside the timed updates"},
         "roofline": {"kernel": "sweep (a2)", "bound": "alu", "achieved": achieved,
                      "peak": fp32_peak, "unit": "TFLOP/s", "frac": achieved / fp32_peak,
                      "traffic": committed_traffic(),

@@ -769,8 +769,16 @@ static mcs_status check_update_args(mcs_ctx* ctx, const void* m, const void* c, 
   return MCS_OK;
 }
 
+// phase events; inside a stream capture they become event-record nodes of the graph (the
+// External flag), so each replay records them and the phases of a replayed update are timed
 static void record(mcs_ctx* ctx, int k) {
-  if (ctx->profiling) cudaEventRecord(ctx->ev[k], ctx->stream);
+  if (!ctx->profiling) return;
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(ctx->stream, &cap);
+  if (cap == cudaStreamCaptureStatusActive)
+    cudaEventRecordWithFlags(ctx->ev[k], ctx->stream, cudaEventRecordExternal);
+  else
+    cudaEventRecord(ctx->ev[k], ctx->stream);
 }
 
 // the hot path a1..a7, stream-ordered; scan already prepared in d_scan
@@ -816,10 +824,12 @@ static mcs_status run_update(mcs_ctx* ctx, int n_pts, double D_now, uint32_t U) 
     const mcs_status ps = dist_peer_setup(ctx);
     if (ps != MCS_OK) return ps;
   }
-  const bool graph = ctx->cfg.graph_replay && !ctx->graph_off && !ctx->profiling &&
+  // (with profiling on, the phase events are recorded inside the graph: timed replays)
+  const bool graph = ctx->cfg.graph_replay && !ctx->graph_off &&
                      weights_device_resident(ctx) && cap == cudaStreamCaptureStatusNone;
   if (!graph) return run_update_body(ctx, n_pts, U);
-  const long long key[4] = {n_pts, ctx->N, ctx->K, ctx->div_maxn};  // R35's gather shape
+  const long long key[5] = {n_pts, ctx->N, ctx->K, ctx->div_maxn,  // R35's gather shape
+                            ctx->profiling ? 1 : 0};                // phase events inside
   if (!ctx->gexec || memcmp(key, ctx->gkey, sizeof(key)) != 0) {
     if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
     ctx->gexec = nullptr;

@@ -207,7 +207,7 @@ struct mcs_ctx {
   int p2p = 0;
   // CUDA graph of the single-rank update body (run_update), replayed while its key holds
   cudaGraphExec_t gexec = nullptr;
-  long long gkey[4] = {-1, -1, -1, -1};  // n_pts, N, K, flags
+  long long gkey[5] = {-1, -1, -1, -1, -1};  // n_pts, N, K, diversity gather rows, profiling
   bool graph_off = false;                // capture failed once: eager from then on
   // neighbour-particle diversity term (R35, cfg.diversity_weight != 0): every rank's
   // translations at the start of the update, padded to the largest shard
