@@ -346,7 +346,8 @@ def run_gpu(args):
         graph = torch.cuda.CUDAGraph()
         ctx.restore()
         torch.cuda.synchronize()
-        with torch.cuda.graph(graph, stream=stream):
+        # thread-local capture: NCCL's own (capture-aware) calls on other threads are legal
+        with torch.cuda.graph(graph, stream=stream, capture_error_mode="thread_local"):
             ctx.update_async(d_m, d_c, s.D_now, s.U, out, stream=stream)
         torch.cuda.synchronize()
 
