@@ -10,8 +10,8 @@ import pytest
 import oracle
 import paper_2504_18056_b200 as mcs
 import synth
-from test_gpu_parity import (G_RTOL, L_RTOL, ROT_TOL, T_TOL, check_slots, make_ctx, orc_cfg,
-                             pose_err, rel_err)
+from test_gpu_parity import (G_RTOL, H_RTOL, L_RTOL, ROT_TOL, T_TOL, check_slots, make_ctx,
+                             orc_cfg, pose_err, rel_err)
 
 pytestmark = pytest.mark.gpu
 
@@ -23,8 +23,9 @@ def c2s():
 
 # The north-star tolerances are for whole scans.  With a handful of points the fp32 rounding of
 # q (~1e-6 m at 10-20 m) against centimetre residuals is ~1e-4 of e per point and nothing
-# averages it out: l is then compared at 2e-3 relative and the (rank-deficient, damping-
-# dominated) pose step is not compared.
+# averages it out: l is then compared at 2e-3 relative, g at 1e-2, H at the full 1e-3, and the
+# (rank-deficient, damping-dominated) pose step is not compared.  mcs.h states this S >= 64
+# domain of the 1e-4 contract.
 FEW = 64
 
 
@@ -55,9 +56,20 @@ def _update_parity(s, **kw):
     assert np.all(np.abs(g["loglik"] - o["loglik"]) <= rt * np.abs(o["loglik"]) + 1e-6)
     np.testing.assert_array_equal(g["flags"] & 1, o["flags"] & 1)
     if s.S < FEW:
+        # g = -2 sum J^T Omega e inherits the ~1e-4-per-point rounding of e, with cancellation
+        # across a handful of terms: 1e-2; H depends on e only through the correspondences (and
+        # on m = q - t, relative 1e-7): the full 1e-3.  Zero rows stay exactly zero.
+        gn = np.linalg.norm(o["grad6"], axis=1) > 0
+        assert np.all(rel_err(g["grad6"][gn], o["grad6"][gn], axis=1) <= 1e-2)
+        assert not g["grad6"][~gn].any()
+        Hg = mcs.unpack_h21(g["hess21"]).reshape(-1, 36).astype(float)
+        Ho = o["hess36"].reshape(-1, 36)
+        hz = np.linalg.norm(Ho, axis=1) > 0
+        assert np.all(rel_err(Hg[hz], Ho[hz], axis=1) <= H_RTOL)
         return g, o
     gn = np.linalg.norm(o["grad6"], axis=1) > 0
     assert np.all(rel_err(g["grad6"][gn], o["grad6"][gn], axis=1) <= G_RTOL)
+    assert not g["grad6"][~gn].any()
     np.testing.assert_array_equal(g["flags"], o["flags"])
     ang, dt = pose_err(st["pose12"], pose)
     assert ang.max() <= ROT_TOL and dt.max() <= T_TOL, (ang.max(), dt.max())
