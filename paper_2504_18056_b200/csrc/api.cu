@@ -433,7 +433,7 @@ mcs_status mcs_create(const mcs_config* cfg, mcs_ctx** out) {
   if (e == cudaSuccess) e = dalloc(c, &c->d_hess, 21 * N);
   if (e == cudaSuccess) e = dalloc(c, &c->d_flags, N);
   if (e == cudaSuccess) e = dalloc(c, &c->d_e, N);
-  if (e == cudaSuccess) e = dalloc(c, &c->d_xg, 32 * (size_t)(cfg->world_size + 1) + 96);
+  if (e == cudaSuccess) e = dalloc(c, &c->d_xg, 64 * (size_t)(cfg->world_size + 1) + 96);
   if (e == cudaSuccess) e = mem_alloc(c, &c->d_ladder, 16 * N);
   // look-back tile flags carry a launch epoch; zero memory matches no published tile
   if (e == cudaSuccess) e = cudaMemset(c->d_ladder, 0, 16 * N);
@@ -726,7 +726,7 @@ mcs_status mcs_get_global_pose(mcs_ctx* ctx, int64_t global_index, float* pose12
     FAIL(ctx, MCS_E_INVALID_ARG, "mcs_get_global_pose: index %lld outside [0, %lld)",
          (long long)global_index, n_total);
   cudaStream_t st = ctx->stream;
-  double* d = reinterpret_cast<double*>(ctx->d_xg) + 4 * (ctx->world + 1);  // 12 doubles
+  double* d = reinterpret_cast<double*>(ctx->d_xg) + 8 * (ctx->world + 1);  // 12 doubles
   const long long li = global_index - ctx->gbase;
   const int owner = li >= 0 && li < ctx->N;
   pose_column_kernel<<<1, 12, 0, st>>>(ctx->d_pose, ctx->capN, owner ? (int)li : -1, d);

@@ -166,7 +166,8 @@ struct mcs_ctx {
   float* d_hess = nullptr;      // [21][Ncap]
   uint8_t* d_flags = nullptr;   // [Ncap]
   double* d_e = nullptr;        // [Ncap] e_i, then e'_i after the respawn: w_i = e'_i / S'
-  char* d_xg = nullptr;         // [4][world+1] x 8 B: device allgathers (Q_g, D_g), (e'_g, rep_g),
+  char* d_xg = nullptr;         // [8][world+1] x 8 B: device allgathers {Q_g, D_g, m'_g, -},
+                                // {S'_g, e'_g, rep_g, -},
                                 // then 12 doubles: the all-reduced pose of mcs_get_global_pose
   void* d_ladder = nullptr;     // [Ncap] 16-B look-back tile states of the ladder scan (zeroed)
   void* d_ladder_scan = nullptr;  // [Ncap] u64 inclusive survivor ladder C_i

@@ -21,10 +21,12 @@
 //                      straight into a peer rank's state over peer memory
 //   renorm_kernel      e' = exp(L - m'), S' and the argmax (ties -> lowest index); w = e' / S'
 //                      is formed where it is read (outputs, mcs_get_particles)
-// Across ranks every quantity above is global: m, l*, S, m', S' are all-reduced, the ladder
-// offsets and totals come from a device allgather of (Q_g, D_g) and a one-thread plan kernel,
-// and the representative from a device allgather of each rank's best.  With NCCL and peer
-// access no step waits on the host; the host-transport and pack/send/recv fallbacks do.
+// Across ranks every quantity above is global: m, l* and S are all-reduced; the ladder
+// offsets and totals and the survivors' max m' come from one device allgather of
+// {Q_g, D_g, m'_g} and a one-thread plan kernel; S' and the representative from one device
+// allgather of {S'_g, best e'_g, index} (S' summed in rank order).  Five collectives with
+// peer-direct migration (the fifth is the barrier after the draws).  With NCCL and peer access
+// no step waits on the host; the host-transport and pack/send/recv fallbacks do.
 #include <algorithm>
 #include <vector>
 
@@ -293,15 +295,20 @@ __global__ void plan_kernel(const long long* __restrict__ QD, int G, int me, Sca
                             long long* __restrict__ plan) {
   unsigned __int128 Q = 0;
   long long D = 0, qo = 0, dof = 0;
+  double m2 = -INFINITY;
   for (int g = 0; g < G; ++g) {
     if (g == me) {
       qo = (long long)Q;
       dof = D;
     }
     plan[g] = D;
-    Q += (unsigned long long)QD[2 * g];
-    D += QD[2 * g + 1];
+    Q += (unsigned long long)QD[4 * g];
+    D += QD[4 * g + 1];
+    double mg;
+    memcpy(&mg, &QD[4 * g + 2], 8);
+    m2 = fmax(m2, mg);  // the global survivors' max of L (-inf where a rank has none)
   }
+  sc->m2 = m2;
   plan[G] = D;
   const bool over = (Q >> 64) != 0;  // the exact ladder needs Q < 2^64 (R18)
   const unsigned long long Qt = (unsigned long long)Q;
@@ -517,27 +524,37 @@ __global__ void __launch_bounds__(kWT) renorm_kernel(double* __restrict__ L, int
   }
 }
 
-// world > 1: every rank's (e'_best, global index) -> the representative; S' is global already
+// world > 1: every rank's {S'_g, e'_best, global index, -}: S' = sum over ranks in rank order
+// (the same on every rank, whatever NCCL's reduction order), the representative = the best
+// (e', index) pair, ties -> lowest index
 __global__ void pick_kernel(const double* __restrict__ all, int G, Scalars* sc) {
-  double bw = -INFINITY;
+  double bw = -INFINITY, S2 = 0.0;
   long long bi = 0x7fffffffffffffffLL;
   for (int g = 0; g < G; ++g) {
     long long ig;
-    memcpy(&ig, &all[2 * g + 1], 8);
-    better(bw, bi, all[2 * g], ig);
+    memcpy(&ig, &all[4 * g + 2], 8);
+    S2 += all[4 * g];
+    better(bw, bi, all[4 * g + 1], ig);
   }
+  sc->S2 = S2;
   sc->rep = bi;
-  sc->wbest = bw / sc->S2;
+  sc->wbest = bw / S2;
 }
 
-__global__ void qd_kernel(const Scalars* sc, long long* out) {  // (Q_g, D_g) for the allgather
+// {Q_g, D_g, m'_g, -} for the allgather that feeds plan_kernel (one collective for the ladder
+// totals and the survivors' max of L)
+__global__ void qd_kernel(const Scalars* sc, long long* out) {
   out[0] = (long long)sc->Q;
   out[1] = sc->D;
+  memcpy(&out[2], &sc->m2, 8);
+  out[3] = 0;
 }
 
-__global__ void best_kernel(const Scalars* sc, double* out) {  // (e'_best, index) for a7
-  out[0] = sc->wbest;
-  memcpy(&out[1], &sc->rep, 8);
+__global__ void best_kernel(const Scalars* sc, double* out) {  // {S'_g, e'_best, index, -}
+  out[0] = sc->S2;
+  out[1] = sc->wbest;
+  memcpy(&out[2], &sc->rep, 8);
+  out[3] = 0.0;
 }
 
 // ---------------------------------------------------------------- transport fallback (pack)
@@ -623,9 +640,9 @@ static mcs_status plan_transfers(mcs_ctx* c, long long* n_send_items, long long*
                                  std::vector<size_t>& rb, std::vector<size_t>& ro) {
   const int G = c->world, me = c->rank;
   const long long* dQD = reinterpret_cast<const long long*>(c->d_xg);
-  std::vector<long long> QD(2 * G);
+  std::vector<long long> QD(4 * G);
   Scalars hs;
-  MCS_CUDA(cudaMemcpyAsync(QD.data(), dQD, sizeof(long long) * 2 * G, cudaMemcpyDeviceToHost,
+  MCS_CUDA(cudaMemcpyAsync(QD.data(), dQD, sizeof(long long) * 4 * G, cudaMemcpyDeviceToHost,
                            c->stream));
   MCS_CUDA(cudaMemcpyAsync(&hs, c->d_scal, sizeof(Scalars), cudaMemcpyDeviceToHost, c->stream));
   MCS_CUDA(cudaStreamSynchronize(c->stream));
@@ -633,8 +650,8 @@ static mcs_status plan_transfers(mcs_ctx* c, long long* n_send_items, long long*
   std::vector<int64_t> D(G), doff(G), clones(G), send((size_t)G * G, 0);
   std::vector<uint64_t> qo(G);
   for (int g = 0; g < G; ++g) {
-    Q[g] = (uint64_t)QD[2 * g];
-    D[g] = QD[2 * g + 1];
+    Q[g] = (uint64_t)QD[4 * g];
+    D[g] = QD[4 * g + 1];
   }
   uint64_t Qt = 0;
   int64_t Dt = 0;
@@ -751,10 +768,9 @@ mcs_status launch_weights_resample(mcs_ctx* c, uint32_t U) {
     // every rank's (Q_g, D_g) on the device, then the plan; the allgather also orders every
     // rank's ladder kernel (its dead list) before any rank's draws read it over peer memory
     long long* dQD = reinterpret_cast<long long*>(c->d_xg);
-    qd_kernel<<<1, 1, 0, st>>>(sc, dQD + 2 * c->world);
-    MCS_TRY(dist_allgather_dev(c, dQD + 2 * c->world, dQD, 16));
+    qd_kernel<<<1, 1, 0, st>>>(sc, dQD + 4 * c->world);
+    MCS_TRY(dist_allgather_dev(c, dQD + 4 * c->world, dQD, 32));
     plan_kernel<<<1, 1, 0, st>>>(dQD, c->world, c->rank, sc, c->d_plan);
-    MCS_TRY(dist_allreduce_f64(c, &sc->m2, 1, 1));
     if (!p2p) {
       MCS_TRY(plan_transfers(c, &n_send, &n_recv, sb, so, rb, ro));
       MCS_TRY(ensure_xfer(c, std::max(n_send, n_recv)));
@@ -806,11 +822,10 @@ mcs_status launch_weights_resample(mcs_ctx* c, uint32_t U) {
   renorm_kernel<<<g, kWT, 0, st>>>(c->d_L, N, sc, c->d_flags, la.C, da.split, c->gbase,
                                    single ? 1 : 0, c->d_e, c->d_partials,
                                    c->d_partials + g, reinterpret_cast<long long*>(c->d_ipartials));
-  if (!single) {
-    MCS_TRY(dist_allreduce_f64(c, &sc->S2, 1, 0));
-    double* dB = reinterpret_cast<double*>(c->d_xg) + 2 * (c->world + 1);
-    best_kernel<<<1, 1, 0, st>>>(sc, dB + 2 * c->world);
-    MCS_TRY(dist_allgather_dev(c, dB + 2 * c->world, dB, 16));
+  if (!single) {  // one allgather: every rank's S'_g and best (e', index)
+    double* dB = reinterpret_cast<double*>(c->d_xg) + 4 * (c->world + 1);
+    best_kernel<<<1, 1, 0, st>>>(sc, dB + 4 * c->world);
+    MCS_TRY(dist_allgather_dev(c, dB + 4 * c->world, dB, 32));
     pick_kernel<<<1, 1, 0, st>>>(dB, c->world, sc);
   }
   return cudaGetLastError() == cudaSuccess ? MCS_OK : MCS_E_CUDA;
