@@ -115,23 +115,40 @@ def own_peaks():
         return {}
 
 
-def committed_ncu_context():
-    """FMA-pipe and issue activity of the sweep from the committed ncu summary (context for the
-    roofline: the kernel is issue/FMA-pipe limited, not memory limited)."""
+def committed_ncu_context(useful_probe_bytes=None):
+    """FMA-pipe and issue activity of the sweep from the committed ncu summary of the kernel
+    this tree builds (context for the roofline: the kernel is issue / FMA-pipe limited, not
+    memory limited), and the north star's hash-probe sector efficiency: the algorithmic probe
+    bytes of one launch over the bytes of the L1 / L2 sectors the launch requested."""
     import glob
     out = {}
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_sweep_v*_ncu.txt")),
-                   key=lambda f: int(f.rsplit("_v", 1)[1].split("_")[0]))
+    pref = os.path.join(ROOT, "profiles", "r02_sweep_v16_ncu.txt")
+    files = [pref] if os.path.exists(pref) else sorted(
+        f for f in glob.glob(os.path.join(ROOT, "profiles", "r*_sweep_v*_ncu.txt"))
+        if "experiment" not in f)
     if not files:
         return None
+    raw = {}
     for line in open(files[-1]):
         parts = line.split()
-        if len(parts) >= 2 and parts[0] in (
-                "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
-                "smsp__issue_active.avg.pct_of_peak_sustained_active",
-                "l1tex__t_sector_hit_rate.pct", "lts__t_sector_hit_rate.pct",
-                "l1tex__throughput.avg.pct_of_peak_sustained_active"):
-            out[parts[0].split(".")[0]] = float(parts[1]) / 100.0
+        if len(parts) >= 2:
+            try:
+                raw[parts[0]] = float(parts[1])
+            except ValueError:
+                pass
+    for k in ("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
+              "smsp__issue_active.avg.pct_of_peak_sustained_active",
+              "l1tex__t_sector_hit_rate.pct", "lts__t_sector_hit_rate.pct",
+              "l1tex__throughput.avg.pct_of_peak_sustained_active"):
+        if k in raw:
+            out[k.split(".")[0]] = raw[k] / 100.0
+    l1 = raw.get("l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum")
+    l2 = raw.get("lts__t_sectors_srcunit_tex_op_read.sum")
+    if useful_probe_bytes and l1 and l2:
+        out["probe_sector_efficiency"] = {"l1": useful_probe_bytes / (32.0 * l1),
+                                          "l2": useful_probe_bytes / (32.0 * l2),
+                                          "note": "algorithmic probe bytes / requested sector "
+                                                  "bytes (> 1: lanes share sectors)"}
     out["source"] = os.path.relpath(files[-1], ROOT)
     return out
 
@@ -466,7 +483,7 @@ def run_gpu(args):
                      "flops_per_launch": flops, "sweep_ms": sweep_avg,
                      "l2_gather_GBps": gather / (sweep_avg * 1e-3) / 1e9,
                      "gather": gather_roofline(gather, sweep_avg),
-                     "ncu": committed_ncu_context()},
+                     "ncu": committed_ncu_context(gather)},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(36 * S),
                 "d2h_bytes_per_step": int(16 * N + 4 + 8), "ms_per_step": 1e3 * e2e_mean},
         "gpu_launches": LAUNCHES_PER_UPDATE * args.steps,

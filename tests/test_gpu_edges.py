@@ -195,3 +195,24 @@ def test_combine_shapes_agree_bitwise():
         np.testing.assert_array_equal(g0[k][:39999], g1[k], err_msg=k)
     np.testing.assert_array_equal(s0["pose12"][:39999], s1["pose12"])
     np.testing.assert_array_equal(s0["kf_pose12"][:39999], s1["kf_pose12"])
+
+
+def test_keyframe_bbox_extent_limit():
+    """mcs.h: a keyframe's occupied cells must fit 2047 x 2048 x 1024 cells (the 32-bit
+    bbox-local table keys); one cell more on any axis is MCS_E_INVALID_ARG with no keyframe
+    added, exactly the limit is accepted."""
+    r = 0.5
+    cov = np.tile(np.array([0.5, 0, 0, 0.5, 0, 0.5], np.float32), (2, 1))
+    with mcs.Context(4, 4, 8, voxel_resolution=r) as ctx:
+        for axis, cells in ((0, 2047), (1, 2048), (2, 1024)):
+            for extra, ok in ((0, True), (1, False)):
+                m = np.zeros((2, 3), np.float32)
+                m[1, axis] = (cells - 1 + extra) * r + 0.1  # cells 0 .. cells - 1 + extra
+                before = ctx.sizes[1]
+                if ok:
+                    ctx.add_keyframe(m, cov, float(before))
+                    assert ctx.sizes[1] == before + 1
+                else:
+                    with pytest.raises(mcs.MCSError) as ei:
+                        ctx.add_keyframe(m, cov, float(before))
+                    assert ei.value.status == 1 and ctx.sizes[1] == before
