@@ -590,15 +590,36 @@ __global__ void __launch_bounds__(kSweepThreads, kCorr == MCS_CORR_NN27 ? MCS_NN
     flush();
   }
 #endif
-  if (!active) return;
-  rec(1) = (double)n;
+  if (active) {
+    rec(1) = (double)n;
 #if !MCS_SWEEP_GACC
-  rec(0) = tot(0);
+    rec(0) = tot(0);
 #pragma unroll
-  for (int k = 0; k < 21; ++k) rec(2 + k) = tot(1 + k);
+    for (int k = 0; k < 21; ++k) rec(2 + k) = tot(1 + k);
 #pragma unroll
-  for (int k = 0; k < 6; ++k) rec(23 + k) = tot(22 + k);
+    for (int k = 0; k < 6; ++k) rec(23 + k) = tot(22 + k);
 #endif
+  }
+}
+
+// Point splits (gridDim.y = P > 1 in the sweep): split 0's record of every item becomes the sum
+// of the P records in split order (the same additions a3 made before), one thread per (word,
+// item), so a3 reads one record per item whatever P (a3 reading P records per particle was
+// latency-bound: +0.09 ms at P = 3 for C2, more than the splits saved).
+__global__ void reduce_splits_kernel(double* __restrict__ part, size_t pstride, int nb, int N,
+                                     int capN, int P) {
+  const long long n_items = (long long)nb * N;
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= 29LL * n_items) return;
+  const int k = (int)(t / n_items);
+  const long long rem = t - (long long)k * n_items;
+  const int s = (int)(rem / N), i = (int)(rem - (long long)s * N);  // item s * capN + i
+  double* r = part + (size_t)k * pstride + (size_t)s * capN + i;
+  double v = r[0];
+#pragma unroll
+  for (int q = 1; q < 8; ++q)
+    if (q < P) v += r[(size_t)q * kSlotWords * pstride];
+  r[0] = v;
 }
 
 // Scan preparation (once per update): Sigma_j = lambda3 I + u u^T + v v^T with u, v the two
@@ -662,7 +683,10 @@ void launch_prepare_scan(const float* mean3, const float* cov6, int S, float4* o
 }
 
 #ifndef MCS_SPLIT_TARGET_CTAS
-#define MCS_SPLIT_TARGET_CTAS 1184  // auto point splits aim for two waves of 148 x 4 CTAs
+// auto point splits aim for ~7,000 CTAs (~12 waves of 148 x 4): more, shorter CTAs balance the
+// uneven per-item hit rates (C2 sweep: 1 split 6.27 ms, 2 6.19, 3 6.13, 4 6.17; with a3's
+// extra partial reads the update is fastest at 3); at most 8 splits (small shards)
+#define MCS_SPLIT_TARGET_CTAS 7000
 #endif
 
 int sweep_splits_for(const mcs_ctx* c, int n) {
@@ -678,7 +702,7 @@ void launch_sweep(mcs_ctx* c, int S) {
   int P = sweep_splits_for(c, c->N);
   P = P > c->part_splits ? c->part_splits : P;
   P = P > stages ? stages : P;
-  c->cur_splits = P;
+  c->cur_splits = 1;  // reduce_splits_kernel sums the point splits into split 0's records
   const dim3 grid((n_items + kSweepThreads - 1) / kSweepThreads, P);
   const float inv_r = 1.0f / c->cfg.voxel_resolution;
   static_assert(!(MCS_SWEEP_TMA && MCS_SWEEP_GACC), "the TMA mbarriers follow s_acc");
@@ -706,6 +730,11 @@ void launch_sweep(mcs_ctx* c, int S) {
     sweep_kernel<MCS_CORR_CELL><<<grid, kSweepThreads, smem, c->stream>>>(
         c->d_items, c->d_order, n_items, c->d_scan, S, c->d_kf_meta, inv_r, 0.f, c->d_part,
         pstride);
+  }
+  if (P > 1) {
+    const long long tot = 29LL * n_items;
+    reduce_splits_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, c->stream>>>(
+        c->d_part, pstride, c->cfg.neighbor_count, c->N, c->capN, P);
   }
 }
 
