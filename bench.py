@@ -36,9 +36,9 @@ FLOPS_UNMATCHED = 21.0   # transform + key for an unmatched triple
 GATHER_MATCHED = 44.0    # algorithmic bytes per matched triple: 8-B key + 12-B mu'
 #                          + 24-B Sigma' (the slot layout moves 40 B + the 4-B key per first probe)
 GATHER_UNMATCHED = 8.0   # the key probe of an unmatched triple
-LAUNCHES_PER_UPDATE = 18  # kernels per mcs_update_async: set_params, prepare_scan, select, 7 CUB
-#                           sort kernels, sweep, combine, propagate, exp_sum, ladder, draws,
-#                           renorm, gather_outputs (profiles/r02_launches.csv)
+LAUNCHES_PER_UPDATE = 19  # kernels per mcs_update_async at C2: set_params, prepare_scan, select,
+#                           7 CUB sort kernels, sweep, reduce_splits, combine, propagate, exp_sum,
+#                           ladder, draws, renorm, gather_outputs (profiles/r02_launches.csv)
 
 
 def dist_env():
