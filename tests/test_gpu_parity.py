@@ -358,3 +358,30 @@ def test_all_dead_is_degenerate(c1):
     with make_ctx(s, posterior_floor=2.0) as ctx:
         g = ctx.update(s.scan_mean3, s.scan_cov6, s.D_now, s.U, raise_degenerate=False)
         assert g["status"] == 7 and g["n_dead"] == s.N and np.all(g["donor"] == -1)
+
+
+def test_c2_survival_variant_respawn_full_n():
+    """The C2 survival variant (bench --config c2_survival: particles 1 mm / 0.1 mrad around the
+    truth, ~30 % survive P:190's floors): tens of thousands of donors and clones instead of the
+    headline's one survivor.  Donors bit-exact against the oracle's resampler fed the GPU's l
+    (full N), every clone a copy of its donor's pose, keyframe poses and L, weights on the
+    oracle's normalisation of the new L."""
+    s = synth.c2(sig_t=1e-3, sig_r=1e-4, drift_t=1e-4, drift_r=1e-5)
+    with make_ctx(s) as ctx:
+        g = ctx.update(s.scan_mean3, s.scan_cov6, s.D_now, s.U)
+        st = ctx.get_particles()
+    L, e, w, _, _ = oracle.weights(np.zeros(s.N), g["loglik"])
+    dead, nd = oracle.dead(g["loglik"], w)
+    assert g["n_dead"] == nd and 0.2 * s.N < nd < 0.9 * s.N, nd
+    donor = oracle.resample(e, dead, s.U)
+    np.testing.assert_array_equal(g["donor"], donor)
+    assert len(np.unique(donor[donor >= 0])) > 1000  # many distinct donors
+    idx = np.nonzero(donor >= 0)[0]
+    np.testing.assert_array_equal(st["pose12"][idx], st["pose12"][donor[idx]])
+    np.testing.assert_array_equal(st["kf_pose12"][idx], st["kf_pose12"][donor[idx]])
+    np.testing.assert_array_equal(st["L"][idx], st["L"][donor[idx]])
+    L2 = L.copy()
+    L2[idx] = L[donor[idx]]
+    _, _, w2, _, _ = oracle.weights(L2)
+    np.testing.assert_allclose(g["weight"], w2, rtol=1e-12, atol=1e-300)
+    assert g["representative"] == oracle.representative(w2)
