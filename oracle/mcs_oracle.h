@@ -19,9 +19,16 @@
  * Twist order: (rho, phi) — translation first (R2).
  * Covariance format cov6: (xx, xy, xz, yy, yz, zz).
  *
- * Parity unpinned (no external pin exists): the absolute likelihood scale on
- * synthetic scenes, the pruning-threshold semantics (R17), pre- vs post-update
- * weighting (R13), Eq.10's frame convention (R16).  See DESIGN.md §3.
+ * Pins (tests/test_oracle_pins.py, test_oracle_rules.py, test_oracle_next.py,
+ * test_oracle_diversity.py; golden hand cases in tests/golden/): every function
+ * here is pinned by closed forms, hand cases, invariants or brute force — the
+ * G-slot combine (R4), the unmatched penalty (R8), the posterior floor
+ * and pre/post-update weighting (R13) by hand cases since round 2.  What no pin
+ * can fix are the readings themselves: the absolute likelihood
+ * scale on synthetic scenes (the paper prints no worked example), the
+ * pruning-threshold semantics (R17), Eq.10's frame convention (R16) and the
+ * diversity term as a whole (R35) are interpretations of the paper, implemented
+ * and pinned as stated.
  */
 #ifndef MCS_ORACLE_H
 #define MCS_ORACLE_H
