@@ -434,9 +434,11 @@ mcs_status mcs_create(const mcs_config* cfg, mcs_ctx** out) {
   if (e == cudaSuccess) e = dalloc(c, &c->d_flags, N);
   if (e == cudaSuccess) e = dalloc(c, &c->d_e, N);
   if (e == cudaSuccess) e = dalloc(c, &c->d_xg, 64 * (size_t)(cfg->world_size + 1) + 96);
-  if (e == cudaSuccess) e = mem_alloc(c, &c->d_ladder, 16 * N);
+  // look-back tile states of the ladder scan: 32 B per 1,024-particle tile
+  const size_t ladder_bytes = 32 * ((N + 1023) / 1024 + 1);
   // look-back tile flags carry a launch epoch; zero memory matches no published tile
-  if (e == cudaSuccess) e = cudaMemset(c->d_ladder, 0, 16 * N);
+  if (e == cudaSuccess) e = mem_alloc(c, &c->d_ladder, ladder_bytes);
+  if (e == cudaSuccess) e = cudaMemset(c->d_ladder, 0, ladder_bytes);
   if (e == cudaSuccess) e = mem_alloc(c, &c->d_ladder_scan, 8 * N);
   if (e == cudaSuccess) e = dalloc(c, &c->d_donor, N);
   if (e == cudaSuccess) e = dalloc(c, &c->d_partials, 2 * maxb);

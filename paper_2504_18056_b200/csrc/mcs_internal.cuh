@@ -169,7 +169,8 @@ struct mcs_ctx {
   char* d_xg = nullptr;         // [8][world+1] x 8 B: device allgathers {Q_g, D_g, m'_g, -},
                                 // {S'_g, e'_g, rep_g, -},
                                 // then 12 doubles: the all-reduced pose of mcs_get_global_pose
-  void* d_ladder = nullptr;     // [Ncap] 16-B look-back tile states of the ladder scan (zeroed)
+  void* d_ladder = nullptr;     // 32-B look-back tile states of the ladder scan, one per 1,024
+                                // particles (zeroed at create)
   void* d_ladder_scan = nullptr;  // [Ncap] u64 inclusive survivor ladder C_i
   int32_t* d_donor = nullptr;   // [Ncap]
   double* d_partials = nullptr; // [4][max_blocks]

@@ -90,7 +90,7 @@ struct LadderArgs {
   int32_t* dead_list;       // [N] local dead slots, ascending
   int32_t* donor;           // [N] reset to -1
   int32_t* donor_g;         // [N] reset to -1, or nullptr
-  TileSt* tiles;            // [ceil(N / kTile)] (32 B each, within the 16 N B of d_ladder)
+  TileSt* tiles;            // [ceil(N / kTile)] (32 B each, d_ladder)
   double* partials;         // [ceil(N / kTile)] survivors' max of L per tile
   int single;               // one device: also write the (trivial) global plan
 };
