@@ -133,6 +133,10 @@ struct mcs_ctx {
   bool profiling = false;
   float phase_ms[5] = {0, 0, 0, 0, 0};
   cudaEvent_t ev[6] = {};
+  // a4 runs on a side stream concurrently with a5 / the ladder (fork after a3, join before the
+  // first step that reads keyframe poses of other particles: the draws' clones)
+  cudaStream_t side = nullptr;
+  cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
 
   // keyframe store (a0)
   int K = 0;
@@ -255,7 +259,7 @@ void launch_propagate(mcs_ctx* c);  // D_now from d_scal (launch_set_params)
 // writes D_now and U into d_scal (a tiny kernel: by value, outside any captured graph)
 void launch_set_params(mcs_ctx* c, double D_now, uint32_t U);
 // a5-a7 (+ the exchange steps when world > 1); degenerate status in d_scal
-mcs_status launch_weights_resample(mcs_ctx* c, uint32_t U);
+mcs_status launch_weights_resample(mcs_ctx* c, uint32_t U, cudaEvent_t join = nullptr);
 // isolated respawn on caller arrays (single device)
 mcs_status launch_resample_only(mcs_ctx* c, const double* d_e, const uint8_t* d_dead, int n,
                                 uint32_t U, int32_t* d_donor);

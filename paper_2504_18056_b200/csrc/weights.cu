@@ -735,7 +735,9 @@ bool weights_device_resident(const mcs_ctx* c) {
   return !dist_active(c) || (c->nccl_comm && c->p2p == 1);
 }
 
-mcs_status launch_weights_resample(mcs_ctx* c, uint32_t U) {
+// join: an event the draws (and, across ranks, the allgather that lets other ranks write into
+// this rank's state) must wait for — a4 running concurrently on a side stream
+mcs_status launch_weights_resample(mcs_ctx* c, uint32_t U, cudaEvent_t join) {
   (void)U;  // the uniform reaches the kernels through d_scal (set_params), graph-replay safe
   cudaStream_t st = c->stream;
   const int N = c->N;
@@ -761,6 +763,7 @@ mcs_status launch_weights_resample(mcs_ctx* c, uint32_t U) {
   la.donor_g = c->d_donor_g;
   la.single = single ? 1 : 0;
   ladder_kernel<<<(N + kTile - 1) / kTile, kLT, 0, st>>>(la);
+  if (join) MCS_CUDA(cudaStreamWaitEvent(st, join, 0));  // a4 done: keyframe poses final
   const bool p2p = !single && c->p2p == 1;
   long long n_send = 0, n_recv = 0;
   std::vector<size_t> sb, so, rb, ro;
