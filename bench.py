@@ -173,6 +173,10 @@ CONFIGS = {
     # drift 0.1 mm / 0.01 mrad per keyframe): their likelihoods differ by units, not thousands,
     # so about a third die under P:190's floors and a6 clones a realistic share (the headline
     # C2 collapses to one survivor)
+    "c3": ("c3", 100_000, "C3: {N} particles x 4096-pt scan vs 200 keyframes (forest grid, "
+                          "r = 1 m, 4 lattice-shifted modes, per-particle keyframe poses)"),
+    "c5": ("c5", 100_000, "C5: {N} particles x 4096-pt scan vs 2 x 20 keyframes (two "
+                          "near-identical floors, particles over both)"),
     "c2_survival": ("c2_survival", 100_000,
                     "C2 survival variant: {N} particles at 1 mm / 0.1 mrad spread (keyframe "
                     "drift 0.1 mm / 0.01 mrad) x 4096-pt scan vs 20 keyframes"),
@@ -183,6 +187,10 @@ def make_scene(config: str, particles: int, seed: int = 0):
     import synth
     if config == "c4":
         return synth.c4(seed=seed, N=particles)
+    if config == "c3":
+        return synth.c3(seed=seed, N=particles)
+    if config == "c5":
+        return synth.c5(seed=seed, N=particles)
     if config == "c2_survival":
         return synth.c2(seed=seed, N=particles, sig_t=1e-3, sig_r=1e-4, drift_t=1e-4,
                         drift_r=1e-5)

@@ -421,7 +421,18 @@ __global__ void __launch_bounds__(kWT) draws_kernel(DrawArgs a) {
       if (lane < 12) dpose[(size_t)lane * dcapN + ss] = a.pose[(size_t)lane * a.capN + jj];
       const float4* s4 = reinterpret_cast<const float4*>(a.kfpose + (size_t)jj * a.capK * 12);
       float4* d4 = reinterpret_cast<float4*>(dkf + (size_t)ss * dcapK * 12);
-      for (int k = lane; k < 3 * a.K; k += 32) d4[k] = s4[k];
+      // keyframe poses: 3K float4, four loads in flight per lane (C3: 9.6 KB per clone)
+      const int n4 = 3 * a.K;
+      int k = lane;
+      for (; k + 96 < n4; k += 128) {
+        const float4 x0 = __ldg(s4 + k), x1 = __ldg(s4 + k + 32), x2 = __ldg(s4 + k + 64),
+                     x3 = __ldg(s4 + k + 96);
+        d4[k] = x0;
+        d4[k + 32] = x1;
+        d4[k + 64] = x2;
+        d4[k + 96] = x3;
+      }
+      for (; k < n4; k += 32) d4[k] = __ldg(s4 + k);
       if (lane == 0) {
         double Lc = a.L[jj];
         if (a.split) {  // R34: the donor's draw count from its own rungs
