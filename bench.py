@@ -122,7 +122,7 @@ def committed_ncu_context(useful_probe_bytes=None):
     bytes of one launch over the bytes of the L1 / L2 sectors the launch requested."""
     import glob
     out = {}
-    pref = os.path.join(ROOT, "profiles", "r02_sweep_v16_ncu.txt")
+    pref = os.path.join(ROOT, "profiles", "r02_sweep_ncu.txt")
     files = [pref] if os.path.exists(pref) else sorted(
         f for f in glob.glob(os.path.join(ROOT, "profiles", "r*_sweep_v*_ncu.txt"))
         if "experiment" not in f)
