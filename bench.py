@@ -129,7 +129,13 @@ def committed_ncu_context(useful_probe_bytes=None):
     if not files:
         return None
     raw = {}
+    headers = 0
     for line in open(files[-1]):
+        if line.startswith("# ") and "sweep_kernel" not in line and not line.startswith("# stall"):
+            if headers:
+                break  # the next kernel's section (the summary lists the sweep first)
+        if line.startswith("# ") and "sweep_kernel" in line:
+            headers += 1
         parts = line.split()
         if len(parts) >= 2:
             try:
