@@ -35,6 +35,9 @@ namespace mcs {
 #ifndef MCS_SWEEP_TMA
 #define MCS_SWEEP_TMA 0  // 1: scan stages double-buffered by TMA bulk copies + mbarriers
 #endif
+#ifndef MCS_SWEEP_PACKED_H
+#define MCS_SWEEP_PACKED_H 1  // 1: the H~ path's rows 1-2 as packed (FFMA2/FADD2) column pairs
+#endif
 #ifndef MCS_SWEEP_GACC
 #define MCS_SWEEP_GACC 0  // 1: fp64 stage totals in the (SoA) partial records, not shared memory
 #endif
@@ -262,6 +265,12 @@ __global__ void __launch_bounds__(kSweepThreads, kCorr == MCS_CORR_NN27 ? MCS_NN
   for (int k = 0; k < 21; ++k) h[k] = 0.f;
 #pragma unroll
   for (int k = 0; k < 6; ++k) bv[k] = 0.f;
+#if MCS_SWEEP_PACKED_H
+  // pair accumulators: H(0,1..2), H(1,1..2), the rho-phi rows 1-2 column by column
+  // ((1,3),(2,3)) ((1,4),(2,4)) ((1,5),(2,5)), and b(1..2); their h[]/bv[] words stay 0
+  float2 hp01 = bc(0.f), hp11 = bc(0.f), hq0 = bc(0.f), hq1 = bc(0.f), hq2 = bc(0.f);
+  float2 bp12 = bc(0.f);
+#endif
 
   // continue linear probing (rare): loads into fresh registers q.s*, waited on inside this
   // path, so the common path never inherits a pending scoreboard from it
@@ -314,6 +323,56 @@ __global__ void __launch_bounds__(kSweepThreads, kCorr == MCS_CORR_NN27 ? MCS_NN
     const float2 k0102 = fma2(bc(c12), c0201, mul2(c0102, neg2(sw(c1122))));
     const float k12 = fmaf(c0102.x, c0102.y, -c00 * c12);
     const float id = rcp_approx(fmaf(c00, k00, fmaf(c0102.x, k0102.x, c0102.y * k0102.y)));
+#if MCS_SWEEP_PACKED_H
+    // Omega as o00 and the pairs C = (o01, o02), A = (o11, o12), B = (o12, o22): rows 1-2 of
+    // Omega [m]x then come out column by column as pairs (o12 is formed twice, one FMUL, so
+    // that A and B need no register moves)
+    const float o00 = k00 * id;
+    const float2 oC = mul2(k0102, bc(id));
+    const float2 oA = make_float2(k1122.x * id, k12 * id);
+    // (o12 formed again by an opaque multiply — the same product, in a second register, so
+    // that the compiler does not merge it with A's and move registers to build the pairs)
+    float o12b;
+    asm("mul.rn.f32 %0, %1, %2;" : "=f"(o12b) : "f"(k12), "f"(id));
+    const float2 oB = make_float2(o12b, k1122.y * id);
+    const float ey = eyz.x, ez = eyz.y;
+    // w = Omega e: w0 = o00 ex + o01 ey + o02 ez; (w1, w2) = ex C + ey A + ez B;  l -= e^T w
+    const float w0 = fmaf(o00, ex, fmaf(oC.x, ey, oC.y * ez));
+    const float2 w12 = fma2(bc(ex), oC, fma2(bc(ey), oA, mul2(bc(ez), oB)));
+    const float w1 = w12.x, w2 = w12.y;
+    l = fmaf(-ex, w0, fmaf(-ey, w1, fmaf(-ez, w2, l)));
+    ++n;
+    if (hb) {
+      // H~ = K^T Omega K = [[Omega, -Omega M], [-M^T Omega, M^T Omega M]], M = [m]x; P = Omega M
+      // row 0 scalar; rows 1-2 per column k: (P1k, P2k)
+      const float o01 = oC.x, o02 = oC.y;
+      const float p00 = o01 * mz - o02 * my, p01 = o02 * mx - o00 * mz, p02 = o00 * my - o01 * mx;
+      const float2 pc0 = fma2(oB, bc(-my), mul2(oA, bc(mz)));  // (P10, P20)
+      const float2 pc1 = fma2(oC, bc(-mz), mul2(oB, bc(mx)));  // (P11, P21)
+      const float2 pc2 = fma2(oA, bc(-mx), mul2(oC, bc(my)));  // (P12, P22)
+      h[0] += o00;
+      hp01 = add2(hp01, oC);
+      hp11 = add2(hp11, oA);
+      h[11] += oB.y;
+      h[3] -= p00; h[4] -= p01; h[5] -= p02;
+      hq0 = add2(hq0, neg2(pc0));
+      hq1 = add2(hq1, neg2(pc1));
+      hq2 = add2(hq2, neg2(pc2));
+      // M^T Omega M = -M P
+      h[15] = fmaf(mz, pc0.x, fmaf(-my, pc0.y, h[15]));  // (3,3)
+      h[16] = fmaf(mz, pc1.x, fmaf(-my, pc1.y, h[16]));  // (3,4)
+      h[17] = fmaf(mz, pc2.x, fmaf(-my, pc2.y, h[17]));  // (3,5)
+      h[18] = fmaf(mx, pc1.y, fmaf(-mz, p01, h[18]));    // (4,4)
+      h[19] = fmaf(mx, pc2.y, fmaf(-mz, p02, h[19]));    // (4,5)
+      h[20] = fmaf(my, p02, fmaf(-mx, pc2.x, h[20]));    // (5,5)
+      // b~ = K^T Omega e = [-w ; w x m]
+      bv[0] -= w0;
+      bp12 = add2(bp12, neg2(w12));
+      bv[3] = fmaf(w1, mz, fmaf(-w2, my, bv[3]));
+      bv[4] = fmaf(w2, mx, fmaf(-w0, mz, bv[4]));
+      bv[5] = fmaf(w0, my, fmaf(-w1, mx, bv[5]));
+    }
+#else
     const float o00 = k00 * id, o12 = k12 * id;
     const float2 o1122 = mul2(k1122, bc(id)), o0102 = mul2(k0102, bc(id));
     const float o01 = o0102.x, o02 = o0102.y, o11 = o1122.x, o22 = o1122.y;
@@ -349,6 +408,7 @@ __global__ void __launch_bounds__(kSweepThreads, kCorr == MCS_CORR_NN27 ? MCS_NN
       bv[4] = fmaf(w2, mx, fmaf(-w0, mz, bv[4]));
       bv[5] = fmaf(w0, my, fmaf(-w1, mx, bv[5]));
     }
+#endif
   };
 
   // first probe: hit -> accumulate; empty slot (or the sentinel) -> miss; else keep probing
@@ -470,6 +530,12 @@ __global__ void __launch_bounds__(kSweepThreads, kCorr == MCS_CORR_NN27 ? MCS_NN
   auto flush = [&]() {
     tot(0) += (double)l;
     l = 0.f;
+#if MCS_SWEEP_PACKED_H
+    h[1] = hp01.x; h[2] = hp01.y; h[6] = hp11.x; h[7] = hp11.y;
+    h[8] = hq0.x; h[12] = hq0.y; h[9] = hq1.x; h[13] = hq1.y; h[10] = hq2.x; h[14] = hq2.y;
+    bv[1] = bp12.x; bv[2] = bp12.y;
+    hp01 = hp11 = hq0 = hq1 = hq2 = bp12 = bc(0.f);
+#endif
 #pragma unroll
     for (int k = 0; k < 21; ++k) {
       tot(1 + k) += (double)h[k];
