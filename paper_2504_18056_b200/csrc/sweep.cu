@@ -36,7 +36,8 @@ namespace mcs {
 #define MCS_SWEEP_TMA 0  // 1: scan stages double-buffered by TMA bulk copies + mbarriers
 #endif
 #ifndef MCS_SWEEP_PACKED_H
-#define MCS_SWEEP_PACKED_H 1  // 1: the H~ path's rows 1-2 as packed (FFMA2/FADD2) column pairs
+#define MCS_SWEEP_PACKED_H 2  // 1: the H~ path's rows 1-2 as packed column pairs; 2: all of
+                              // P, phi-phi and b~_phi as pairs (signs folded, undone at flush)
 #endif
 #ifndef MCS_SWEEP_GACC
 #define MCS_SWEEP_GACC 0  // 1: fp64 stage totals in the (SoA) partial records, not shared memory
@@ -266,10 +267,17 @@ __global__ void __launch_bounds__(kSweepThreads, kCorr == MCS_CORR_NN27 ? MCS_NN
 #pragma unroll
   for (int k = 0; k < 6; ++k) bv[k] = 0.f;
 #if MCS_SWEEP_PACKED_H
-  // pair accumulators: H(0,1..2), H(1,1..2), the rho-phi rows 1-2 column by column
-  // ((1,3),(2,3)) ((1,4),(2,4)) ((1,5),(2,5)), and b(1..2); their h[]/bv[] words stay 0
-  float2 hp01 = bc(0.f), hp11 = bc(0.f), hq0 = bc(0.f), hq1 = bc(0.f), hq2 = bc(0.f);
-  float2 bp12 = bc(0.f);
+  // pair accumulators (their h[]/bv[] words stay 0 until flush): H(0,1..2), H(1,1..2), b(1..2)
+  float2 hp01 = bc(0.f), hp11 = bc(0.f), bp12 = bc(0.f);
+#endif
+#if MCS_SWEEP_PACKED_H >= 2
+  // ((1,3), (2,3)), and with the second lane negated: ((0,4), (0,5)) ((1,4), (1,5))
+  // ((2,4), (2,5)) ((3,4), (3,5)) ((4,4), (4,5)) (b4, b5)
+  float2 hy = bc(0.f), hx0 = bc(0.f), hx1 = bc(0.f), hx2 = bc(0.f), hf34 = bc(0.f),
+         hf45 = bc(0.f), bp45 = bc(0.f);
+#elif MCS_SWEEP_PACKED_H
+  // the rho-phi rows 1-2 column by column: ((1,3),(2,3)) ((1,4),(2,4)) ((1,5),(2,5))
+  float2 hq0 = bc(0.f), hq1 = bc(0.f), hq2 = bc(0.f);
 #endif
 
   // continue linear probing (rare): loads into fresh registers q.s*, waited on inside this
@@ -342,6 +350,40 @@ __global__ void __launch_bounds__(kSweepThreads, kCorr == MCS_CORR_NN27 ? MCS_NN
     const float w1 = w12.x, w2 = w12.y;
     l = fmaf(-ex, w0, fmaf(-ey, w1, fmaf(-ez, w2, l)));
     ++n;
+#if MCS_SWEEP_PACKED_H >= 2
+    if (hb) {
+      // H~ = K^T Omega K = [[Omega, -Omega M], [-M^T Omega, M^T Omega M]], M = [m]x; P = Omega M
+      // as X_r = (P_r1, -P_r2) = mx (Omega_r2, Omega_r1) - Omega_r0 (mz, my)  (r = 0, 1, 2),
+      // Y = (P10, P20) = mz A - my B and the scalar P00
+      const float2 mzy = sw(myz);
+      const float o01 = oC.x, o02 = oC.y;
+      const float2 X0 = fma2(bc(mx), sw(oC), mul2(bc(-o00), mzy));
+      const float2 X1 = fma2(bc(mx), sw(oA), mul2(bc(-o01), mzy));
+      const float2 X2 = fma2(bc(mx), sw(oB), mul2(bc(-o02), mzy));
+      const float2 Y = fma2(bc(-my), oB, mul2(bc(mz), oA));
+      const float p00 = o01 * mz - o02 * my;
+      h[0] += o00;
+      hp01 = add2(hp01, oC);
+      hp11 = add2(hp11, oA);
+      h[11] += oB.y;
+      h[3] -= p00;
+      hx0 = add2(hx0, neg2(X0));
+      hx1 = add2(hx1, neg2(X1));
+      hx2 = add2(hx2, neg2(X2));
+      hy = add2(hy, neg2(Y));
+      // M^T Omega M = -M P:  (3,3) = mz P10 - my P20;  ((3,4), -(3,5)) = mz X1 - my X2;
+      // ((4,4), -(4,5)) = mx X2 - mz X0;  (5,5) = my P02 - mx P12
+      h[15] = fmaf(mz, Y.x, fmaf(-my, Y.y, h[15]));
+      hf34 = fma2(bc(mz), X1, fma2(bc(-my), X2, hf34));
+      hf45 = fma2(bc(mx), X2, fma2(bc(-mz), X0, hf45));
+      h[20] = fmaf(mx, X1.y, fmaf(-my, X0.y, h[20]));
+      // b~ = K^T Omega e = [-w ; w x m]:  b3 = w1 mz - w2 my;  (b4, -b5) = mx (w2, w1) - w0 (mz, my)
+      bv[0] -= w0;
+      bp12 = add2(bp12, neg2(w12));
+      bv[3] = fmaf(w1, mz, fmaf(-w2, my, bv[3]));
+      bp45 = fma2(bc(mx), sw(w12), fma2(bc(-w0), mzy, bp45));
+    }
+#else
     if (hb) {
       // H~ = K^T Omega K = [[Omega, -Omega M], [-M^T Omega, M^T Omega M]], M = [m]x; P = Omega M
       // row 0 scalar; rows 1-2 per column k: (P1k, P2k)
@@ -372,6 +414,7 @@ __global__ void __launch_bounds__(kSweepThreads, kCorr == MCS_CORR_NN27 ? MCS_NN
       bv[4] = fmaf(w2, mx, fmaf(-w0, mz, bv[4]));
       bv[5] = fmaf(w0, my, fmaf(-w1, mx, bv[5]));
     }
+#endif
 #else
     const float o00 = k00 * id, o12 = k12 * id;
     const float2 o1122 = mul2(k1122, bc(id)), o0102 = mul2(k0102, bc(id));
@@ -531,10 +574,18 @@ __global__ void __launch_bounds__(kSweepThreads, kCorr == MCS_CORR_NN27 ? MCS_NN
     tot(0) += (double)l;
     l = 0.f;
 #if MCS_SWEEP_PACKED_H
-    h[1] = hp01.x; h[2] = hp01.y; h[6] = hp11.x; h[7] = hp11.y;
+    h[1] = hp01.x; h[2] = hp01.y; h[6] = hp11.x; h[7] = hp11.y; bv[1] = bp12.x; bv[2] = bp12.y;
+    hp01 = hp11 = bp12 = bc(0.f);
+#endif
+#if MCS_SWEEP_PACKED_H >= 2
+    h[8] = hy.x; h[12] = hy.y;
+    h[4] = hx0.x; h[5] = -hx0.y; h[9] = hx1.x; h[10] = -hx1.y; h[13] = hx2.x; h[14] = -hx2.y;
+    h[16] = hf34.x; h[17] = -hf34.y; h[18] = hf45.x; h[19] = -hf45.y;
+    bv[4] = bp45.x; bv[5] = -bp45.y;
+    hy = hx0 = hx1 = hx2 = hf34 = hf45 = bp45 = bc(0.f);
+#elif MCS_SWEEP_PACKED_H
     h[8] = hq0.x; h[12] = hq0.y; h[9] = hq1.x; h[13] = hq1.y; h[10] = hq2.x; h[14] = hq2.y;
-    bv[1] = bp12.x; bv[2] = bp12.y;
-    hp01 = hp11 = hq0 = hq1 = hq2 = bp12 = bc(0.f);
+    hq0 = hq1 = hq2 = bc(0.f);
 #endif
 #pragma unroll
     for (int k = 0; k < 21; ++k) {
