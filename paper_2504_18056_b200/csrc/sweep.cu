@@ -35,6 +35,9 @@ namespace mcs {
 #ifndef MCS_SWEEP_TMA
 #define MCS_SWEEP_TMA 0  // 1: scan stages double-buffered by TMA bulk copies + mbarriers
 #endif
+#ifndef MCS_SWEEP_CONVERGENT
+#define MCS_SWEEP_CONVERGENT 1  // 1: threads without an item run the stage loop (always missing)
+#endif
 #ifndef MCS_SWEEP_PACKED_H
 #define MCS_SWEEP_PACKED_H 2  // 1: the H~ path's rows 1-2 as packed column pairs; 2: all of
                               // P, phi-phi and b~_phi as pairs (signs folded, undone at flush)
@@ -200,6 +203,14 @@ __global__ void __launch_bounds__(kSweepThreads, kCorr == MCS_CORR_NN27 ? MCS_NN
   const bool active = kf >= 0;
   const bool hb = active && (__float_as_int(inf.z) & 1);
   KfMeta m;
+#if MCS_SWEEP_CONVERGENT
+  // a thread without an item runs the stage loop with the others, on keyframe 0's table with an
+  // empty bbox: every point reads that table's always-empty sentinel slot and misses, and the
+  // record is never written.  The loop then stays warp-convergent, and ptxas keeps its bound in
+  // a uniform register instead of a spilled one
+  m = kmeta[active ? kf : 0];
+  if (!active) m.ex = m.ey = m.ez = 0;
+#else
   if (active) {
     m = kmeta[kf];
   } else {
@@ -209,6 +220,7 @@ __global__ void __launch_bounds__(kSweepThreads, kCorr == MCS_CORR_NN27 ? MCS_NN
     m.shift = 31;
     m.mask = 0;
   }
+#endif
   const unsigned int offx = (unsigned)__float_as_int(kMagic) + (unsigned)m.ox;
   const unsigned int offy = (unsigned)__float_as_int(kMagic) + (unsigned)m.oy;
   const unsigned int offz = (unsigned)__float_as_int(kMagic) + (unsigned)m.oz;
@@ -242,7 +254,7 @@ __global__ void __launch_bounds__(kSweepThreads, kCorr == MCS_CORR_NN27 ? MCS_NN
   // the (unconditional) first-probe loads; volatile: the compiler may not sink them towards
   // their use (that would undo the look-ahead)
   auto load = [&](Probe& p) {
-    if (active) ld_slot(m.slots + 4 * (size_t)p.h, p.s0, p.s1, p.s2);
+    if (MCS_SWEEP_CONVERGENT || active) ld_slot(m.slots + 4 * (size_t)p.h, p.s0, p.s1, p.s2);
   };
   auto issue = [&](uint32_t j) {
     Probe p = locate(j);
@@ -254,7 +266,7 @@ __global__ void __launch_bounds__(kSweepThreads, kCorr == MCS_CORR_NN27 ? MCS_NN
   // share one scoreboard, so a later wait would also drain the new ones)
   auto issue_after = [&](uint32_t j, unsigned int kdep) {
     Probe p = locate(j);
-    if (active & (kdep != 0xFFFFFFFDu)) ld_slot(m.slots + 4 * (size_t)p.h, p.s0, p.s1, p.s2);
+    if ((MCS_SWEEP_CONVERGENT || active) & (kdep != 0xFFFFFFFDu)) ld_slot(m.slots + 4 * (size_t)p.h, p.s0, p.s1, p.s2);
     return p;
   };
 
@@ -702,7 +714,7 @@ __global__ void __launch_bounds__(kSweepThreads, kCorr == MCS_CORR_NN27 ? MCS_NN
     __syncthreads();
     for (int k = threadIdx.x; k < cnt * 3; k += kSweepThreads) s_pt[k] = scan[3 * base + k];
     __syncthreads();
-    if (!active) continue;
+    if (!MCS_SWEEP_CONVERGENT && !active) continue;
     stage(cnt);
     flush();
   }
