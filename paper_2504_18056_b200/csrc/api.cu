@@ -796,10 +796,10 @@ static mcs_status run_update_body(mcs_ctx* ctx, int n_pts, uint32_t U) {
   const bool div = ctx->cfg.diversity_weight != 0.0;
   record(ctx, 0);
   if (div) MCS_TRY(launch_diversity_snapshot(ctx));  // R35: translations at the start
-  // the default path (one GN step, pre-update weighting, no R35) runs a4 on a side stream,
-  // concurrently with a5 and the ladder: nothing before the draws reads keyframe poses
+  // the default path (one GN step, pre-update weighting, no R35) runs a4 inside a5-a7, on a
+  // side stream beside the ladder and for the survivors only: nothing before the draws reads
+  // keyframe poses, and a dead particle's are replaced by its donor's
   const bool fork = iters == 1 && !post && !div;
-  cudaEvent_t join = nullptr;
   for (int it = 0; it < iters; ++it) {  // R12: each iteration is a full a1-a4 pass
     MCS_TRY(launch_select(ctx, kSelectUpdate));                         // a1
     if (it == 0) record(ctx, 1);
@@ -807,18 +807,7 @@ static mcs_status run_update_body(mcs_ctx* ctx, int n_pts, uint32_t U) {
     if (it == 0) record(ctx, 2);
     launch_combine(ctx, n_pts, (it == 0 && !post) ? kCombineUpdateWeight : kCombineUpdate,
                    nullptr, nullptr, nullptr, nullptr, nullptr, nullptr);  // a3 (+ L += l)
-    if (fork) {                                                         // a4 on the side
-      CUDA_TRY(ctx, cudaEventRecord(ctx->fork_ev, ctx->stream));
-      CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->side, ctx->fork_ev, 0));
-      cudaStream_t main = ctx->stream;
-      ctx->stream = ctx->side;
-      launch_propagate(ctx);
-      ctx->stream = main;
-      CUDA_TRY(ctx, cudaEventRecord(ctx->join_ev, ctx->side));
-      join = ctx->join_ev;
-    } else {
-      launch_propagate(ctx);                                            // a4
-    }
+    if (!fork) launch_propagate(ctx);                                   // a4
   }
   if (div) MCS_TRY(launch_diversity_apply(ctx));  // R35: t_i += eta d_i after the GN step(s)
   if (post) {  // R13 variant: weight with l re-evaluated at the updated poses
@@ -828,7 +817,7 @@ static mcs_status run_update_body(mcs_ctx* ctx, int n_pts, uint32_t U) {
                    nullptr);
   }
   record(ctx, 3);
-  const mcs_status s = launch_weights_resample(ctx, U, join);           // a5-a7 (+ exchanges)
+  const mcs_status s = launch_weights_resample(ctx, U, fork);           // (a4,) a5-a7
   record(ctx, 4);
   return s;
 }

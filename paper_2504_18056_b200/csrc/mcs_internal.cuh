@@ -255,11 +255,23 @@ enum { kCombineEval = 0, kCombineUpdateWeight = 1, kCombineUpdate = 2, kCombineW
 void launch_combine(mcs_ctx* c, int S, int mode, double* slot_l, float* slot_H21,
                     float* slot_b6, int32_t* slot_n, int32_t* slot_kf, uint8_t* loop_out);
 // a4
-void launch_propagate(mcs_ctx* c);  // D_now from d_scal (launch_set_params)
+// a4 over every loop particle (kPropAll); over the survivors of this update's a6 only
+// (kPropSurvivors: a dead particle's keyframe poses are replaced by its donor's clone); or, after
+// a6 found no survivor at all (respawn skipped, sc->status = MCS_E_DEGENERATE), over the rest
+// (kPropIfDegenerate, a no-op otherwise).  D_now from d_scal (launch_set_params)
+enum { kPropAll = 0, kPropSurvivors = 1, kPropIfDegenerate = 2 };
+void launch_propagate(mcs_ctx* c, int mode = kPropAll);
+// a6's dead test (R17) — the ladder and the survivor-only a4 take the same decision
+__device__ __forceinline__ bool particle_dead(double l_i, double lstar, double e_i, double S,
+                                              double rel_floor, double post_floor) {
+  return (l_i - lstar < rel_floor) || (e_i / S < post_floor);
+}
 // writes D_now and U into d_scal (a tiny kernel: by value, outside any captured graph)
 void launch_set_params(mcs_ctx* c, double D_now, uint32_t U);
 // a5-a7 (+ the exchange steps when world > 1); degenerate status in d_scal
-mcs_status launch_weights_resample(mcs_ctx* c, uint32_t U, cudaEvent_t join = nullptr);
+// fork_a4: run a4 (survivors only) on c->side once the dead set is decided (after the S
+// allreduce), concurrently with the ladder, joined before the draws
+mcs_status launch_weights_resample(mcs_ctx* c, uint32_t U, bool fork_a4 = false);
 // isolated respawn on caller arrays (single device)
 mcs_status launch_resample_only(mcs_ctx* c, const double* d_e, const uint8_t* d_dead, int n,
                                 uint32_t U, int32_t* d_donor);

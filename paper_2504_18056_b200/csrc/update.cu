@@ -575,11 +575,19 @@ __global__ void propagate_kernel(float* __restrict__ kfpose, int capK, int K, in
                                  const uint8_t* __restrict__ flags, const int32_t* __restrict__ to,
                                  const double* __restrict__ psi, int capN,
                                  const double* __restrict__ D,
-                                 const Scalars* __restrict__ sc) {
+                                 const Scalars* __restrict__ sc, int mode,
+                                 const double* __restrict__ l, const double* __restrict__ e,
+                                 double rel_floor, double post_floor) {
   const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= (long long)N * K) return;
   const int i = (int)(t / K), k = (int)(t - (long long)i * K);
   if (!(flags[i] & 2)) return;
+  if (mode == kPropSurvivors) {  // a dead particle's keyframe poses are its donor's (a6)
+    if (particle_dead(l[i], sc->lstar, e[i], sc->S, rel_floor, post_floor)) return;
+  } else if (mode == kPropIfDegenerate) {  // no survivor: a6 kept every state, propagate the
+    if (sc->status != (int)MCS_E_DEGENERATE) return;  // ones kPropSurvivors skipped
+    if (!particle_dead(l[i], sc->lstar, e[i], sc->S, rel_floor, post_floor)) return;
+  }
   const int t_o = to[i];
   if (k < t_o) return;  // older keyframes untouched (R15)
   const double D_now = sc->D_now;
@@ -605,12 +613,14 @@ __global__ void propagate_kernel(float* __restrict__ kfpose, int capK, int K, in
   q4[2] = make_float4(T[8], T[9], T[10], T[11]);
 }
 
-void launch_propagate(mcs_ctx* c) {
+void launch_propagate(mcs_ctx* c, int mode) {
   const long long total = (long long)c->N * c->K;
   if (total == 0) return;
   const int grid = (int)((total + 255) / 256);
   propagate_kernel<<<grid, 256, 0, c->stream>>>(c->d_kfpose, c->capK, c->K, c->N, c->d_flags,
-                                                c->d_to, c->d_psi, c->capN, c->d_D, c->d_scal);
+                                                c->d_to, c->d_psi, c->capN, c->d_D, c->d_scal,
+                                                mode, c->d_l, c->d_e, c->cfg.loglik_rel_floor,
+                                                c->cfg.posterior_floor);
 }
 
 // the per-update scalars, by value at launch (outside any captured graph)

@@ -141,8 +141,7 @@ __global__ void __launch_bounds__(kLT) ladder_kernel(LadderArgs a) {
     if (a.dead_in) {
       dead = a.dead_in[i] != 0;
     } else {
-      const double wi = ei / S;
-      dead = (a.l[i] - lstar < a.rel_floor) || (wi < a.post_floor);  // P:190, R17
+      dead = particle_dead(a.l[i], lstar, ei, S, a.rel_floor, a.post_floor);  // P:190, R17
       if (dead) a.flags[i] |= 8;
     }
     if (!dead) q[k] = (unsigned long long)floor(ei * 4294967296.0);  // rung (R18)
@@ -746,9 +745,10 @@ bool weights_device_resident(const mcs_ctx* c) {
   return !dist_active(c) || (c->nccl_comm && c->p2p == 1);
 }
 
-// join: an event the draws (and, across ranks, the allgather that lets other ranks write into
-// this rank's state) must wait for — a4 running concurrently on a side stream
-mcs_status launch_weights_resample(mcs_ctx* c, uint32_t U, cudaEvent_t join) {
+// fork_a4: a4 runs on the side stream for the survivors only, from the moment the dead set is
+// decided (after the S allreduce) and concurrently with the ladder; the draws (and, across
+// ranks, the allgather that lets other ranks write into this rank's dead slots) wait for it
+mcs_status launch_weights_resample(mcs_ctx* c, uint32_t U, bool fork_a4) {
   (void)U;  // the uniform reaches the kernels through d_scal (set_params), graph-replay safe
   cudaStream_t st = c->stream;
   const int N = c->N;
@@ -760,6 +760,16 @@ mcs_status launch_weights_resample(mcs_ctx* c, uint32_t U, cudaEvent_t join) {
   exp_sum_kernel<<<g, kWT, 0, st>>>(c->d_L, N, &sc->m, c->d_e, c->d_partials, &sc->S,
                                     &sc->counter[1]);
   MCS_TRY(dist_allreduce_f64(c, &sc->S, 1, 0));
+  cudaEvent_t join = nullptr;
+  if (fork_a4) {  // a4 for the survivors, beside the ladder
+    MCS_CUDA(cudaEventRecord(c->fork_ev, st));
+    MCS_CUDA(cudaStreamWaitEvent(c->side, c->fork_ev, 0));
+    c->stream = c->side;
+    launch_propagate(c, kPropSurvivors);
+    c->stream = st;
+    MCS_CUDA(cudaEventRecord(c->join_ev, c->side));
+    join = c->join_ev;
+  }
   // a6: dead set, ladder scan, dead list, local totals
   if (!single) MCS_TRY(dist_peer_setup(c));  // once per context (collective)
   LadderArgs la{};
@@ -790,6 +800,9 @@ mcs_status launch_weights_resample(mcs_ctx* c, uint32_t U, cudaEvent_t join) {
       MCS_TRY(ensure_xfer(c, std::max(n_send, n_recv)));
     }
   }
+  // no survivor anywhere (sc->status, final here): the respawn is skipped and every state kept,
+  // so the particles the survivor-only a4 skipped are propagated after all
+  if (fork_a4) launch_propagate(c, kPropIfDegenerate);
   DrawArgs da{};
   da.C = la.C;
   da.N = N;

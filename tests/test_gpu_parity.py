@@ -360,6 +360,27 @@ def test_all_dead_is_degenerate(c1):
         assert g["status"] == 7 and g["n_dead"] == s.N and np.all(g["donor"] == -1)
 
 
+def test_c2_degenerate_update_keeps_and_propagates_every_state(c2):
+    """S:381 with loop closures: a posterior floor above 1 kills every particle, so a6 skips
+    the respawn and every particle keeps its own updated state — including the keyframe poses
+    the survivor-only a4 had skipped (propagated after all once the ladder finds no survivor).
+    Poses and keyframe poses on every 64th particle vs the oracle's a1-a4."""
+    s = c2
+    idx = np.arange(0, s.N, 64, dtype=np.int32)
+    with make_ctx(s, posterior_floor=2.0) as ctx:
+        g = ctx.update(s.scan_mean3, s.scan_cov6, s.D_now, s.U, raise_degenerate=False)
+        st = ctx.get_particles()
+    assert g["status"] == 7 and g["n_dead"] == s.N and np.all(g["donor"] == -1)
+    pose, kp = s.pose12.copy(), s.kf_pose12.copy()
+    oracle.particles(orc_cfg(s), oracle.Keyframes(s.keyframes, s.D, s.r), s.D_now, pose, kp,
+                     s.scan_mean3, s.scan_cov6, idx=idx)
+    assert np.any(kp[idx] != s.kf_pose12[idx])
+    ang, dt = pose_err(st["pose12"][idx], pose[idx])
+    assert ang.max() <= ROT_TOL and dt.max() <= T_TOL, (ang.max(), dt.max())
+    ak, dk = pose_err(st["kf_pose12"][idx].reshape(-1, 12), kp[idx].reshape(-1, 12))
+    assert ak.max() <= ROT_TOL and dk.max() <= T_TOL, (ak.max(), dk.max())
+
+
 def test_c2_survival_variant_respawn_full_n():
     """The C2 survival variant (bench --config c2_survival: particles 1 mm / 0.1 mrad around the
     truth, ~30 % survive P:190's floors): tens of thousands of donors and clones instead of the
@@ -378,6 +399,17 @@ def test_c2_survival_variant_respawn_full_n():
     assert len(np.unique(donor[donor >= 0])) > 1000  # many distinct donors
     idx = np.nonzero(donor >= 0)[0]
     np.testing.assert_array_equal(st["pose12"][idx], st["pose12"][donor[idx]])
+    # a4 runs for the survivors only (a dead particle's keyframe poses are its donor's): the
+    # clones carry their donors' propagated keyframe poses, and the survivors' match the
+    # oracle's a1-a4 on a subsample
+    np.testing.assert_array_equal(st["kf_pose12"][idx], st["kf_pose12"][donor[idx]])
+    surv = np.nonzero(donor < 0)[0][::37].astype(np.int32)
+    pose, kp = s.pose12.copy(), s.kf_pose12.copy()
+    oracle.particles(orc_cfg(s), oracle.Keyframes(s.keyframes, s.D, s.r), s.D_now, pose, kp,
+                     s.scan_mean3, s.scan_cov6, idx=surv)
+    assert np.any(kp[surv] != s.kf_pose12[surv])  # the oracle propagated them
+    ak, dk = pose_err(st["kf_pose12"][surv].reshape(-1, 12), kp[surv].reshape(-1, 12))
+    assert ak.max() <= ROT_TOL and dk.max() <= T_TOL, (ak.max(), dk.max())
     np.testing.assert_array_equal(st["kf_pose12"][idx], st["kf_pose12"][donor[idx]])
     np.testing.assert_array_equal(st["L"][idx], st["L"][donor[idx]])
     L2 = L.copy()
