@@ -36,9 +36,12 @@ FLOPS_UNMATCHED = 21.0   # transform + key for an unmatched triple
 GATHER_MATCHED = 44.0    # algorithmic bytes per matched triple: 8-B key + 12-B mu'
 #                          + 24-B Sigma' (the slot layout moves 40 B + the 4-B key per first probe)
 GATHER_UNMATCHED = 8.0   # the key probe of an unmatched triple
-LAUNCHES_PER_UPDATE = 19  # kernels per mcs_update_async at C2: set_params, prepare_scan, select,
-#                           7 CUB sort kernels, sweep, reduce_splits, combine, propagate, exp_sum,
-#                           ladder, draws, renorm, gather_outputs (profiles/r02_launches.csv)
+LAUNCHES_PER_UPDATE = 13  # own kernels per mcs_update_async at C2: set_params, prepare_scan,
+#                           select, sweep, reduce_splits, combine, exp_sum, propagate (survivors),
+#                           ladder, propagate (no-op unless no survivor), draws, renorm,
+#                           gather_outputs (profiles/r02_launches.csv)
+LIBRARY_LAUNCHES_PER_UPDATE = 7  # CUB radix sort of the coherence keys inside a1: histogram,
+#                                  exclusive sum, 5 onesweep passes
 
 
 def dist_env():
@@ -501,6 +504,7 @@ def run_gpu(args):
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(36 * S),
                 "d2h_bytes_per_step": int(16 * N + 4 + 8), "ms_per_step": 1e3 * e2e_mean},
         "gpu_launches": LAUNCHES_PER_UPDATE * args.steps,
+        "gpu_launches_library": LIBRARY_LAUNCHES_PER_UPDATE * args.steps,
         "clocks": dict(clocks.summary(), **({"remeasured_after": remeasured} if remeasured
                                              else {})),
         "ms_p10_p50_p90": [float(np.percentile(step_ms, q)) for q in (10, 50, 90)],
