@@ -40,6 +40,11 @@ LAUNCHES_PER_UPDATE = 13  # own kernels per mcs_update_async at C2: set_params, 
 #                           select, sweep, reduce_splits, combine, exp_sum, propagate (survivors),
 #                           ladder, propagate (no-op unless no survivor), draws, renorm,
 #                           gather_outputs (profiles/r02_launches.csv)
+# the paper's own figure (context only, another machine and the whole system)
+PAPER_CONTEXT = {"particles_in_real_time": 100000, "ms_per_frame": [50, 60],
+                 "what": "whole SLAM system per frame (indoor elevator ~50 ms, outdoor forest "
+                         "~60 ms), scan size not stated",
+                 "hardware": "NVIDIA GeForce RTX 4090", "cite": "PAPER.md P:203, P:240"}
 LIBRARY_LAUNCHES_PER_UPDATE = 7  # CUB radix sort of the coherence keys inside a1: histogram,
 #                                  exclusive sum, 5 onesweep passes
 
@@ -513,6 +518,7 @@ def run_gpu(args):
         "match_rate": matched / max(triples, 1),
         "a0_ms_per_keyframe": a0_ms,
         "n_dead": int(out["n_dead"][0]),
+        "paper_context": PAPER_CONTEXT,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"], _ = cpu_baseline(s, args.cpu_budget_s)
