@@ -12,6 +12,8 @@
 // a4, one thread per (particle, keyframe): for updated particles and t_o <= k <= latest,
 //   r_k = (D_k - D_{t_o}) / (D_now - D_{t_o}) (R14, R15); T_k <- T_k exp(r_k psi) (Eq.10, R16).
 #include "mcs_internal.cuh"
+
+#include <algorithm>
 #include "reduce.cuh"
 #include "se3.cuh"
 
@@ -571,52 +573,88 @@ void launch_combine(mcs_ctx* c, int S, int mode, double* slot_l, float* slot_H21
   }
 }
 
-__global__ void propagate_kernel(float* __restrict__ kfpose, int capK, int K, int N,
-                                 const uint8_t* __restrict__ flags, const int32_t* __restrict__ to,
-                                 const double* __restrict__ psi, int capN,
-                                 const double* __restrict__ D,
-                                 const Scalars* __restrict__ sc, int mode,
-                                 const double* __restrict__ l, const double* __restrict__ e,
-                                 double rel_floor, double post_floor) {
-  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= (long long)N * K) return;
-  const int i = (int)(t / K), k = (int)(t - (long long)i * K);
-  if (!(flags[i] & 2)) return;
-  if (mode == kPropSurvivors) {  // a dead particle's keyframe poses are its donor's (a6)
-    if (particle_dead(l[i], sc->lstar, e[i], sc->S, rel_floor, post_floor)) return;
-  } else if (mode == kPropIfDegenerate) {  // no survivor: a6 kept every state, propagate the
-    if (sc->status != (int)MCS_E_DEGENERATE) return;  // ones kPropSurvivors skipped
-    if (!particle_dead(l[i], sc->lstar, e[i], sc->S, rel_floor, post_floor)) return;
-  }
-  const int t_o = to[i];
-  if (k < t_o) return;  // older keyframes untouched (R15)
+// One warp per 32 consecutive particles (grid-stride): each lane decides for its particle
+// whether a4 applies (looped and updated; survivor / dead per mode; D_now > D_{t_o}) and how
+// many keyframes it moves (t_o .. K-1), a warp scan flattens the (particle, keyframe) pairs of
+// the warp, and the lanes take the pairs 32 at a time.  Only the work that exists is spread over
+// the lanes: at C2 (one survivor) a4 is a check per particle, not a thread per (particle,
+// keyframe) — N K threads cost ~0.1 ms at C3's 200 keyframes even when they all return.
+__global__ void __launch_bounds__(256) propagate_kernel(
+    float* __restrict__ kfpose, int capK, int K, int N, const uint8_t* __restrict__ flags,
+    const int32_t* __restrict__ to, const double* __restrict__ psi, int capN,
+    const double* __restrict__ D, const Scalars* __restrict__ sc, int mode,
+    const double* __restrict__ l, const double* __restrict__ e, double rel_floor,
+    double post_floor) {
+  if (mode == kPropIfDegenerate && sc->status != (int)MCS_E_DEGENERATE) return;  // usual case
+  const int lane = threadIdx.x & 31;
+  const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
   const double D_now = sc->D_now;
-  const double den = D_now - D[t_o];
-  if (!(den > 0.0)) return;
-  const double r = (D[k] - D[t_o]) / den;  // Eqs.8-9 (R14)
-  if (r == 0.0) return;
-  double xi[6];
+  for (long long base = gw * 32; base < N; base += nw * 32) {
+    const long long i = base + lane;
+    int cnt = 0, t_o = 0;
+    double den = 0.0;
+    if (i < N && (flags[i] & 2)) {
+      bool act = true;
+      if (mode != kPropAll) {  // kPropSurvivors: a dead particle's keyframe poses are its
+        // donor's (a6); kPropIfDegenerate: no survivor, a6 kept every state
+        const bool dead = particle_dead(l[i], sc->lstar, e[i], sc->S, rel_floor, post_floor);
+        act = (mode == kPropSurvivors) ? !dead : dead;
+      }
+      if (act) {
+        t_o = to[i];
+        den = D_now - D[t_o];
+        if (den > 0.0) cnt = K - t_o;  // keyframes t_o .. K-1; older ones untouched (R15)
+      }
+    }
+    int inc = cnt;  // inclusive scan of the pair counts over the warp
 #pragma unroll
-  for (int c = 0; c < 6; ++c) xi[c] = r * psi[(size_t)c * capN + i];
-  MCS_DCHECK(k >= 0 && k < K && K <= capK);
-  float* Tk = kfpose + ((size_t)i * capK + k) * 12;
-  float T[12];
-  const float4* p4 = reinterpret_cast<const float4*>(Tk);
-  float4 v0 = p4[0], v1 = p4[1], v2 = p4[2];
-  T[0] = v0.x; T[1] = v0.y; T[2] = v0.z; T[3] = v0.w;
-  T[4] = v1.x; T[5] = v1.y; T[6] = v1.z; T[7] = v1.w;
-  T[8] = v2.x; T[9] = v2.y; T[10] = v2.z; T[11] = v2.w;
-  pose_right_update(T, xi);  // Eq.10
-  float4* q4 = reinterpret_cast<float4*>(Tk);
-  q4[0] = make_float4(T[0], T[1], T[2], T[3]);
-  q4[1] = make_float4(T[4], T[5], T[6], T[7]);
-  q4[2] = make_float4(T[8], T[9], T[10], T[11]);
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += v;
+    }
+    const int total = __shfl_sync(0xffffffffu, inc, 31);
+    for (int p0 = 0; p0 < total; p0 += 32) {  // warp-uniform trip count
+      const int p = p0 + lane;
+      int j = 0;  // owner lane: the first with inc_j > p
+#pragma unroll
+      for (int step = 16; step > 0; step >>= 1) {
+        const int v = __shfl_sync(0xffffffffu, inc, j + step - 1);
+        if (v <= p) j += step;
+      }
+      const int inc_j = __shfl_sync(0xffffffffu, inc, j);
+      const int cnt_j = __shfl_sync(0xffffffffu, cnt, j);
+      const int to_j = __shfl_sync(0xffffffffu, t_o, j);
+      const double den_j = __shfl_sync(0xffffffffu, den, j);
+      if (p >= total) continue;
+      const int k = to_j + (p - (inc_j - cnt_j));
+      const long long ij = base + j;
+      const double r = (D[k] - D[to_j]) / den_j;  // Eqs.8-9 (R14)
+      if (r == 0.0) continue;                      // k = t_o (and equal path lengths)
+      double xi[6];
+#pragma unroll
+      for (int c = 0; c < 6; ++c) xi[c] = r * psi[(size_t)c * capN + ij];
+      MCS_DCHECK(k >= 0 && k < K && K <= capK && ij < N);
+      float* Tk = kfpose + ((size_t)ij * capK + k) * 12;
+      float T[12];
+      const float4* p4 = reinterpret_cast<const float4*>(Tk);
+      const float4 v0 = p4[0], v1 = p4[1], v2 = p4[2];
+      T[0] = v0.x; T[1] = v0.y; T[2] = v0.z; T[3] = v0.w;
+      T[4] = v1.x; T[5] = v1.y; T[6] = v1.z; T[7] = v1.w;
+      T[8] = v2.x; T[9] = v2.y; T[10] = v2.z; T[11] = v2.w;
+      pose_right_update(T, xi);  // Eq.10
+      float4* q4 = reinterpret_cast<float4*>(Tk);
+      q4[0] = make_float4(T[0], T[1], T[2], T[3]);
+      q4[1] = make_float4(T[4], T[5], T[6], T[7]);
+      q4[2] = make_float4(T[8], T[9], T[10], T[11]);
+    }
+  }
 }
 
 void launch_propagate(mcs_ctx* c, int mode) {
-  const long long total = (long long)c->N * c->K;
-  if (total == 0) return;
-  const int grid = (int)((total + 255) / 256);
+  if ((long long)c->N * c->K == 0) return;
+  const long long warps = (c->N + 31) / 32;
+  const int grid = (int)std::min<long long>((warps + 7) / 8, 148LL * 16);
   propagate_kernel<<<grid, 256, 0, c->stream>>>(c->d_kfpose, c->capK, c->K, c->N, c->d_flags,
                                                 c->d_to, c->d_psi, c->capN, c->d_D, c->d_scal,
                                                 mode, c->d_l, c->d_e, c->cfg.loglik_rel_floor,
