@@ -46,7 +46,8 @@ static thread_local std::string g_create_error;
 
 // ------------------------------------------------------------------ small device kernels
 __global__ void fill_kf_from_current_kernel(const float* __restrict__ pose, int capN, int N,
-                                            float* __restrict__ kfpose, int capK, int k0, int k1) {
+                                            float* __restrict__ kfpose, float4* __restrict__ kft,
+                                            int capK, int k0, int k1) {
   const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const int nk = k1 - k0;
   if (t >= (long long)N * nk) return;
@@ -54,6 +55,17 @@ __global__ void fill_kf_from_current_kernel(const float* __restrict__ pose, int 
   float* dst = kfpose + ((size_t)i * capK + k) * 12;
 #pragma unroll
   for (int e = 0; e < 12; ++e) dst[e] = pose[(size_t)e * capN + i];
+  kft[(size_t)i * capK + k] = make_float4(dst[3], dst[7], dst[11], 0.f);
+}
+
+// the translation plane of keyframes [0, K) from the poses (after a bulk pose copy)
+__global__ void kft_from_kfpose_kernel(const float* __restrict__ kfpose, int capK, int N, int K,
+                                       float4* __restrict__ kft) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (long long)N * K) return;
+  const int i = (int)(t / K), k = (int)(t - (long long)i * K);
+  const float* T = kfpose + ((size_t)i * capK + k) * 12;
+  kft[(size_t)i * capK + k] = make_float4(T[3], T[7], T[11], 0.f);
 }
 
 __global__ void aos_to_soa_kernel(const float* __restrict__ aos, int N, int capN,
@@ -218,7 +230,7 @@ static bool is_pow2_float(float r) {
 
 static void free_all(mcs_ctx* c) {
   for (auto& k : c->kf) mem_free_async(c, k.slots, c->stream);
-  void* ptrs[] = {c->d_kf_meta, c->d_D,       c->d_pose,     c->d_kfpose,   c->d_L,
+  void* ptrs[] = {c->d_kf_meta, c->d_D,       c->d_pose,     c->d_kfpose,   c->d_kft, c->d_L,
                   c->d_snapshot, c->d_scan_raw, c->d_scan,    c->d_items,    c->d_order,
                   c->d_part,    c->d_meta,    c->d_to,       c->d_l,        c->d_psi,
                   c->d_grad,    c->d_hess,    c->d_flags,    c->d_e,        c->d_xg,
@@ -390,6 +402,7 @@ mcs_status mcs_create(const mcs_config* cfg, mcs_ctx** out) {
   if (e == cudaSuccess) e = dalloc(c, &c->d_D, K);
   if (e == cudaSuccess) e = dalloc(c, &c->d_pose, 12 * N);
   if (e == cudaSuccess) e = dalloc(c, &c->d_kfpose, N * K * 12);
+  if (e == cudaSuccess) e = dalloc(c, &c->d_kft, N * K);
   if (e == cudaSuccess) e = dalloc(c, &c->d_L, N);
   if (e == cudaSuccess) e = dalloc(c, &c->d_scan_raw, 9 * S);
   if (e == cudaSuccess) e = dalloc(c, &c->d_scan, 3 * S);
@@ -559,7 +572,7 @@ mcs_status mcs_add_keyframe(mcs_ctx* ctx, const float* mean3, const float* cov6,
   // lockstep extension: T_k^i := T_t^i (R24)
   if (ctx->N > 0) {
     fill_kf_from_current_kernel<<<(ctx->N + 255) / 256, 256, 0, st>>>(
-        ctx->d_pose, ctx->capN, ctx->N, ctx->d_kfpose, ctx->capK, k, k + 1);
+        ctx->d_pose, ctx->capN, ctx->N, ctx->d_kfpose, ctx->d_kft, ctx->capK, k, k + 1);
     CUDA_TRY(ctx, cudaGetLastError());
   }
   CUDA_TRY(ctx, cudaStreamSynchronize(st));
@@ -618,10 +631,13 @@ mcs_status mcs_set_particles(mcs_ctx* ctx, int32_t n, const float* pose12,
       CUDA_TRY(ctx, cudaMemcpy2DAsync(ctx->d_kfpose, sizeof(float) * 12 * ctx->capK, tk,
                                       sizeof(float) * 12 * K, sizeof(float) * 12 * K, n,
                                       cudaMemcpyDeviceToDevice, st));
+      const long long tot = (long long)n * K;
+      kft_from_kfpose_kernel<<<(int)((tot + 255) / 256), 256, 0, st>>>(ctx->d_kfpose, ctx->capK,
+                                                                         n, K, ctx->d_kft);
     } else {
       const long long tot = (long long)n * K;
       fill_kf_from_current_kernel<<<(int)((tot + 255) / 256), 256, 0, st>>>(
-          ctx->d_pose, ctx->capN, n, ctx->d_kfpose, ctx->capK, 0, K);
+          ctx->d_pose, ctx->capN, n, ctx->d_kfpose, ctx->d_kft, ctx->capK, 0, K);
     }
   }
   if (tl) {
@@ -1085,16 +1101,17 @@ mcs_status mcs_overlap(mcs_ctx* ctx, const float* scan_mean3, int32_t n_pts, con
 mcs_status mcs_snapshot(mcs_ctx* ctx) {
   CHECK_CTX(ctx);
   const size_t bp = sizeof(float) * 12 * ctx->capN, bk = sizeof(float) * 12 * ctx->capN * ctx->capK,
-               bl = sizeof(double) * ctx->capN;
+               bt = sizeof(float4) * ctx->capN * ctx->capK, bl = sizeof(double) * ctx->capN;
   if (!ctx->d_snapshot) {
-    CUDA_TRY(ctx, mem_alloc(ctx, &ctx->d_snapshot, bp + bk + bl));
-    ctx->snapshot_bytes = bp + bk + bl;
+    CUDA_TRY(ctx, mem_alloc(ctx, &ctx->d_snapshot, bp + bk + bt + bl));
+    ctx->snapshot_bytes = bp + bk + bt + bl;
   }
   char* s = (char*)ctx->d_snapshot;
   cudaStream_t st = ctx->stream;
   CUDA_TRY(ctx, cudaMemcpyAsync(s, ctx->d_pose, bp, cudaMemcpyDeviceToDevice, st));
   CUDA_TRY(ctx, cudaMemcpyAsync(s + bp, ctx->d_kfpose, bk, cudaMemcpyDeviceToDevice, st));
-  CUDA_TRY(ctx, cudaMemcpyAsync(s + bp + bk, ctx->d_L, bl, cudaMemcpyDeviceToDevice, st));
+  CUDA_TRY(ctx, cudaMemcpyAsync(s + bp + bk, ctx->d_kft, bt, cudaMemcpyDeviceToDevice, st));
+  CUDA_TRY(ctx, cudaMemcpyAsync(s + bp + bk + bt, ctx->d_L, bl, cudaMemcpyDeviceToDevice, st));
   return MCS_OK;
 }
 
@@ -1102,12 +1119,13 @@ mcs_status mcs_restore(mcs_ctx* ctx) {
   CHECK_CTX(ctx);
   if (!ctx->d_snapshot) FAIL(ctx, MCS_E_STATE, "no snapshot");
   const size_t bp = sizeof(float) * 12 * ctx->capN, bk = sizeof(float) * 12 * ctx->capN * ctx->capK,
-               bl = sizeof(double) * ctx->capN;
+               bt = sizeof(float4) * ctx->capN * ctx->capK, bl = sizeof(double) * ctx->capN;
   char* s = (char*)ctx->d_snapshot;
   cudaStream_t st = ctx->stream;
   CUDA_TRY(ctx, cudaMemcpyAsync(ctx->d_pose, s, bp, cudaMemcpyDeviceToDevice, st));
   CUDA_TRY(ctx, cudaMemcpyAsync(ctx->d_kfpose, s + bp, bk, cudaMemcpyDeviceToDevice, st));
-  CUDA_TRY(ctx, cudaMemcpyAsync(ctx->d_L, s + bp + bk, bl, cudaMemcpyDeviceToDevice, st));
+  CUDA_TRY(ctx, cudaMemcpyAsync(ctx->d_kft, s + bp + bk, bt, cudaMemcpyDeviceToDevice, st));
+  CUDA_TRY(ctx, cudaMemcpyAsync(ctx->d_L, s + bp + bk + bt, bl, cudaMemcpyDeviceToDevice, st));
   return MCS_OK;
 }
 

@@ -411,8 +411,8 @@ mcs_status dist_barrier(mcs_ctx* c) {
 namespace {
 struct PeerInfo {  // what a rank publishes about its state buffers
   int32_t pid, dev, capN, capK, ipc_ok, pad;
-  uint64_t ptr[5];                 // pose, kfpose, L, dead_list, donor_g
-  cudaIpcMemHandle_t handle[5];
+  uint64_t ptr[6];                 // pose, kfpose, L, dead_list, donor_g, kft
+  cudaIpcMemHandle_t handle[6];
 };
 }  // namespace
 
@@ -427,10 +427,10 @@ mcs_status dist_peer_setup(mcs_ctx* c) {
   me.dev = c->dev;
   me.capN = c->capN;
   me.capK = c->capK;
-  void* mine[5] = {c->d_pose, c->d_kfpose, c->d_L, c->d_dead_list, c->d_donor_g};
+  void* mine[6] = {c->d_pose, c->d_kfpose, c->d_L, c->d_dead_list, c->d_donor_g, c->d_kft};
   // CUDA IPC needs whole cudaMalloc allocations: not available under a user allocator
   me.ipc_ok = c->alloc.alloc ? 0 : 1;
-  for (int k = 0; k < 5; ++k) {
+  for (int k = 0; k < 6; ++k) {
     me.ptr[k] = (uint64_t)(uintptr_t)mine[k];
     if (me.ipc_ok && cudaIpcGetMemHandle(&me.handle[k], mine[k]) != cudaSuccess) me.ipc_ok = 0;
   }
@@ -442,9 +442,9 @@ mcs_status dist_peer_setup(mcs_ctx* c) {
   std::vector<void*> opened;
   for (int p = 0; p < G && ok; ++p) {
     const PeerInfo& q = all[p];
-    void* ptr[5];
+    void* ptr[6];
     if (q.pid == me.pid) {  // same process: raw pointers (peer access if another device)
-      for (int k = 0; k < 5; ++k) ptr[k] = (void*)(uintptr_t)q.ptr[k];
+      for (int k = 0; k < 6; ++k) ptr[k] = (void*)(uintptr_t)q.ptr[k];
       if (q.dev != c->dev) {
         int can = 0;
         if (cudaDeviceCanAccessPeer(&can, c->dev, q.dev) != cudaSuccess || !can) {
@@ -460,7 +460,7 @@ mcs_status dist_peer_setup(mcs_ctx* c) {
         ok = 0;
         break;
       }
-      for (int k = 0; k < 5 && ok; ++k) {
+      for (int k = 0; k < 6 && ok; ++k) {
         if (cudaIpcOpenMemHandle(&ptr[k], q.handle[k], cudaIpcMemLazyEnablePeerAccess) !=
             cudaSuccess) {
           ok = 0;
@@ -471,8 +471,8 @@ mcs_status dist_peer_setup(mcs_ctx* c) {
       }
     }
     if (!ok) break;
-    views[p] = PeerView{(float*)ptr[0], (float*)ptr[1], (double*)ptr[2], (int32_t*)ptr[3],
-                        (int32_t*)ptr[4], q.capN, q.capK};
+    views[p] = PeerView{(float*)ptr[0], (float*)ptr[1], (float4*)ptr[5], (double*)ptr[2],
+                        (int32_t*)ptr[3], (int32_t*)ptr[4], q.capN, q.capK};
   }
   // every rank must agree (one failed open anywhere -> all use the transport path)
   std::vector<int32_t> oks(G);

@@ -149,6 +149,10 @@ struct mcs_ctx {
   int N = 0;                    // local particles
   float* d_pose = nullptr;      // [12][Ncap]
   float* d_kfpose = nullptr;    // [Ncap][Kcap][12]
+  // the keyframe translations again, {t_x, t_y, t_z, 0} per (particle, keyframe) [Ncap][Kcap]:
+  // a1's nearest-keyframe search reads 16 B per keyframe instead of the 48-B pose.  Every
+  // writer of d_kfpose writes it too (insertion, set_particles, a4, clones, unpack, restore)
+  float4* d_kft = nullptr;
   double* d_L = nullptr;        // [Ncap]
   void* d_snapshot = nullptr;   // mcs_snapshot buffer
   size_t snapshot_bytes = 0;
@@ -285,6 +289,7 @@ void launch_weights_out(mcs_ctx* c, double* d_w);
 struct PeerView {
   float* pose;         // SoA [12][capN]
   float* kfpose;       // [capN][capK][12]
+  float4* kft;         // [capN][capK] keyframe translations
   double* L;           // [capN]
   int32_t* dead_list;  // [capN] local dead slots, ascending
   int32_t* donor_g;    // [capN] global donor index

@@ -60,7 +60,8 @@ __device__ __forceinline__ unsigned long long coherence_key(int kf, const float*
 }
 
 __global__ void select_kernel(const float* __restrict__ pose, int capN, int N,
-                              const float* __restrict__ kfpose, int capK, int K, int nb_max,
+                              const float* __restrict__ kfpose,
+                              const float4* __restrict__ kft, int capK, int K, int nb_max,
                               int gap, int gn_all, int eval_mode, float4* __restrict__ items,
                               uint8_t* __restrict__ meta, int32_t* __restrict__ t_o_out,
                               unsigned long long* __restrict__ skeys, int32_t* __restrict__ sids,
@@ -76,11 +77,12 @@ __global__ void select_kernel(const float* __restrict__ pose, int capN, int N,
   int bk[kMaxNb];
 #pragma unroll
   for (int s = 0; s < kMaxNb; ++s) { bd[s] = 0.f; bk[s] = -1; }
+  const float4* tk = kft + (size_t)i * capK;  // the keyframe translations (16 B each)
   for (int k = 0; k < K; ++k) {
-    const float* Tk = kp + 12 * k;
-    float dx = __fsub_rn(Tk[3], Tt[3]);
-    float dy = __fsub_rn(Tk[7], Tt[7]);
-    float dz = __fsub_rn(Tk[11], Tt[11]);
+    const float4 t4 = tk[k];
+    float dx = __fsub_rn(t4.x, Tt[3]);
+    float dy = __fsub_rn(t4.y, Tt[7]);
+    float dz = __fsub_rn(t4.z, Tt[11]);
     float d = __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, __fmul_rn(dx, dx)));
     // insertion into the sorted top-nb list; strict < keeps the lower id on ties
 #pragma unroll
@@ -159,7 +161,8 @@ mcs_status launch_select(mcs_ctx* c, int mode) {
   const int end_bit = sort_end_bit(c->capK);
   const unsigned long long inactive = (end_bit >= 64) ? ~0ull : ((1ull << end_bit) - 1ull);
   select_kernel<<<(N + 127) / 128, 128, 0, c->stream>>>(
-      c->d_pose, c->capN, N, c->d_kfpose, c->capK, c->K, nb_max, c->cfg.loop_recency_gap,
+      c->d_pose, c->capN, N, c->d_kfpose, c->d_kft, c->capK, c->K, nb_max,
+      c->cfg.loop_recency_gap,
       c->cfg.gn_slots == MCS_GN_ALL_SLOTS, mode, c->d_items, c->d_meta, c->d_to,
       c->d_skeys, c->d_sids, inactive);
   size_t tb = c->cub_temp_bytes;

@@ -580,7 +580,8 @@ void launch_combine(mcs_ctx* c, int S, int mode, double* slot_l, float* slot_H21
 // the lanes: at C2 (one survivor) a4 is a check per particle, not a thread per (particle,
 // keyframe) — N K threads cost ~0.1 ms at C3's 200 keyframes even when they all return.
 __global__ void __launch_bounds__(256) propagate_kernel(
-    float* __restrict__ kfpose, int capK, int K, int N, const uint8_t* __restrict__ flags,
+    float* __restrict__ kfpose, float4* __restrict__ kft, int capK, int K, int N,
+    const uint8_t* __restrict__ flags,
     const int32_t* __restrict__ to, const double* __restrict__ psi, int capN,
     const double* __restrict__ D, const Scalars* __restrict__ sc, int mode,
     const double* __restrict__ l, const double* __restrict__ e, double rel_floor,
@@ -647,6 +648,7 @@ __global__ void __launch_bounds__(256) propagate_kernel(
       q4[0] = make_float4(T[0], T[1], T[2], T[3]);
       q4[1] = make_float4(T[4], T[5], T[6], T[7]);
       q4[2] = make_float4(T[8], T[9], T[10], T[11]);
+      kft[(size_t)ij * capK + k] = make_float4(T[3], T[7], T[11], 0.f);
     }
   }
 }
@@ -655,7 +657,8 @@ void launch_propagate(mcs_ctx* c, int mode) {
   if ((long long)c->N * c->K == 0) return;
   const long long warps = (c->N + 31) / 32;
   const int grid = (int)std::min<long long>((warps + 7) / 8, 148LL * 16);
-  propagate_kernel<<<grid, 256, 0, c->stream>>>(c->d_kfpose, c->capK, c->K, c->N, c->d_flags,
+  propagate_kernel<<<grid, 256, 0, c->stream>>>(c->d_kfpose, c->d_kft, c->capK, c->K, c->N,
+                                                c->d_flags,
                                                 c->d_to, c->d_psi, c->capN, c->d_D, c->d_scal,
                                                 mode, c->d_l, c->d_e, c->cfg.loglik_rel_floor,
                                                 c->cfg.posterior_floor);

@@ -344,6 +344,7 @@ struct DrawArgs {
   int K, capK, capN;
   float* pose;
   float* kfpose;
+  float4* kft;
   double* L;
 };
 
@@ -405,12 +406,14 @@ __global__ void __launch_bounds__(kWT) draws_kernel(DrawArgs a) {
       const int ss = __shfl_sync(0xffffffffu, slot, src);
       float* dpose = a.pose;
       float* dkf = a.kfpose;
+      float4* dkt = a.kft;
       double* dL = a.L;
       int dcapN = a.capN, dcapK = a.capK;
       if (dd != a.me) {
         const PeerView& P = a.peers[dd];
         dpose = P.pose;
         dkf = P.kfpose;
+        dkt = P.kft;
         dL = P.L;
         dcapN = P.capN;
         dcapK = P.capK;
@@ -432,6 +435,9 @@ __global__ void __launch_bounds__(kWT) draws_kernel(DrawArgs a) {
         d4[k + 96] = x3;
       }
       for (; k < n4; k += 32) d4[k] = __ldg(s4 + k);
+      const float4* st4 = a.kft + (size_t)jj * a.capK;  // the translation plane, K float4
+      float4* dt4 = dkt + (size_t)ss * dcapK;
+      for (k = lane; k < a.K; k += 32) dt4[k] = __ldg(st4 + k);
       if (lane == 0) {
         double Lc = a.L[jj];
         if (a.split) {  // R34: the donor's draw count from its own rungs
@@ -599,8 +605,8 @@ __global__ void pack_kernel(const int32_t* __restrict__ pack_src, long long n_it
 __global__ void unpack_kernel(const float* __restrict__ in, long long n_items, int K, int capK,
                               int capN, int world, const long long* __restrict__ plan,
                               const int32_t* __restrict__ dead_list, float* __restrict__ pose,
-                              float* __restrict__ kfpose, double* __restrict__ L,
-                              int32_t* __restrict__ donor_g) {
+                              float* __restrict__ kfpose, float4* __restrict__ kft,
+                              double* __restrict__ L, int32_t* __restrict__ donor_g) {
   const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const int KK = K + 1;
   if (t >= n_items * KK) return;
@@ -624,6 +630,8 @@ __global__ void unpack_kernel(const float* __restrict__ in, long long n_items, i
   } else {
     float* dst = kfpose + ((size_t)slot * capK + k) * 12;
     for (int e = 0; e < 12; ++e) dst[e] = s[12 + 12 * k + e];
+    kft[(size_t)slot * capK + k] =
+        make_float4(s[12 + 12 * k + 3], s[12 + 12 * k + 7], s[12 + 12 * k + 11], 0.f);
   }
 }
 
@@ -823,6 +831,7 @@ mcs_status launch_weights_resample(mcs_ctx* c, uint32_t U, bool fork_a4) {
   da.capN = c->capN;
   da.pose = c->d_pose;
   da.kfpose = c->d_kfpose;
+  da.kft = c->d_kft;
   da.L = c->d_L;
   draws_kernel<<<draw_grid(c), kWT, 0, st>>>(da);
   if (p2p) {
@@ -842,7 +851,7 @@ mcs_status launch_weights_resample(mcs_ctx* c, uint32_t U, bool fork_a4) {
       const long long tr = n_recv * (c->K + 1);
       unpack_kernel<<<(int)((tr + 255) / 256), 256, 0, st>>>(
           c->d_recv, n_recv, c->K, c->capK, c->capN, c->world, c->d_plan, c->d_dead_list,
-          c->d_pose, c->d_kfpose, c->d_L, c->d_donor_g);
+          c->d_pose, c->d_kfpose, c->d_kft, c->d_L, c->d_donor_g);
     }
   }
   // re-normalise on the new L (global shift and sum), then a7
