@@ -405,7 +405,11 @@ mcs_status mcs_create(const mcs_config* cfg, mcs_ctx** out) {
   if (e == cudaSuccess) e = dalloc(c, &c->d_kft, N * K);
   if (e == cudaSuccess) e = dalloc(c, &c->d_L, N);
   if (e == cudaSuccess) e = dalloc(c, &c->d_scan_raw, 9 * S);
-  if (e == cudaSuccess) e = dalloc(c, &c->d_scan, 3 * S);
+  if (e == cudaSuccess) e = dalloc(c, &c->d_scan, 5 * S + 1);
+  if (e == cudaSuccess) {
+    c->d_scan_plane = c->d_scan + 3 * S;
+    c->d_scan_np = reinterpret_cast<int*>(c->d_scan + 5 * S);
+  }
   if (e == cudaSuccess) e = dalloc(c, &c->d_items, 4 * nb * N);
   if (e == cudaSuccess) e = dalloc(c, &c->d_order, nb * N);
   if (e == cudaSuccess) e = dalloc(c, &c->d_skeys, nb * N);
@@ -896,7 +900,7 @@ mcs_status mcs_update(mcs_ctx* ctx, const float* scan_mean3, const float* scan_c
   CUDA_TRY(ctx, to_device(raw_c, scan_cov6, sizeof(float) * 6 * n_pts, st));
   s = validate_scan(ctx, n_pts);
   if (s != MCS_OK) return s;
-  launch_prepare_scan(raw_m, raw_c, n_pts, ctx->d_scan, st);
+  launch_prepare_scan(raw_m, raw_c, n_pts, ctx->d_scan, ctx->d_scan_plane, ctx->d_scan_np, st);
   s = run_update(ctx, n_pts, D_now, resample_u);
   if (s != MCS_OK) {
     ctx->sticky = s;
@@ -945,7 +949,7 @@ mcs_status mcs_update_async(mcs_ctx* ctx, const float* d_scan_mean3, const float
   if (s != MCS_OK) return s;
   cudaStream_t saved = ctx->stream;
   if (cuda_stream) ctx->stream = (cudaStream_t)cuda_stream;
-  launch_prepare_scan(d_scan_mean3, d_scan_cov6, n_pts, ctx->d_scan, ctx->stream);
+  launch_prepare_scan(d_scan_mean3, d_scan_cov6, n_pts, ctx->d_scan, ctx->d_scan_plane, ctx->d_scan_np, ctx->stream);
   s = run_update(ctx, n_pts, D_now, resample_u);
   if (s != MCS_OK) {
     ctx->stream = saved;
@@ -979,7 +983,7 @@ mcs_status mcs_eval(mcs_ctx* ctx, const float* scan_mean3, const float* scan_cov
   CUDA_TRY(ctx, to_device(raw_c, scan_cov6, sizeof(float) * 6 * n_pts, st));
   s = validate_scan(ctx, n_pts);
   if (s != MCS_OK) return s;
-  launch_prepare_scan(raw_m, raw_c, n_pts, ctx->d_scan, st);
+  launch_prepare_scan(raw_m, raw_c, n_pts, ctx->d_scan, ctx->d_scan_plane, ctx->d_scan_np, st);
   const size_t NS = (size_t)ctx->N * ctx->cfg.neighbor_count;
   double* dl = nullptr;
   float *dH = nullptr, *db = nullptr;

@@ -159,7 +159,9 @@ struct mcs_ctx {
 
   // per-update scratch
   float* d_scan_raw = nullptr;  // [Scap][9]
-  float4* d_scan = nullptr;     // [Scap][3]
+  float4* d_scan = nullptr;     // [Scap][3], then d_scan_plane, then one float4 for d_scan_np
+  float4* d_scan_plane = nullptr;  // [Scap][2] plane-form layout (R36)
+  int* d_scan_np = nullptr;     // number of scan points not in plane form (prepare_scan)
   float4* d_items = nullptr;    // [nb*Ncap][4]
   int32_t* d_order = nullptr;   // [nb*Ncap] sweep order (item ids, coherence-sorted)
   unsigned long long* d_skeys = nullptr;      // [nb*Ncap] coherence keys (a1)
@@ -236,10 +238,12 @@ namespace mcs {
 // bounding box exceeds 2047 x 2048 x 1024 cells.
 cudaError_t kf_build(mcs_ctx* c, const float* d_mean3, const float* d_cov6, int n, KfHost& out,
                      int* bad_cell, int* bad_extent);
-// raw [S][3] + [S][6] -> the sweep's float4 x3 layout {mu, lambda3} {u, 0} {v, 0}
-// (spectral form Sigma = lambda3 I + u u^T + v v^T, fp64 Jacobi)
+// raw [S][3] + [S][6] -> the sweep's float4 x3 layout {mu, lambda3} {u, 0} {v, 0} (spectral
+// form Sigma = lambda3 I + u u^T + v v^T, fp64 Jacobi), and the plane-form layout {mu, lambda3}
+// {x, 0} (Sigma = lambda3 I + [x]x^T [x]x, R36) in out_plane; *nonplanar = number of points
+// that are not plane-form
 void launch_prepare_scan(const float* mean3, const float* cov6, int S, float4* out,
-                         cudaStream_t st);
+                         float4* out_plane, int* nonplanar, cudaStream_t st);
 // a1; mode: kSelectUpdate (H~, b~ for slots in G), kSelectEval (all slots), kSelectWeight (none)
 enum { kSelectUpdate = 0, kSelectEval = 1, kSelectWeight = 2 };
 mcs_status launch_select(mcs_ctx* c, int mode);  // MCS_E_CUDA if a launch (or the sort) fails

@@ -18,6 +18,7 @@
 // spectral form of Sigma_j (prepare_scan_kernel below).  Accumulation is two-level (fp32 within
 // a 256-point stage, fp64 across stages) in a fixed order: bitwise reproducible.  DESIGN.md §5.
 #include <atomic>
+#include <type_traits>
 
 #include "mcs_internal.cuh"
 
@@ -151,15 +152,23 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 constexpr float kMagic = 12582912.0f;
 
 // kCorr: MCS_CORR_CELL (one probe of the containing voxel, R7) or MCS_CORR_NN27 (R33)
-template <int kCorr>
+// kPlane: the instantiation for scans whose points are all plane-form (R36); both CELL
+// instantiations are launched and the one that does not match the scan's flag (written by
+// prepare_scan_kernel) returns at once (two instantiations, not a branch per stage: with both
+// stage loops in one kernel ptxas spills the probe buffers)
+template <int kCorr, bool kPlane>
 __global__ void __launch_bounds__(kSweepThreads, kCorr == MCS_CORR_NN27 ? MCS_NN27_MINBLOCKS
                                                                        : MCS_SWEEP_MINBLOCKS)
     sweep_kernel(const float4* __restrict__ items, const int32_t* __restrict__ order,
                  int n_items, const float4* __restrict__ scan, int S,
                  const KfMeta* __restrict__ kmeta, float inv_r, float nn_r2,
-                 double* __restrict__ part, size_t pstride) {
+                 double* __restrict__ part, size_t pstride, const int* __restrict__ nonplanar) {
+  static_assert(!kPlane || kCorr == MCS_CORR_CELL, "NN27 has one (general) instantiation");
+  if (kCorr == MCS_CORR_CELL && ((*nonplanar == 0) != kPlane)) return;
+  using PlaneTag = std::integral_constant<bool, kPlane>;
   // dynamic shared memory: [(kChunk + 2) * 3] float4 scan stage, then [28][threads] fp64 totals
-  constexpr int kStage = (kChunk + 2) * 3;  // float4 per stage buffer (2 spare points)
+  constexpr int kW = kPlane ? 2 : 3;          // float4 words per scan point in the stage
+  constexpr int kStage = (kChunk + 2) * kW;  // float4 per stage buffer (2 spare points)
   constexpr int kBufs = MCS_SWEEP_TMA ? 2 : 1;
 #if MCS_SWEEP_STATIC_SMEM
   // static shared memory: link-time addresses, nothing to rematerialise per point
@@ -179,7 +188,7 @@ __global__ void __launch_bounds__(kSweepThreads, kCorr == MCS_CORR_NN27 ? MCS_NN
   // a point is named by its shared-window address (48 B per point): a loop-carried register
   // that ptxas cannot rematerialise from %cgactaid at every use, as it does for a stage-constant
   // base plus an index
-  constexpr uint32_t kPt = 48u;
+  constexpr uint32_t kPt = 16u * kW;
   auto pt = [&](uint32_t j, int w) { return lds4(j + 16u * w); };  // word w of point j
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   const int item = t < n_items ? order[t] : -1;
@@ -314,10 +323,13 @@ __global__ void __launch_bounds__(kSweepThreads, kCorr == MCS_CORR_NN27 ? MCS_NN
 
   // Eqs.3-4 and Eq.6 for one matched (item, point); the (y, z) halves of the 3-vectors and of
   // the symmetric 3x3 matrices travel as register pairs (packed FFMA2/FMUL2/FADD2)
-  auto accumulate = [&](uint32_t j, const Probe& p) {
-    const float4 A = pt(j, 0);  // {mu, lambda3}
-    const float4 U = pt(j, 1);  // {u, 0}
-    const float4 V = pt(j, 2);  // {v, 0}   Sigma_j = lambda3 I + u u^T + v v^T
+  // general scan point: Sigma_j = lam3 I + u u^T + v v^T (words {mu, lam3} {u, 0} {v, 0});
+  // plane-form point (kPlane, R36): Sigma_j = lam3 I + |n|^2 I - n n^T = lam3 I + [n]x^T [n]x
+  // (words {mu, lam3} {n, 0}), whose diagonal is a sum of squares, as in the general form
+  auto accumulate = [&](auto plane_tag, uint32_t j, const Probe& p) {
+    constexpr bool kPl = decltype(plane_tag)::value;
+    const float4 A = pt(j, 0);  // {mu, lam3}
+    const float4 U = pt(j, 1);  // {u, 0}, or {n, 0}
     // payload {key, mu'} {S'yy, S'zz, S'xy, S'xz} {S'xx, S'yz}
     const float4 P0 = p.s0, P1 = p.s1, P2 = p.s2;
     // e = mu' - kT mu   (Eq.4);  m = R mu = q - t
@@ -326,15 +338,26 @@ __global__ void __launch_bounds__(kSweepThreads, kCorr == MCS_CORR_NN27 ? MCS_NN
     const float mx = p.qx - tx;
     const float2 myz = add2(p.qyz, ntyz);
     const float my = myz.x, mz = myz.y;
-    // C = Sigma' + R Sigma R^T = Sigma' + lambda3 I + (Ru)(Ru)^T + (Rv)(Rv)^T  (Eq.4)
+    // C = Sigma' + R Sigma R^T  (Eq.4):  Sigma' + lam3 I + (Ru)(Ru)^T + (Rv)(Rv)^T, or with
+    // x = R n:  Sigma' + lam3 I + [x]x^T [x]x,  diagonal (x1^2 + x2^2, x0^2 + x2^2, x0^2 + x1^2)
     const float ux = fmaf(R02, U.z, fmaf(R01, U.y, R00 * U.x));
     const float2 uyz = fma2(Ryz2, bc(U.z), fma2(Ryz1, bc(U.y), mul2(Ryz0, bc(U.x))));
-    const float vx = fmaf(R02, V.z, fmaf(R01, V.y, R00 * V.x));
-    const float2 vyz = fma2(Ryz2, bc(V.z), fma2(Ryz1, bc(V.y), mul2(Ryz0, bc(V.x))));
-    const float c00 = fmaf(ux, ux, fmaf(vx, vx, P2.x + A.w));
-    const float2 c1122 = fma2(uyz, uyz, fma2(vyz, vyz, add2(make_float2(P1.x, P1.y), bc(A.w))));
-    const float2 c0102 = fma2(bc(ux), uyz, fma2(bc(vx), vyz, make_float2(P1.z, P1.w)));
-    const float c12 = fmaf(uyz.x, uyz.y, fmaf(vyz.x, vyz.y, P2.y));
+    float c00, c12;
+    float2 c1122, c0102;
+    if constexpr (kPl) {
+      c00 = fmaf(uyz.x, uyz.x, fmaf(uyz.y, uyz.y, P2.x + A.w));
+      c1122 = fma2(bc(ux), bc(ux), fma2(sw(uyz), sw(uyz), add2(make_float2(P1.x, P1.y), bc(A.w))));
+      c0102 = fma2(bc(-ux), uyz, make_float2(P1.z, P1.w));
+      c12 = fmaf(-uyz.x, uyz.y, P2.y);
+    } else {
+      const float4 V = pt(j, 2);  // {v, 0}
+      const float vx = fmaf(R02, V.z, fmaf(R01, V.y, R00 * V.x));
+      const float2 vyz = fma2(Ryz2, bc(V.z), fma2(Ryz1, bc(V.y), mul2(Ryz0, bc(V.x))));
+      c00 = fmaf(ux, ux, fmaf(vx, vx, P2.x + A.w));
+      c1122 = fma2(uyz, uyz, fma2(vyz, vyz, add2(make_float2(P1.x, P1.y), bc(A.w))));
+      c0102 = fma2(bc(ux), uyz, fma2(bc(vx), vyz, make_float2(P1.z, P1.w)));
+      c12 = fmaf(uyz.x, uyz.y, fmaf(vyz.x, vyz.y, P2.y));
+    }
     // Omega = C^-1 = adj(C) / det(C):  (k11, k22) = c00 (c22, c11) - (c02, c01)^2,
     // (k01, k02) = c12 (c02, c01) - (c01 c22, c02 c11)
     const float k00 = fmaf(c1122.x, c1122.y, -c12 * c12);
@@ -467,16 +490,18 @@ __global__ void __launch_bounds__(kSweepThreads, kCorr == MCS_CORR_NN27 ? MCS_NN
   };
 
   // first probe: hit -> accumulate; empty slot (or the sentinel) -> miss; else keep probing
-  auto act = [&](uint32_t j, const Probe& p, unsigned int k0) {
+  auto act = [&](auto tg, uint32_t j, const Probe& p, unsigned int k0) {
     if (k0 == p.key) {
-      accumulate(j, p);
+      accumulate(tg, j, p);
     } else if (k0 != kEmptyKey32) {
       Probe q;
       q.qx = p.qx; q.qyz = p.qyz; q.key = p.key;
-      if (probe_on(q)) accumulate(j, q);
+      if (probe_on(q)) accumulate(tg, j, q);
     }
   };
-  auto consume = [&](uint32_t j, const Probe& p) { act(j, p, __float_as_uint(p.s0.x)); };
+  auto consume = [&](auto tg, uint32_t j, const Probe& p) {
+    act(tg, j, p, __float_as_uint(p.s0.x));
+  };
 
   // NN27 (R33): the nearest cell representative within nn_radius among the 27 voxels around
   // q's voxel, d = mu'32 - q32, d2 = fma(dz, dz, fma(dy, dy, dx * dx)) (pinned fp32), ties ->
@@ -562,7 +587,7 @@ __global__ void __launch_bounds__(kSweepThreads, kCorr == MCS_CORR_NN27 ? MCS_NN
       p.s0 = __ldg(sl);
       p.s1 = __ldg(sl + 1);
       p.s2 = __ldg(sl + 2);
-      accumulate(j, p);
+      accumulate(std::false_type{}, j, p);
     }
   };
 
@@ -612,7 +637,7 @@ __global__ void __launch_bounds__(kSweepThreads, kCorr == MCS_CORR_NN27 ? MCS_NN
   };
 
   // the math of one stage of cnt points in s_pt (active threads)
-  auto stage = [&](const int cnt) {
+  auto stage = [&](auto tg, const int cnt) {
     const uint32_t e = s_pt_u32 + kPt * (uint32_t)cnt;  // one past the last point
     if (kCorr == MCS_CORR_NN27) {
       for (uint32_t j = s_pt_u32; j < e; j += kPt) nn27_point(j);
@@ -631,30 +656,30 @@ __global__ void __launch_bounds__(kSweepThreads, kCorr == MCS_CORR_NN27 ? MCS_NN
       const unsigned int ka = __float_as_uint(pa.s0.x), kb = __float_as_uint(pb.s0.x);
       pc = issue_after(j + 2 * kPt, ka);
       pd = issue_after(j + 3 * kPt, kb);
-      act(j, pa, ka);
-      act(j + kPt, pb, kb);
+      act(tg, j, pa, ka);
+      act(tg, j + kPt, pb, kb);
       const unsigned int kc = __float_as_uint(pc.s0.x), kd = __float_as_uint(pd.s0.x);
       pa = issue_after(j + 4 * kPt, kc);
       pb = issue_after(j + 5 * kPt, kd);
-      act(j + 2 * kPt, pc, kc);
-      act(j + 3 * kPt, pd, kd);
+      act(tg, j + 2 * kPt, pc, kc);
+      act(tg, j + 3 * kPt, pd, kd);
     }
-    if (j < e) consume(j, pa);
-    if (j + kPt < e) consume(j + kPt, pb);
+    if (j < e) consume(tg, j, pa);
+    if (j + kPt < e) consume(tg, j + kPt, pb);
     if (j + 2 * kPt < e) {
       pc = issue(j + 2 * kPt);
-      consume(j + 2 * kPt, pc);
+      consume(tg, j + 2 * kPt, pc);
     }
 #else
     Probe pa = issue(s_pt_u32), pb;
     uint32_t j = s_pt_u32;
     for (; j + kPt < e; j += 2 * kPt) {
       pb = issue(j + kPt);
-      consume(j, pa);
+      consume(tg, j, pa);
       pa = issue(j + 2 * kPt);
-      consume(j + kPt, pb);
+      consume(tg, j + kPt, pb);
     }
-    if (j < e) consume(j, pa);
+    if (j < e) consume(tg, j, pa);
 #endif
   };
 
@@ -670,10 +695,10 @@ __global__ void __launch_bounds__(kSweepThreads, kCorr == MCS_CORR_NN27 ? MCS_NN
   auto refill = [&](int k) {  // one thread: stage st_lo + k into buffer k & 1
     const int base = (st_lo + k) * kChunk;
     const int cnt = min(kChunk, S - base);
-    bulk_stage(smem_dyn + (k & 1) * kStage, scan + 3 * (size_t)base, 48u * cnt, &full[k & 1]);
+    bulk_stage(smem_dyn + (k & 1) * kStage, scan + kW * (size_t)base, kPt * cnt, &full[k & 1]);
   };
-  if (threadIdx.x < 12)
-    smem_dyn[(threadIdx.x / 6) * kStage + 3 * kChunk + threadIdx.x % 6] =
+  if (threadIdx.x < 4 * kW)
+    smem_dyn[(threadIdx.x / (2 * kW)) * kStage + kW * kChunk + threadIdx.x % (2 * kW)] =
         make_float4(0.f, 0.f, 0.f, 0.f);
   if (threadIdx.x == 0) {
     mbar_init(&full[0], 1);
@@ -691,7 +716,7 @@ __global__ void __launch_bounds__(kSweepThreads, kCorr == MCS_CORR_NN27 ? MCS_NN
     s_pt_u32 = (uint32_t)__cvta_generic_to_shared(s_pt);
     mbar_wait(&full[k & 1], (k >> 1) & 1);
     if (active) {
-      stage(min(kChunk, S - (st_lo + k) * kChunk));
+      stage(PlaneTag{}, min(kChunk, S - (st_lo + k) * kChunk));
       flush();
     }
     __syncwarp();
@@ -708,14 +733,14 @@ __global__ void __launch_bounds__(kSweepThreads, kCorr == MCS_CORR_NN27 ? MCS_NN
     }
   }
 #else
-  if (threadIdx.x < 6) s_pt[3 * kChunk + threadIdx.x] = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (threadIdx.x < 2 * kW) s_pt[kW * kChunk + threadIdx.x] = make_float4(0.f, 0.f, 0.f, 0.f);
   for (int base = st_lo * kChunk; base < st_hi * kChunk; base += kChunk) {
     const int cnt = min(kChunk, S - base);
     __syncthreads();
-    for (int k = threadIdx.x; k < cnt * 3; k += kSweepThreads) s_pt[k] = scan[3 * base + k];
+    for (int k = threadIdx.x; k < cnt * kW; k += kSweepThreads) s_pt[k] = scan[kW * base + k];
     __syncthreads();
     if (!MCS_SWEEP_CONVERGENT && !active) continue;
-    stage(cnt);
+    stage(PlaneTag{}, cnt);
     flush();
   }
 #endif
@@ -755,9 +780,12 @@ __global__ void reduce_splits_kernel(double* __restrict__ part, size_t pstride, 
 // leading eigenvectors scaled by sqrt(lambda_k - lambda3) — the spectral decomposition,
 // exact up to rounding for any symmetric Sigma (fp64 cyclic Jacobi, then rounded).  The sweep
 // then forms R Sigma R^T as lambda3 I + (Ru)(Ru)^T + (Rv)(Rv)^T (33 FP32 ops instead of 45).
+// Plane-form points also get {mu, lambda3} {x, 0} in out_plane (R36 below), and *nonplanar
+// counts the points that are not plane-form: 0 selects the plane instantiation of the sweep.
 __global__ void prepare_scan_kernel(const float* __restrict__ mean3,
                                     const float* __restrict__ cov6, int S,
-                                    float4* __restrict__ out) {
+                                    float4* __restrict__ out, float4* __restrict__ out_plane,
+                                    int* __restrict__ nonplanar) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= S) return;
   const float* c = cov6 + 6 * j;
@@ -804,11 +832,23 @@ __global__ void prepare_scan_kernel(const float* __restrict__ mean3,
                                (float)(su * v[2][i0]), 0.f);
   out[3 * j + 2] = make_float4((float)(sv * v[0][i1]), (float)(sv * v[1][i1]),
                                (float)(sv * v[2][i1]), 0.f);
+  // plane form (R36): GICP's plane-regularised covariances (eigenvalues (1, 1, eps), R9) have
+  // l0 = l1 up to the rounding of their fp32 entries.  A split within 4 ulps of l0 is merged:
+  // Sigma = l3 I + a (I - n n^T) = l3 I + [x]x^T [x]x with a = (l0 + l1) / 2 - l3 and
+  // x = sqrt(a) n, n the eigenvector of l3 — one vector for the sweep to rotate instead of two
+  const bool plane = lam[i0] - lam[i1] <= 0x1p-21 * fabs(lam[i0]);
+  const double sa = sqrt(fmax(0.5 * (lam[i0] + lam[i1]) - l3, 0.0));
+  out_plane[2 * j + 0] = make_float4(m[0], m[1], m[2], (float)l3);
+  out_plane[2 * j + 1] = make_float4((float)(sa * v[0][i2]), (float)(sa * v[1][i2]),
+                                     (float)(sa * v[2][i2]), 0.f);
+  if (!plane) atomicAdd(nonplanar, 1);
 }
 
 void launch_prepare_scan(const float* mean3, const float* cov6, int S, float4* out,
-                         cudaStream_t st) {
-  prepare_scan_kernel<<<(S + 127) / 128, 128, 0, st>>>(mean3, cov6, S, out);
+                         float4* out_plane, int* nonplanar, cudaStream_t st) {
+  cudaMemsetAsync(nonplanar, 0, sizeof(int), st);
+  prepare_scan_kernel<<<(S + 127) / 128, 128, 0, st>>>(mean3, cov6, S, out, out_plane,
+                                                       nonplanar);
 }
 
 #ifndef MCS_SPLIT_TARGET_CTAS
@@ -844,21 +884,27 @@ void launch_sweep(mcs_ctx* c, int S) {
   // driven from several host threads (repeating the idempotent call is harmless)
   static std::atomic<bool> attr_set[128];
   if (c->dev < 0 || c->dev >= 128 || !attr_set[c->dev].load(std::memory_order_acquire)) {
-    cudaFuncSetAttribute(sweep_kernel<MCS_CORR_CELL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-    cudaFuncSetAttribute(sweep_kernel<MCS_CORR_NN27>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
+    cudaFuncSetAttribute(sweep_kernel<MCS_CORR_CELL, true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(sweep_kernel<MCS_CORR_CELL, false>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(sweep_kernel<MCS_CORR_NN27, false>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (c->dev >= 0 && c->dev < 128) attr_set[c->dev].store(true, std::memory_order_release);
   }
   if (c->cfg.corr_mode == MCS_CORR_NN27) {
     const float nn_r2 = c->cfg.nn_radius * c->cfg.nn_radius;
-    sweep_kernel<MCS_CORR_NN27><<<grid, kSweepThreads, smem, c->stream>>>(
+    sweep_kernel<MCS_CORR_NN27, false><<<grid, kSweepThreads, smem, c->stream>>>(
         c->d_items, c->d_order, n_items, c->d_scan, S, c->d_kf_meta, inv_r, nn_r2, c->d_part,
-        pstride);
+        pstride, c->d_scan_np);
   } else {
-    sweep_kernel<MCS_CORR_CELL><<<grid, kSweepThreads, smem, c->stream>>>(
+    // the plane-form instantiation first: it is the one that runs on GICP scans (R36)
+    sweep_kernel<MCS_CORR_CELL, true><<<grid, kSweepThreads, smem, c->stream>>>(
+        c->d_items, c->d_order, n_items, c->d_scan_plane, S, c->d_kf_meta, inv_r, 0.f, c->d_part,
+        pstride, c->d_scan_np);
+    sweep_kernel<MCS_CORR_CELL, false><<<grid, kSweepThreads, smem, c->stream>>>(
         c->d_items, c->d_order, n_items, c->d_scan, S, c->d_kf_meta, inv_r, 0.f, c->d_part,
-        pstride);
+        pstride, c->d_scan_np);
   }
   if (P > 1) {
     const long long tot = 29LL * n_items;
