@@ -36,8 +36,9 @@ FLOPS_UNMATCHED = 21.0   # transform + key for an unmatched triple
 GATHER_MATCHED = 44.0    # algorithmic bytes per matched triple: 8-B key + 12-B mu'
 #                          + 24-B Sigma' (the slot layout moves 40 B + the 4-B key per first probe)
 GATHER_UNMATCHED = 8.0   # the key probe of an unmatched triple
-LAUNCHES_PER_UPDATE = 13  # own kernels per mcs_update_async at C2: set_params, prepare_scan,
-#                           select, sweep, reduce_splits, combine, exp_sum, propagate (survivors),
+LAUNCHES_PER_UPDATE = 14  # own kernels per mcs_update_async at C2: set_params, prepare_scan,
+#                           select, sweep (plane-form instantiation), sweep (general, returns at
+#                           once on a plane-form scan), reduce_splits, combine, exp_sum, propagate (survivors),
 #                           ladder, propagate (no-op unless no survivor), draws, renorm,
 #                           gather_outputs (profiles/r02_launches.csv)
 # the paper's own figure (context only, another machine and the whole system)

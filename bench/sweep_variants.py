@@ -9,12 +9,11 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 VARIANTS = {
-    "base": [],
-    "t256": ["MCS_SWEEP_THREADS=256", "MCS_SWEEP_MINBLOCKS=2"],
-    "split5k": ["MCS_SPLIT_TARGET_CTAS=5000"],
-    "split9k": ["MCS_SPLIT_TARGET_CTAS=9000"],
-    "chunk512": ["MCS_SWEEP_CHUNK=512"],
-    "packed1": ["MCS_SWEEP_PACKED_H=1"],
+    "pre0": ["MCS_SWEEP_PRELOAD=0"],
+    "pre1": ["MCS_SWEEP_PRELOAD=1"],
+    "pre2": ["MCS_SWEEP_PRELOAD=2"],
+    "pre0b": ["MCS_SWEEP_PRELOAD=0"],
+    "pre1b": ["MCS_SWEEP_PRELOAD=1"],
 }
 OUT = os.path.join(ROOT, "bench", "_variants")
 
