@@ -320,6 +320,14 @@ MCS_API int32_t mcs_peer_migration_state(const mcs_ctx* ctx);
 /* 1 if the library holds a captured CUDA graph of the update body (mcs_config.graph_replay and
  * a device-resident exchange path: one device, or NCCL with peer-direct migration), else 0. */
 MCS_API int32_t mcs_graph_state(const mcs_ctx* ctx);
+/* Scan form of the last scan prepared by mcs_update / mcs_update_async / mcs_eval (R36,
+ * DESIGN.md §3): *n_out = the number of its points whose covariance is NOT plane-form (the two
+ * largest eigenvalues of the fp32 covariance differ by more than 2^-21 of the largest).  0
+ * selects the sweep's plane-form instantiation (one rotated vector per point, Sigma =
+ * lambda3 I + [x]x^T [x]x); any other value the general one (Sigma = lambda3 I + u u^T + v v^T).
+ * Both compute C = Sigma' + R Sigma R^T of Eq.4 up to rounding.  Synchronises the
+ * context's stream; MCS_E_STATE before any scan was prepared. */
+MCS_API mcs_status mcs_scan_nonplanar(mcs_ctx* ctx, int32_t* n_out);
 
 #ifdef __cplusplus
 }

@@ -901,6 +901,7 @@ mcs_status mcs_update(mcs_ctx* ctx, const float* scan_mean3, const float* scan_c
   s = validate_scan(ctx, n_pts);
   if (s != MCS_OK) return s;
   launch_prepare_scan(raw_m, raw_c, n_pts, ctx->d_scan, ctx->d_scan_plane, ctx->d_scan_np, st);
+  ctx->scan_prepared = true;
   s = run_update(ctx, n_pts, D_now, resample_u);
   if (s != MCS_OK) {
     ctx->sticky = s;
@@ -950,6 +951,7 @@ mcs_status mcs_update_async(mcs_ctx* ctx, const float* d_scan_mean3, const float
   cudaStream_t saved = ctx->stream;
   if (cuda_stream) ctx->stream = (cudaStream_t)cuda_stream;
   launch_prepare_scan(d_scan_mean3, d_scan_cov6, n_pts, ctx->d_scan, ctx->d_scan_plane, ctx->d_scan_np, ctx->stream);
+  ctx->scan_prepared = true;
   s = run_update(ctx, n_pts, D_now, resample_u);
   if (s != MCS_OK) {
     ctx->stream = saved;
@@ -984,6 +986,7 @@ mcs_status mcs_eval(mcs_ctx* ctx, const float* scan_mean3, const float* scan_cov
   s = validate_scan(ctx, n_pts);
   if (s != MCS_OK) return s;
   launch_prepare_scan(raw_m, raw_c, n_pts, ctx->d_scan, ctx->d_scan_plane, ctx->d_scan_np, st);
+  ctx->scan_prepared = true;
   const size_t NS = (size_t)ctx->N * ctx->cfg.neighbor_count;
   double* dl = nullptr;
   float *dH = nullptr, *db = nullptr;
@@ -1141,6 +1144,18 @@ mcs_status mcs_set_profiling(mcs_ctx* ctx, int32_t enable) {
 
 int32_t mcs_peer_migration_state(const mcs_ctx* ctx) { return ctx ? ctx->p2p : 0; }
 int32_t mcs_graph_state(const mcs_ctx* ctx) { return ctx && ctx->gexec ? 1 : 0; }
+
+mcs_status mcs_scan_nonplanar(mcs_ctx* ctx, int32_t* n_out) {
+  CHECK_CTX(ctx);
+  if (!n_out) FAIL(ctx, MCS_E_INVALID_ARG, "n_out is NULL");
+  if (!ctx->scan_prepared) FAIL(ctx, MCS_E_STATE, "no scan prepared yet");
+  int v = 0;
+  CUDA_TRY(ctx, cudaMemcpyAsync(&v, ctx->d_scan_np, sizeof(int), cudaMemcpyDeviceToHost,
+                                ctx->stream));
+  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  *n_out = v;
+  return MCS_OK;
+}
 
 mcs_status mcs_get_phase_ms(const mcs_ctx* ctx, float* ms5) {
   if (!ctx || !ms5) return MCS_E_INVALID_ARG;

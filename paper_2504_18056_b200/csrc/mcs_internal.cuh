@@ -162,6 +162,7 @@ struct mcs_ctx {
   float4* d_scan = nullptr;     // [Scap][3], then d_scan_plane, then one float4 for d_scan_np
   float4* d_scan_plane = nullptr;  // [Scap][2] plane-form layout (R36)
   int* d_scan_np = nullptr;     // number of scan points not in plane form (prepare_scan)
+  bool scan_prepared = false;   // a scan went through prepare_scan (mcs_scan_nonplanar)
   float4* d_items = nullptr;    // [nb*Ncap][4]
   int32_t* d_order = nullptr;   // [nb*Ncap] sweep order (item ids, coherence-sorted)
   unsigned long long* d_skeys = nullptr;      // [nb*Ncap] coherence keys (a1)

@@ -154,6 +154,7 @@ def load() -> C.CDLL:
         "mcs_plan_migration": (st, [i32, vp, vp, vp]),
         "mcs_peer_migration_state": (i32, [vp]),
         "mcs_graph_state": (i32, [vp]),
+        "mcs_scan_nonplanar": (st, [vp, vp]),
         "mcs_get_global_pose": (i32, [vp, C.c_int64, vp]),
         "mcs_get_pose": (st, [vp, i32, vp]),
         "mcs_config_size": (C.c_size_t, []),
@@ -308,6 +309,13 @@ class Context:
     def graph_captured(self) -> bool:
         """True when the library replays a captured CUDA graph of the update body."""
         return bool(self._lib.mcs_graph_state(self._ctx))
+
+    def scan_nonplanar(self) -> int:
+        """Points of the last prepared scan whose covariance is not plane-form (0: the sweep's
+        plane-form instantiation runs; R36, mcs_scan_nonplanar)."""
+        n = C.c_int32(0)
+        self._check(self._lib.mcs_scan_nonplanar(self._ctx, C.byref(n)))
+        return int(n.value)
 
     def get_pose(self, index: int) -> np.ndarray:
         """One local particle's current pose (12,) fp32 [R|t] row-major (mcs_get_pose)."""

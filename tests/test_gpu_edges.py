@@ -32,6 +32,7 @@ FEW = 64
 def _eval_parity(s, **kw):
     with make_ctx(s, **kw) as ctx:
         g = ctx.eval(s.scan_mean3, s.scan_cov6)
+        g["nonplanar"] = ctx.scan_nonplanar()
     o = oracle.particles(orc_cfg(s, **kw), oracle.Keyframes(s.keyframes, s.D, s.r), s.D_now,
                          s.pose12.copy(), s.kf_pose12.copy(), s.scan_mean3, s.scan_cov6,
                          apply_update=False, slots=True)
@@ -216,3 +217,52 @@ def test_keyframe_bbox_extent_limit():
                     with pytest.raises(mcs.MCSError) as ei:
                         ctx.add_keyframe(m, cov, float(before))
                     assert ei.value.status == 1 and ctx.sizes[1] == before
+
+
+def _cov6_from_eig(rng, lam):
+    """fp32 cov6 (xx, xy, xz, yy, yz, zz) of V diag(lam) V^T, V random rotations (fp64)."""
+    V, _ = np.linalg.qr(rng.standard_normal((len(lam), 3, 3)))
+    A = np.einsum("nij,nj,nkj->nik", V, lam, V)
+    return np.ascontiguousarray(A[:, [0, 0, 0, 1, 1, 2], [0, 1, 2, 1, 2, 2]].astype(np.float32))
+
+
+def test_plane_form_scan_takes_the_plane_path(c2s):
+    """The synthetic scans are GICP plane-regularised (eigenvalues (1, 1, 1e-3), R9): every
+    point is plane-form, so the sweep's plane instantiation runs (R36) — parity as usual."""
+    g, _ = _eval_parity(c2s)
+    assert g["nonplanar"] == 0
+
+
+def test_general_scan_covariances(c2s):
+    """Random SPD scan covariances (three distinct eigenvalues, log-uniform in [1e-3, 1]):
+    the general instantiation (Sigma = lam3 I + u u^T + v v^T) against the oracle."""
+    rng = np.random.default_rng(36)
+    lam = np.exp(rng.uniform(np.log(1e-3), 0.0, (c2s.S, 3)))
+    s = dataclasses.replace(c2s, scan_cov6=_cov6_from_eig(rng, lam))
+    g, _ = _eval_parity(s)
+    assert g["nonplanar"] == s.S
+    _update_parity(s)
+
+
+def test_one_general_point_selects_the_general_path(c2s):
+    """A single non-plane point sends the whole scan through the general instantiation."""
+    rng = np.random.default_rng(7)
+    c6 = c2s.scan_cov6.copy()
+    c6[17] = _cov6_from_eig(rng, np.array([[0.7, 0.3, 2e-3]]))[0]
+    s = dataclasses.replace(c2s, scan_cov6=c6)
+    g, _ = _eval_parity(s)
+    assert g["nonplanar"] == 1
+    _update_parity(s)
+
+
+@pytest.mark.parametrize("split,plane", [(1e-7, True), (2e-6, False)])
+def test_plane_merge_tolerance(c2s, split, plane):
+    """R36's merge rule: top-two eigenvalue splits within 2^-21 of the largest (4 ulps, the
+    rounding of the fp32 entries) are plane-form (their mean is used), larger ones are not;
+    both sides of the rule agree with the oracle, which uses the covariance as given."""
+    rng = np.random.default_rng(11)
+    lam = np.tile([1.0 + split, 1.0, 1e-3], (c2s.S, 1))
+    s = dataclasses.replace(c2s, scan_cov6=_cov6_from_eig(rng, lam))
+    g, _ = _eval_parity(s)
+    assert (g["nonplanar"] == 0) == plane, g["nonplanar"]
+    _update_parity(s)
