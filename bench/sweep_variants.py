@@ -9,11 +9,9 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 VARIANTS = {
-    "pre0": ["MCS_SWEEP_PRELOAD=0"],
-    "pre1": ["MCS_SWEEP_PRELOAD=1"],
-    "pre2": ["MCS_SWEEP_PRELOAD=2"],
-    "pre0b": ["MCS_SWEEP_PRELOAD=0"],
-    "pre1b": ["MCS_SWEEP_PRELOAD=1"],
+    "base": [],
+    "morton4": ["MCS_MORTON_BITS=4"],
+    "morton4_s8": ["MCS_MORTON_BITS=4", "MCS_MORTON_SCALE=8.0f"],
 }
 OUT = os.path.join(ROOT, "bench", "_variants")
 

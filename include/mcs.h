@@ -135,7 +135,7 @@ typedef struct mcs_config {
                                     processes) when every rank's state is reachable, else (and
                                     with 0) packed and exchanged by NCCL send/recv or the
                                     transport's alltoallv                                     */
-  int32_t  point_splits;         /* scan-point ranges per work item in the sweep, 1..8; 0 (default)
+  int32_t  point_splits;         /* scan-point ranges per work item in the sweep, 1..16; 0 (default)
                                     = auto: more splits when the particles alone cannot fill the
                                     GPU (results differ only in fp rounding; bitwise equality of
                                     runs holds for a fixed value)                               */

@@ -357,10 +357,10 @@ mcs_status mcs_create(const mcs_config* cfg, mcs_ctx** out) {
       (cfg->clone_split != 0 && cfg->clone_split != 1) ||
       (cfg->peer_migration != 0 && cfg->peer_migration != 1) ||
       (cfg->graph_replay != 0 && cfg->graph_replay != 1) ||
-      cfg->point_splits < 0 || cfg->point_splits > 8 || cfg->kf_table_mib < 0 ||
+      cfg->point_splits < 0 || cfg->point_splits > 16 || cfg->kf_table_mib < 0 ||
       cfg->kf_table_mib > 65536) {
     g_create_error = "corr_mode must be CELL or NN27 (with 0 < nn_radius <= voxel_resolution), "
-                     "clone_split, peer_migration and graph_replay 0 or 1; point_splits 0..8; "
+                     "clone_split, peer_migration and graph_replay 0 or 1; point_splits 0..16; "
                      "kf_table_mib 0..65536";
     return MCS_E_INVALID_ARG;
   }

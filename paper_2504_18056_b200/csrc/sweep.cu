@@ -771,8 +771,7 @@ __global__ void reduce_splits_kernel(double* __restrict__ part, size_t pstride, 
   double* r = part + (size_t)k * pstride + (size_t)s * capN + i;
   double v = r[0];
 #pragma unroll
-  for (int q = 1; q < 8; ++q)
-    if (q < P) v += r[(size_t)q * kSlotWords * pstride];
+  for (int q = 1; q < P; ++q) v += r[(size_t)q * kSlotWords * pstride];
   r[0] = v;
 }
 
