@@ -10,8 +10,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 VARIANTS = {
     "base": [],
-    "morton4": ["MCS_MORTON_BITS=4"],
-    "morton4_s8": ["MCS_MORTON_BITS=4", "MCS_MORTON_SCALE=8.0f"],
+    "clamp": ["MCS_SWEEP_CLAMP=1"],
+    "base2": [],
+    "clamp2": ["MCS_SWEEP_CLAMP=1"],
 }
 OUT = os.path.join(ROOT, "bench", "_variants")
 

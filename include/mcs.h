@@ -175,8 +175,8 @@ MCS_API mcs_status  mcs_set_stream(mcs_ctx* ctx, void* cuda_stream);
  * keyframe (Eq.9 reading R14).  Builds the keyframe's voxel hash once (off the update
  * clock).  Every particle's new keyframe pose is its current pose: T_k^i := T_t^i (R24).
  * MCS_E_INVALID_ARG if a point's cell lies outside the 21-bit range, if the occupied cells'
- * bounding box is wider than 2047 x 2048 x 1024 cells (the 32-bit bbox-local table keys: at
- * r = 0.5 m that is 1023.5 x 1024 x 512 m), or if n < 1. */
+ * bounding box is wider than 2046 x 2047 x 1023 cells (the 32-bit bbox-local table keys: at
+ * r = 0.5 m that is 1023 x 1023.5 x 511.5 m), or if n < 1. */
 MCS_API mcs_status mcs_add_keyframe(mcs_ctx* ctx, const float* mean3, const float* cov6, int32_t n,
                             double path_length, int32_t* out_kf_id);
 

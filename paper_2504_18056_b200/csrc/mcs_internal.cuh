@@ -61,9 +61,11 @@ constexpr int kMaxNb = MCS_MAX_NEIGHBORS;
 // issued together with the key; the (y, z) pairs (mu'y, mu'z), (S'yy, S'zz), (S'xy, S'xz) land
 // in aligned register pairs, the operands of the sweep's packed FFMA2 math).  Load factor <= 1/4
 // (down to 1/64 within a 64 MiB table, kf_store.cu).
-constexpr unsigned int kEmptyKey32 = 0xFFFFFFFFu;  // dx = 2047 never occurs (ex <= 2047)
+constexpr unsigned int kEmptyKey32 = 0xFFFFFFFFu;  // dx = 2047 never occurs (ex <= 2046)
 constexpr unsigned int kNoKey32 = 0xFFFFFFFEu;     // query key of an out-of-bbox point (dx = 2047)
-constexpr int kMaxEx = 2047, kMaxEy = 2048, kMaxEz = 1024;
+// keyframe bbox extents (cells): one below the 11/11/10-bit fields, so that a query cell clamped
+// to the extents (sweep.cu, MCS_SWEEP_CLAMP) stays a key no slot holds, below the markers
+constexpr int kMaxEx = 2046, kMaxEy = 2047, kMaxEz = 1023;
 constexpr unsigned int kHashMul32 = 0x9E3779B1u;
 
 struct KfMeta {                 // one per keyframe (device array, read through L1)

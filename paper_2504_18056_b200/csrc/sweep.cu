@@ -43,6 +43,10 @@ namespace mcs {
 #define MCS_SWEEP_PACKED_H 2  // 1: the H~ path's rows 1-2 as packed column pairs; 2: all of
                               // P, phi-phi and b~_phi as pairs (signs folded, undone at flush)
 #endif
+#ifndef MCS_SWEEP_CLAMP
+#define MCS_SWEEP_CLAMP 1  // 1: out-of-bbox cells clamped to the extents instead of the sentinel
+                           // (C2 sweep 5.546 -> 5.490 ms: two fewer ALU instructions per point)
+#endif
 #ifndef MCS_SWEEP_GACC
 #define MCS_SWEEP_GACC 0  // 1: fp64 stage totals in the (SoA) partial records, not shared memory
 #endif
@@ -214,8 +218,8 @@ __global__ void __launch_bounds__(kSweepThreads, kCorr == MCS_CORR_NN27 ? MCS_NN
   KfMeta m;
 #if MCS_SWEEP_CONVERGENT
   // a thread without an item runs the stage loop with the others, on keyframe 0's table with an
-  // empty bbox: every point reads that table's always-empty sentinel slot and misses, and the
-  // record is never written.  The loop then stays warp-convergent, and ptxas keeps its bound in
+  // empty bbox: every point probes one fixed slot (the sentinel, or with MCS_SWEEP_CLAMP the
+  // clamped cell (0, 0, 0)), and the record is never written.  The loop then stays warp-convergent, and ptxas keeps its bound in
   // a uniform register instead of a spilled one
   m = kmeta[active ? kf : 0];
   if (!active) m.ex = m.ey = m.ez = 0;
@@ -252,11 +256,21 @@ __global__ void __launch_bounds__(kSweepThreads, kCorr == MCS_CORR_NN27 ? MCS_NN
     const float2 fyz = __ffma2_rd(p.qyz, bc(inv_r), bc(kMagic));
     const unsigned int dy = (unsigned)__float_as_int(fyz.x) - offy;
     const unsigned int dz = (unsigned)__float_as_int(fyz.y) - offz;
+#if MCS_SWEEP_CLAMP
+    // outside the keyframe's bbox: the cell clamped to the extents has a coordinate equal to
+    // its extent, so no slot holds its key (every stored cell lies inside, and extents of at
+    // most 2046 x 2047 x 1023 keep it below the empty / no-key markers); it probes an
+    // ordinary, almost always empty, slot
+    const unsigned int lk = local_key(min(dx, m.ex), min(dy, m.ey), min(dz, m.ez));
+    p.key = lk;
+    p.h = slot_hash(lk, m.shift);
+#else
     // outside the keyframe's bbox: a key no slot holds, probing the always-empty sentinel slot
     const bool in = (dx < m.ex) & (dy < m.ey) & (dz < m.ez);
     const unsigned int lk = local_key(dx, dy, dz);
     p.key = in ? lk : kNoKey32;
     p.h = in ? slot_hash(lk, m.shift) : m.mask + 1;  // the hash is < cap already
+#endif
     MCS_DCHECK(!active || p.h <= m.mask + 1);
     return p;
   };

@@ -199,13 +199,13 @@ def test_combine_shapes_agree_bitwise():
 
 
 def test_keyframe_bbox_extent_limit():
-    """mcs.h: a keyframe's occupied cells must fit 2047 x 2048 x 1024 cells (the 32-bit
+    """mcs.h: a keyframe's occupied cells must fit 2046 x 2047 x 1023 cells (the 32-bit
     bbox-local table keys); one cell more on any axis is MCS_E_INVALID_ARG with no keyframe
     added, exactly the limit is accepted."""
     r = 0.5
     cov = np.tile(np.array([0.5, 0, 0, 0.5, 0, 0.5], np.float32), (2, 1))
     with mcs.Context(4, 4, 8, voxel_resolution=r) as ctx:
-        for axis, cells in ((0, 2047), (1, 2048), (2, 1024)):
+        for axis, cells in ((0, 2046), (1, 2047), (2, 1023)):
             for extra, ok in ((0, True), (1, False)):
                 m = np.zeros((2, 3), np.float32)
                 m[1, axis] = (cells - 1 + extra) * r + 0.1  # cells 0 .. cells - 1 + extra
