@@ -10,9 +10,10 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 VARIANTS = {
     "base": [],
-    "clamp": ["MCS_SWEEP_CLAMP=1"],
+    "lea": ["MCS_SWEEP_LEA_KEY=1"],
+    "resolve1": ["MCS_SWEEP_RESOLVE1=1"],
+    "both": ["MCS_SWEEP_LEA_KEY=1", "MCS_SWEEP_RESOLVE1=1"],
     "base2": [],
-    "clamp2": ["MCS_SWEEP_CLAMP=1"],
 }
 OUT = os.path.join(ROOT, "bench", "_variants")
 

@@ -85,6 +85,11 @@ __host__ __device__ inline unsigned int local_key(unsigned int dx, unsigned int 
                                                   unsigned int dz) {
   return (dx << 21) | (dy << 10) | dz;
 }
+// the same key for in-range fields (dx < 2^11, dy < 2^11, dz < 2^10), as two shift-adds (LEA)
+__host__ __device__ inline unsigned int local_key_lea(unsigned int dx, unsigned int dy,
+                                                      unsigned int dz) {
+  return (((dx << 11) + dy) << 10) + dz;
+}
 
 __host__ __device__ inline unsigned int slot_hash(unsigned int key, unsigned int shift) {
   return (key * kHashMul32) >> shift;
