@@ -10,10 +10,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 VARIANTS = {
     "base": [],
-    "lea": ["MCS_SWEEP_LEA_KEY=1"],
-    "resolve1": ["MCS_SWEEP_RESOLVE1=1"],
-    "both": ["MCS_SWEEP_LEA_KEY=1", "MCS_SWEEP_RESOLVE1=1"],
+    "f32": ["MCS_PART_F32=1"],
     "base2": [],
+    "f32b": ["MCS_PART_F32=1"],
 }
 OUT = os.path.join(ROOT, "bench", "_variants")
 
