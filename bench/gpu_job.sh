@@ -1,2 +1,2 @@
-python bench/sweep_variants.py run 2>&1
-for v in base morton4 morton4_s8; do MCS_LIB=bench/_variants/libmcs_$v.so python bench/shard_splits.py 12500 0 | sed "s/^/$v /"; done
+python bench.py --config c4 --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/bench_c4.json 2> gpurun_out/bench_c4.err; python -c "import json; d=json.load(open('gpurun_out/bench_c4.json')); print('c4', d['ms_per_step'], d.get('phase_ms'), d['value'])"
+python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/ref.json 2> gpurun_out/ref.err; tail -c 400 gpurun_out/ref.json
