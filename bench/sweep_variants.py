@@ -9,10 +9,10 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 VARIANTS = {
-    "base": [],
-    "f32": ["MCS_PART_F32=1"],
-    "base2": [],
-    "f32b": ["MCS_PART_F32=1"],
+    "c256": ["MCS_SWEEP_CHUNK_PLANE=256"],
+    "c448": ["MCS_SWEEP_CHUNK_PLANE=448"],
+    "c448t": ["MCS_SWEEP_CHUNK_PLANE=448", "MCS_SWEEP_TRIM_SPLITS=1"],
+    "c512t": ["MCS_SWEEP_CHUNK_PLANE=512", "MCS_SWEEP_TRIM_SPLITS=1"],
 }
 OUT = os.path.join(ROOT, "bench", "_variants")
 

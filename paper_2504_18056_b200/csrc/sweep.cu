@@ -17,6 +17,7 @@
 // halves of the 3-vector / 3x3 math run as packed FFMA2.  R Sigma_j R^T uses the per-scan
 // spectral form of Sigma_j (prepare_scan_kernel below).  Accumulation is two-level (fp32 within
 // a 256-point stage, fp64 across stages) in a fixed order: bitwise reproducible.  DESIGN.md §5.
+#include <algorithm>
 #include <atomic>
 #include <type_traits>
 
@@ -54,7 +55,8 @@ namespace mcs {
 #define MCS_SWEEP_GACC 0  // 1: fp64 stage totals in the (SoA) partial records, not shared memory
 #endif
 #ifndef MCS_SWEEP_STATIC_SMEM  // static shared arrays when they fit in 48 KB (default build)
-#if MCS_SWEEP_TMA || MCS_SWEEP_GACC || (MCS_SWEEP_CHUNK + 2) * 48 + 224 * MCS_SWEEP_THREADS > 49152
+#if MCS_SWEEP_TMA || MCS_SWEEP_GACC || (MCS_SWEEP_CHUNK + 2) * 48 + 224 * MCS_SWEEP_THREADS > 49152 || \
+    (MCS_SWEEP_CHUNK_PLANE + 2) * 32 + 232 * MCS_SWEEP_THREADS > 49152
 #define MCS_SWEEP_STATIC_SMEM 0
 #else
 #define MCS_SWEEP_STATIC_SMEM 1
@@ -70,7 +72,19 @@ namespace mcs {
 #define MCS_NN27_BATCH 9  // NN27: cells whose first-probe loads are issued together (1, 3, 9, 27)
 #endif
 constexpr int kSweepThreads = MCS_SWEEP_THREADS;
-constexpr int kChunk = MCS_SWEEP_CHUNK;  // scan points per shared-memory stage (48 B each)
+#ifndef MCS_SWEEP_TRIM_SPLITS
+#define MCS_SWEEP_TRIM_SPLITS 1  // 1: as many point splits as the plane-form stages fill
+#endif
+#ifndef MCS_SWEEP_CHUNK_PLANE
+// stage points of the plane-form instantiation (32 B each).  C2 sweep by stage size (ms): 256
+// 5.48, 384 5.45, 416 5.42, 448 5.40, 456 5.47, 480 5.46, 512 5.43 (3 splits of 4/4/2 stages
+// at 448 beat 3/3/3 at 456); with the split count trimmed to the stages (12.5k particles:
+// 10 stages over 5 splits, not 8 with 3 empty) 448 is also the best for the strong-scaling
+// shards (12.5k 0.915, 25k 1.617, 50k 2.959 ms per update vs 0.932 / 1.647 / 2.980 at 256)
+#define MCS_SWEEP_CHUNK_PLANE 448
+#endif
+constexpr int kChunkGeneral = MCS_SWEEP_CHUNK;      // scan points per shared-memory stage (48 B)
+constexpr int kChunkPlane = MCS_SWEEP_CHUNK_PLANE;  // the same for plane-form points (32 B)
 
 struct Probe {
   float4 s0, s1, s2;   // slot payload at the first probe position (speculatively loaded)
@@ -175,6 +189,7 @@ __global__ void __launch_bounds__(kSweepThreads, kCorr == MCS_CORR_NN27 ? MCS_NN
   using PlaneTag = std::integral_constant<bool, kPlane>;
   // dynamic shared memory: [(kChunk + 2) * 3] float4 scan stage, then [28][threads] fp64 totals
   constexpr int kW = kPlane ? 2 : 3;          // float4 words per scan point in the stage
+  constexpr int kChunk = kPlane ? kChunkPlane : kChunkGeneral;
   constexpr int kStage = (kChunk + 2) * kW;  // float4 per stage buffer (2 spare points)
   constexpr int kBufs = MCS_SWEEP_TMA ? 2 : 1;
 #if MCS_SWEEP_STATIC_SMEM
@@ -887,16 +902,25 @@ int sweep_splits_for(const mcs_ctx* c, int n) {
 
 void launch_sweep(mcs_ctx* c, int S) {
   const int n_items = c->cfg.neighbor_count * c->N;
-  const int stages = (S + kChunk - 1) / kChunk;
+  const int stages = (S + kChunkGeneral - 1) / kChunkGeneral;  // (an instantiation with fewer
+  // stages than splits leaves the surplus splits' records zero)
   int P = sweep_splits_for(c, c->N);
   P = P > c->part_splits ? c->part_splits : P;
   P = P > stages ? stages : P;
+#if MCS_SWEEP_TRIM_SPLITS
+  {  // no split without a stage in the plane-form instantiation: P = ceil(stages / per split)
+    const int sp = (S + kChunkPlane - 1) / kChunkPlane, per = (sp + P - 1) / P;
+    P = (sp + per - 1) / per;
+  }
+#endif
   c->cur_splits = 1;  // reduce_splits_kernel sums the point splits into split 0's records
   const dim3 grid((n_items + kSweepThreads - 1) / kSweepThreads, P);
   const float inv_r = 1.0f / c->cfg.voxel_resolution;
   static_assert(!(MCS_SWEEP_TMA && MCS_SWEEP_GACC), "the TMA mbarriers follow s_acc");
   constexpr size_t smem = MCS_SWEEP_STATIC_SMEM ? 0 :
-                          sizeof(float4) * (kChunk + 2) * 3 * (MCS_SWEEP_TMA ? 2 : 1) +
+                          sizeof(float4) * (std::max(3 * (kChunkGeneral + 2),
+                                                     2 * (kChunkPlane + 2))) *
+                              (MCS_SWEEP_TMA ? 2 : 1) +
                           (MCS_SWEEP_GACC ? 0 : sizeof(double) * 28 * kSweepThreads) +
                           (MCS_SWEEP_TMA ? 32 : 0);
   const size_t pstride = (size_t)c->cfg.neighbor_count * c->capN;

@@ -1,5 +1,6 @@
-"""Edge cases of the CUDA path against the oracle: scan sizes at and around the 256-point
-shared-memory stage and the 4-point probe batch (1, 2, 3, 5, 255, 256, 257, 513), every
+"""Edge cases of the CUDA path against the oracle: scan sizes at and around the
+shared-memory stages (256 points general, 448 plane-form) and the 4-point probe batch (1, 2,
+3, 5, 255, 256, 257, 447, 448, 449, 513, 897), every
 neighbour count 1..MCS_MAX_NEIGHBORS, GN over all slots, a voxel size of 2 m, and one-point
 keyframes."""
 import dataclasses
@@ -79,7 +80,7 @@ def _update_parity(s, **kw):
     return g, o
 
 
-@pytest.mark.parametrize("S", [1, 2, 3, 5, 255, 256, 257, 513])
+@pytest.mark.parametrize("S", [1, 2, 3, 5, 255, 256, 257, 447, 448, 449, 513, 897])
 def test_scan_sizes_around_stage_and_batch(c2s, S):
     s = dataclasses.replace(c2s, scan_mean3=np.ascontiguousarray(c2s.scan_mean3[:S]),
                             scan_cov6=np.ascontiguousarray(c2s.scan_cov6[:S]))
