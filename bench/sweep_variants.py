@@ -9,10 +9,11 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 VARIANTS = {
-    "c256": ["MCS_SWEEP_CHUNK_PLANE=256"],
-    "c448": ["MCS_SWEEP_CHUNK_PLANE=448"],
-    "c448t": ["MCS_SWEEP_CHUNK_PLANE=448", "MCS_SWEEP_TRIM_SPLITS=1"],
-    "c512t": ["MCS_SWEEP_CHUNK_PLANE=512", "MCS_SWEEP_TRIM_SPLITS=1"],
+    "cdef": [],
+    "c60": ["MCS_SWEEP_CARVEOUT=60"],
+    "c77": ["MCS_SWEEP_CARVEOUT=77"],
+    "c86": ["MCS_SWEEP_CARVEOUT=86"],
+    "c100": ["MCS_SWEEP_CARVEOUT=100"],
 }
 OUT = os.path.join(ROOT, "bench", "_variants")
 

@@ -72,6 +72,9 @@ namespace mcs {
 #define MCS_NN27_BATCH 9  // NN27: cells whose first-probe loads are issued together (1, 3, 9, 27)
 #endif
 constexpr int kSweepThreads = MCS_SWEEP_THREADS;
+#ifndef MCS_SWEEP_CARVEOUT
+#define MCS_SWEEP_CARVEOUT -1  // shared-memory carveout hint (percent) for the plane sweep; -1 default
+#endif
 #ifndef MCS_SWEEP_TRIM_SPLITS
 #define MCS_SWEEP_TRIM_SPLITS 1  // 1: as many point splits as the plane-form stages fill
 #endif
@@ -934,6 +937,10 @@ void launch_sweep(mcs_ctx* c, int S) {
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaFuncSetAttribute(sweep_kernel<MCS_CORR_NN27, false>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+#if MCS_SWEEP_CARVEOUT >= 0
+    cudaFuncSetAttribute(sweep_kernel<MCS_CORR_CELL, true>,
+                         cudaFuncAttributePreferredSharedMemoryCarveout, MCS_SWEEP_CARVEOUT);
+#endif
     if (c->dev >= 0 && c->dev < 128) attr_set[c->dev].store(true, std::memory_order_release);
   }
   if (c->cfg.corr_mode == MCS_CORR_NN27) {
