@@ -326,7 +326,8 @@ MCS_API int32_t mcs_graph_state(const mcs_ctx* ctx);
  * selects the sweep's plane-form instantiation (one rotated vector per point, Sigma =
  * lambda3 I + [x]x^T [x]x); any other value the general one (Sigma = lambda3 I + u u^T + v v^T).
  * Both compute C = Sigma' + R Sigma R^T of Eq.4 up to rounding.  Synchronises the
- * context's stream; MCS_E_STATE before any scan was prepared. */
+ * context's stream (after mcs_update_async on another stream, synchronise that stream first);
+ * MCS_E_STATE before any scan was prepared, MCS_E_INVALID_ARG if n_out is NULL. */
 MCS_API mcs_status mcs_scan_nonplanar(mcs_ctx* ctx, int32_t* n_out);
 
 #ifdef __cplusplus

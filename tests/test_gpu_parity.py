@@ -317,6 +317,9 @@ def test_errors_before_state_change(c1):
     s = c1
     with mcs.Context(10, 2, 16, voxel_resolution=s.r) as ctx:
         with pytest.raises(mcs.MCSError) as ei:
+            ctx.scan_nonplanar()
+        assert ei.value.status == 6  # no scan prepared yet
+        with pytest.raises(mcs.MCSError) as ei:
             ctx.update(s.scan_mean3[:16], s.scan_cov6[:16], 1.0, 0)
         assert ei.value.status == 6  # no keyframe
         bad = s.keyframes[0][1][:16].copy()
