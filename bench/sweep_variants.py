@@ -9,11 +9,9 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 VARIANTS = {
-    "cdef": [],
-    "c60": ["MCS_SWEEP_CARVEOUT=60"],
-    "c77": ["MCS_SWEEP_CARVEOUT=77"],
-    "c86": ["MCS_SWEEP_CARVEOUT=86"],
-    "c100": ["MCS_SWEEP_CARVEOUT=100"],
+    "base": [],
+    "mb5": ["MCS_SWEEP_MINBLOCKS=5"],
+    "mb5_c256": ["MCS_SWEEP_MINBLOCKS=5", "MCS_SWEEP_CHUNK_PLANE=256"],
 }
 OUT = os.path.join(ROOT, "bench", "_variants")
 

@@ -15,8 +15,11 @@
 // Table probes (key + 40 B of payload from one 64-byte slot) are issued in batches of two
 // points, two points ahead of the math, so the L2 gather latency hides behind it; the (y, z)
 // halves of the 3-vector / 3x3 math run as packed FFMA2.  R Sigma_j R^T uses the per-scan
-// spectral form of Sigma_j (prepare_scan_kernel below).  Accumulation is two-level (fp32 within
-// a 256-point stage, fp64 across stages) in a fixed order: bitwise reproducible.  DESIGN.md §5.
+// spectral form of Sigma_j (prepare_scan_kernel below); a scan whose points are all plane-form
+// (GICP's plane regularisation, R36) runs the kPlane instantiation, one rotated vector per
+// point.  A query cell outside the keyframe's bbox is clamped to the bbox extents (a key no slot
+// holds).  Accumulation is two-level (fp32 within a stage of 256 / 448 points, fp64 across
+// stages) in a fixed order: bitwise reproducible.  DESIGN.md §5.
 #include <algorithm>
 #include <atomic>
 #include <type_traits>
