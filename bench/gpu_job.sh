@@ -1,7 +1,2 @@
-# round-2 measurement job (one B200): bench lines, shards, launch list, ncu of the sweep
-python bench.py --steps 30 --warmup 5 > gpurun_out/bench_c2.json 2> gpurun_out/bench_c2.err; python -c "import json; d=json.load(open('gpurun_out/bench_c2.json')); print('c2', d['ms_per_step'], d['phase_ms'], d['e2e']['ms_per_step'], d['roofline']['frac'], d['clocks'])"
-for c in c2_survival c3 c5 c4; do python bench.py --steps 8 --warmup 3 --no-cpu-baseline --config $c > gpurun_out/bench_$c.json 2> gpurun_out/bench_$c.err; python -c "import json; d=json.load(open('gpurun_out/bench_$c.json')); print('$c', d['ms_per_step'], d.get('phase_ms'))"; done
-for n in 12500 25000 50000; do python bench.py --steps 20 --warmup 5 --no-cpu-baseline --particles $n > gpurun_out/shard_$n.json 2> gpurun_out/shard_$n.err; python -c "import json; d=json.load(open('gpurun_out/shard_$n.json')); print($n, round(d['ms_per_step'],4), {k: round(v,4) for k,v in d['phase_ms'].items()})"; done
-ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file gpurun_out/launches.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_launches.log 2>&1; echo launches=$?
-ncu --set full --import-source on --clock-control none -k regex:sweep_kernel --launch-skip 2 --launch-count 2 -o gpurun_out/sweep_r02g -f python bench/one_update.py 2 > gpurun_out/ncu.log 2>&1; echo ncu=$?
-python -c "import __graft_entry__ as g; g.smoke()"
+python bench/sweep_variants.py run
+for v in base noreduce slots slots_noreduce; do MCS_LIB=bench/_variants/libmcs_$v.so python bench/shard_splits.py 12500 0 | sed "s/^/$v /"; done

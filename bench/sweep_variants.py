@@ -10,8 +10,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 VARIANTS = {
     "base": [],
-    "mb5": ["MCS_SWEEP_MINBLOCKS=5"],
-    "mb5_c256": ["MCS_SWEEP_MINBLOCKS=5", "MCS_SWEEP_CHUNK_PLANE=256"],
+    "noreduce": ["MCS_SWEEP_REDUCE=0"],
+    "slots": ["MCS_COMBINE_SLOTS_BELOW=100000000"],
+    "slots_noreduce": ["MCS_COMBINE_SLOTS_BELOW=100000000", "MCS_SWEEP_REDUCE=0"],
 }
 OUT = os.path.join(ROOT, "bench", "_variants")
 

@@ -75,6 +75,9 @@ namespace mcs {
 #define MCS_NN27_BATCH 9  // NN27: cells whose first-probe loads are issued together (1, 3, 9, 27)
 #endif
 constexpr int kSweepThreads = MCS_SWEEP_THREADS;
+#ifndef MCS_SWEEP_REDUCE
+#define MCS_SWEEP_REDUCE 1  // 1: reduce_splits_kernel sums the point splits; 0: a3 reads them all
+#endif
 #ifndef MCS_SWEEP_CARVEOUT
 #define MCS_SWEEP_CARVEOUT -1  // shared-memory carveout hint (percent) for the plane sweep; -1 default
 #endif
@@ -919,7 +922,11 @@ void launch_sweep(mcs_ctx* c, int S) {
     P = (sp + per - 1) / per;
   }
 #endif
+#if MCS_SWEEP_REDUCE
   c->cur_splits = 1;  // reduce_splits_kernel sums the point splits into split 0's records
+#else
+  c->cur_splits = P;  // a3 sums the P records of every item itself
+#endif
   const dim3 grid((n_items + kSweepThreads - 1) / kSweepThreads, P);
   const float inv_r = 1.0f / c->cfg.voxel_resolution;
   static_assert(!(MCS_SWEEP_TMA && MCS_SWEEP_GACC), "the TMA mbarriers follow s_acc");
@@ -960,7 +967,7 @@ void launch_sweep(mcs_ctx* c, int S) {
         c->d_items, c->d_order, n_items, c->d_scan, S, c->d_kf_meta, inv_r, 0.f, c->d_part,
         pstride, c->d_scan_np);
   }
-  if (P > 1) {
+  if (P > 1 && MCS_SWEEP_REDUCE) {
     const long long tot = 29LL * n_items;
     reduce_splits_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, c->stream>>>(
         c->d_part, pstride, c->cfg.neighbor_count, c->N, c->capN, P);
