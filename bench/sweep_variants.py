@@ -10,9 +10,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 VARIANTS = {
     "base": [],
-    "noreduce": ["MCS_SWEEP_REDUCE=0"],
-    "slots": ["MCS_COMBINE_SLOTS_BELOW=100000000"],
-    "slots_noreduce": ["MCS_COMBINE_SLOTS_BELOW=100000000", "MCS_SWEEP_REDUCE=0"],
+    "t256": ["MCS_SWEEP_THREADS=256", "MCS_SWEEP_MINBLOCKS=2"],
+    "t256_c256": ["MCS_SWEEP_THREADS=256", "MCS_SWEEP_MINBLOCKS=2", "MCS_SWEEP_CHUNK_PLANE=256"],
+    "t64": ["MCS_SWEEP_THREADS=64", "MCS_SWEEP_MINBLOCKS=8", "MCS_SWEEP_CHUNK_PLANE=256"],
 }
 OUT = os.path.join(ROOT, "bench", "_variants")
 
