@@ -46,8 +46,8 @@ PAPER_CONTEXT = {"particles_in_real_time": 100000, "ms_per_frame": [50, 60],
                  "what": "whole SLAM system per frame (indoor elevator ~50 ms, outdoor forest "
                          "~60 ms), scan size not stated",
                  "hardware": "NVIDIA GeForce RTX 4090", "cite": "PAPER.md P:203, P:240"}
-LIBRARY_LAUNCHES_PER_UPDATE = 7  # CUB radix sort of the coherence keys inside a1: histogram,
-#                                  exclusive sum, 5 onesweep passes
+LIBRARY_LAUNCHES_PER_UPDATE = 6  # CUB radix sort of the coherence keys inside a1: histogram,
+#                                  exclusive sum, 4 onesweep passes (the top 32 key bits)
 
 
 def dist_env():

@@ -10,9 +10,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 VARIANTS = {
     "base": [],
-    "t256": ["MCS_SWEEP_THREADS=256", "MCS_SWEEP_MINBLOCKS=2"],
-    "t256_c256": ["MCS_SWEEP_THREADS=256", "MCS_SWEEP_MINBLOCKS=2", "MCS_SWEEP_CHUNK_PLANE=256"],
-    "t64": ["MCS_SWEEP_THREADS=64", "MCS_SWEEP_MINBLOCKS=8", "MCS_SWEEP_CHUNK_PLANE=256"],
+    "sort32": ["MCS_SORT_BITS=32"],
+    "sort24": ["MCS_SORT_BITS=24"],
 }
 OUT = os.path.join(ROOT, "bench", "_variants")
 

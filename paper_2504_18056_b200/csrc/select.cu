@@ -37,6 +37,12 @@ namespace mcs {
 #define MCS_MORTON_PTS 2  // reference points on the x, y (, z) axes
 #endif
 constexpr int kMortonBitsPerDim = MCS_MORTON_BITS;
+#ifndef MCS_SORT_BITS
+// the top 32 bits of the (keyframe, Morton) key are sorted: four radix passes instead of five
+// (the finest Morton level of 3 of the 6 coordinates stays in input order).  C2 update 5.627 ->
+// 5.626 ms, 12.5k particles 0.915 -> 0.907 ms; 24 bits costs the sweep its coherence (C2 5.83)
+#define MCS_SORT_BITS 32
+#endif
 constexpr int kMortonDims = 3 * MCS_MORTON_PTS;
 constexpr int kMortonBits = kMortonDims * kMortonBitsPerDim;
 
@@ -166,8 +172,10 @@ mcs_status launch_select(mcs_ctx* c, int mode) {
       c->cfg.gn_slots == MCS_GN_ALL_SLOTS, mode, c->d_items, c->d_meta, c->d_to,
       c->d_skeys, c->d_sids, inactive);
   size_t tb = c->cub_temp_bytes;
+  // MCS_SORT_BITS: the number of key bits sorted (the top ones; 0 = all)
+  const int begin_bit = (MCS_SORT_BITS > 0 && end_bit > MCS_SORT_BITS) ? end_bit - MCS_SORT_BITS : 0;
   if (cub::DeviceRadixSort::SortPairs(c->d_cub_temp, tb, c->d_skeys, c->d_skeys_out, c->d_sids,
-                                      c->d_order, nb_max * N, 0, end_bit, c->stream) !=
+                                      c->d_order, nb_max * N, begin_bit, end_bit, c->stream) !=
       cudaSuccess)
     return MCS_E_CUDA;
   return cudaGetLastError() == cudaSuccess ? MCS_OK : MCS_E_CUDA;
