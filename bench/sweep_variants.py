@@ -10,8 +10,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 VARIANTS = {
     "base": [],
-    "sort32": ["MCS_SORT_BITS=32"],
-    "sort24": ["MCS_SORT_BITS=24"],
+    "u4": ["MCS_SELECT_UNROLL=4"],
+    "u8": ["MCS_SELECT_UNROLL=8"],
 }
 OUT = os.path.join(ROOT, "bench", "_variants")
 

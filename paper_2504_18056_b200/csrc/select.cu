@@ -37,6 +37,10 @@ namespace mcs {
 #define MCS_MORTON_PTS 2  // reference points on the x, y (, z) axes
 #endif
 constexpr int kMortonBitsPerDim = MCS_MORTON_BITS;
+#ifndef MCS_SELECT_UNROLL
+#define MCS_SELECT_UNROLL 1  // the keyframe-distance loop of select_kernel, unrolled
+#endif
+constexpr int kSelectUnroll = MCS_SELECT_UNROLL;
 #ifndef MCS_SORT_BITS
 // the top 32 bits of the (keyframe, Morton) key are sorted: four radix passes instead of five
 // (the finest Morton level of 3 of the 6 coordinates stays in input order).  C2 update 5.627 ->
@@ -84,8 +88,9 @@ __global__ void select_kernel(const float* __restrict__ pose, int capN, int N,
 #pragma unroll
   for (int s = 0; s < kMaxNb; ++s) { bd[s] = 0.f; bk[s] = -1; }
   const float4* tk = kft + (size_t)i * capK;  // the keyframe translations (16 B each)
+#pragma unroll kSelectUnroll
   for (int k = 0; k < K; ++k) {
-    const float4 t4 = tk[k];
+    const float4 t4 = __ldg(tk + k);
     float dx = __fsub_rn(t4.x, Tt[3]);
     float dy = __fsub_rn(t4.y, Tt[7]);
     float dz = __fsub_rn(t4.z, Tt[11]);
