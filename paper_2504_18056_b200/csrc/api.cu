@@ -900,7 +900,8 @@ mcs_status mcs_update(mcs_ctx* ctx, const float* scan_mean3, const float* scan_c
   CUDA_TRY(ctx, to_device(raw_c, scan_cov6, sizeof(float) * 6 * n_pts, st));
   s = validate_scan(ctx, n_pts);
   if (s != MCS_OK) return s;
-  launch_prepare_scan(raw_m, raw_c, n_pts, ctx->d_scan, ctx->d_scan_plane, ctx->d_scan_np, st);
+  CUDA_TRY(ctx, launch_prepare_scan(raw_m, raw_c, n_pts, ctx->d_scan, ctx->d_scan_plane,
+                                    ctx->d_scan_np, st));
   ctx->scan_prepared = true;
   s = run_update(ctx, n_pts, D_now, resample_u);
   if (s != MCS_OK) {
@@ -950,7 +951,10 @@ mcs_status mcs_update_async(mcs_ctx* ctx, const float* d_scan_mean3, const float
   if (s != MCS_OK) return s;
   cudaStream_t saved = ctx->stream;
   if (cuda_stream) ctx->stream = (cudaStream_t)cuda_stream;
-  launch_prepare_scan(d_scan_mean3, d_scan_cov6, n_pts, ctx->d_scan, ctx->d_scan_plane, ctx->d_scan_np, ctx->stream);
+  const cudaError_t pe = launch_prepare_scan(d_scan_mean3, d_scan_cov6, n_pts, ctx->d_scan,
+                                             ctx->d_scan_plane, ctx->d_scan_np, ctx->stream);
+  if (pe != cudaSuccess) ctx->stream = saved;  // (CUDA_TRY returns)
+  CUDA_TRY(ctx, pe);
   ctx->scan_prepared = true;
   s = run_update(ctx, n_pts, D_now, resample_u);
   if (s != MCS_OK) {
@@ -985,7 +989,8 @@ mcs_status mcs_eval(mcs_ctx* ctx, const float* scan_mean3, const float* scan_cov
   CUDA_TRY(ctx, to_device(raw_c, scan_cov6, sizeof(float) * 6 * n_pts, st));
   s = validate_scan(ctx, n_pts);
   if (s != MCS_OK) return s;
-  launch_prepare_scan(raw_m, raw_c, n_pts, ctx->d_scan, ctx->d_scan_plane, ctx->d_scan_np, st);
+  CUDA_TRY(ctx, launch_prepare_scan(raw_m, raw_c, n_pts, ctx->d_scan, ctx->d_scan_plane,
+                                    ctx->d_scan_np, st));
   ctx->scan_prepared = true;
   const size_t NS = (size_t)ctx->N * ctx->cfg.neighbor_count;
   double* dl = nullptr;

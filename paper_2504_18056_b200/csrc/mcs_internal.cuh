@@ -250,8 +250,8 @@ cudaError_t kf_build(mcs_ctx* c, const float* d_mean3, const float* d_cov6, int 
 // form Sigma = lambda3 I + u u^T + v v^T, fp64 Jacobi), and the plane-form layout {mu, lambda3}
 // {x, 0} (Sigma = lambda3 I + [x]x^T [x]x, R36) in out_plane; *nonplanar = number of points
 // that are not plane-form
-void launch_prepare_scan(const float* mean3, const float* cov6, int S, float4* out,
-                         float4* out_plane, int* nonplanar, cudaStream_t st);
+cudaError_t launch_prepare_scan(const float* mean3, const float* cov6, int S, float4* out,
+                                float4* out_plane, int* nonplanar, cudaStream_t st);
 // a1; mode: kSelectUpdate (H~, b~ for slots in G), kSelectEval (all slots), kSelectWeight (none)
 enum { kSelectUpdate = 0, kSelectEval = 1, kSelectWeight = 2 };
 mcs_status launch_select(mcs_ctx* c, int mode);  // MCS_E_CUDA if a launch (or the sort) fails

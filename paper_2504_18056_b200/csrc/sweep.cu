@@ -888,11 +888,13 @@ __global__ void prepare_scan_kernel(const float* __restrict__ mean3,
   if (!plane) atomicAdd(nonplanar, 1);
 }
 
-void launch_prepare_scan(const float* mean3, const float* cov6, int S, float4* out,
-                         float4* out_plane, int* nonplanar, cudaStream_t st) {
-  cudaMemsetAsync(nonplanar, 0, sizeof(int), st);
+cudaError_t launch_prepare_scan(const float* mean3, const float* cov6, int S, float4* out,
+                                float4* out_plane, int* nonplanar, cudaStream_t st) {
+  const cudaError_t e = cudaMemsetAsync(nonplanar, 0, sizeof(int), st);
+  if (e != cudaSuccess) return e;
   prepare_scan_kernel<<<(S + 127) / 128, 128, 0, st>>>(mean3, cov6, S, out, out_plane,
                                                        nonplanar);
+  return cudaGetLastError();
 }
 
 #ifndef MCS_SPLIT_TARGET_CTAS
