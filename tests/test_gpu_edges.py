@@ -54,8 +54,10 @@ def _update_parity(s, **kw):
     pose, kp, L = s.pose12.copy(), s.kf_pose12.copy(), np.zeros(s.N)
     o = oracle.update(orc_cfg(s, **kw, **nd), oracle.Keyframes(s.keyframes, s.D, s.r),
                       s.D_now, pose, kp, L, s.scan_mean3, s.scan_cov6, s.U)
-    rt = L_RTOL if s.S >= FEW else 2e-3
-    assert np.all(np.abs(g["loglik"] - o["loglik"]) <= rt * np.abs(o["loglik"]) + 1e-6)
+    if s.S >= FEW:  # the north-star contract: 1e-4 relative, no absolute slack
+        assert np.all(np.abs(g["loglik"] - o["loglik"]) <= L_RTOL * np.abs(o["loglik"]))
+    else:
+        assert np.all(np.abs(g["loglik"] - o["loglik"]) <= 2e-3 * np.abs(o["loglik"]) + 1e-6)
     np.testing.assert_array_equal(g["flags"] & 1, o["flags"] & 1)
     if s.S < FEW:
         # g = -2 sum J^T Omega e inherits the ~1e-4-per-point rounding of e, with cancellation
