@@ -32,6 +32,8 @@ METRIC = ("particle·point likelihood+grad evals/s; ms per update @100k particle
           "1–8 GPU")
 UNIT = "particle·point evals/s"
 FLOPS_MATCHED = 236.0    # FP32 flops per matched (particle, point, slot) with H~, b~
+FLOPS_MATCHED_PLANE = 191.0  # the same with a plane-form scan covariance (R36): R Sigma R^T as
+#                              x = Rn (15) + lam3 I + [x]x^T [x]x (21) instead of 81
 FLOPS_UNMATCHED = 21.0   # transform + key for an unmatched triple
 GATHER_MATCHED = 44.0    # algorithmic bytes per matched triple: 8-B key + 12-B mu'
 #                          + 24-B Sigma' (the slot layout moves 40 B + the 4-B key per first probe)
@@ -479,6 +481,8 @@ def run_gpu(args):
     sm_mhz = peaks.get("sm_max_mhz", 1965.0)
     fp32_peak = 148 * 128 * 2 * sm_mhz * 1e6 / 1e12  # TFLOP/s
     flops = matched * FLOPS_MATCHED + (triples - matched) * FLOPS_UNMATCHED
+    plane_scan = ctx.scan_nonplanar() == 0  # which sweep instantiation ran (R36)
+    flops_plane = matched * FLOPS_MATCHED_PLANE + (triples - matched) * FLOPS_UNMATCHED
     sweep_avg = float(np.mean(sweep_ms))
     achieved = flops / (sweep_avg * 1e-3) / 1e12
     gather = (matched * GATHER_MATCHED + (triples - matched) * GATHER_UNMATCHED)
@@ -504,6 +508,11 @@ def run_gpu(args):
                      "peak_source": f"148 SM x 128 FP32 lanes x 2 x {sm_mhz:.0f} MHz "
                                     f"({peak_src} sm_max_mhz)",
                      "flops_per_launch": flops, "sweep_ms": sweep_avg,
+                     "flops_basis": "236 per matched triple (SURVEY Appendix A, general covariances)"
+                                    ", 21 per unmatched",
+                     "plane_form_scan": plane_scan,
+                     "frac_plane_form_flops": ((flops_plane / (sweep_avg * 1e-3) / 1e12)
+                                               / fp32_peak) if plane_scan else None,
                      "l2_gather_GBps": gather / (sweep_avg * 1e-3) / 1e9,
                      "gather": gather_roofline(gather, sweep_avg),
                      "ncu": committed_ncu_context(gather)},
