@@ -897,6 +897,9 @@ cudaError_t launch_prepare_scan(const float* mean3, const float* cov6, int S, fl
   return cudaGetLastError();
 }
 
+#ifndef MCS_SPLIT_MIDRANGE
+#define MCS_SPLIT_MIDRANGE 1
+#endif
 #ifndef MCS_SPLIT_TARGET_CTAS
 // auto point splits aim for ~7,000 CTAs (~12 waves of 148 x 4): more, shorter CTAs balance the
 // uneven per-item hit rates (C2 sweep: 1 split 6.27 ms, 2 6.19, 3 6.13, 4 6.17; with a3's
@@ -907,7 +910,13 @@ cudaError_t launch_prepare_scan(const float* mean3, const float* cov6, int S, fl
 int sweep_splits_for(const mcs_ctx* c, int n) {
   if (c->cfg.point_splits > 0) return c->cfg.point_splits;
   const long long ctas = ((long long)c->cfg.neighbor_count * n + kSweepThreads - 1) / kSweepThreads;
-  const long long p = (MCS_SPLIT_TARGET_CTAS + ctas - 1) / (ctas > 0 ? ctas : 1);
+  long long p = (MCS_SPLIT_TARGET_CTAS + ctas - 1) / (ctas > 0 ? ctas : 1);
+#if MCS_SPLIT_MIDRANGE
+  // 500-7,000 item CTAs (25k-300k particles at 3 slots): three splits (4/4/2 of the ten
+  // 448-point stages at S = 4,096) measured best — 25k 1.591 vs 1.616 ms with five, 50k 2.930
+  // vs 2.954 with five, 100k (already 3) 5.63; 12.5k (293 CTAs) keeps five, 1M (23k CTAs) one
+  if (ctas >= 500 && ctas < MCS_SPLIT_TARGET_CTAS && p > 3) p = 3;
+#endif
   return (int)(p < 1 ? 1 : (p > 8 ? 8 : p));
 }
 
