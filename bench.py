@@ -346,8 +346,27 @@ def run_gpu(args):
     s = shard(s_all, lo, hi) if world > 1 else s_all
     N, S, K = hi - lo, s.S, s.K
     stream = torch.cuda.Stream(device=dev)
-    ctx = mcs.Context(N, K, S, neighbor_count=3, loop_recency_gap=s.gap, voxel_resolution=s.r,
-                      device=local, **extra)
+    ckw = dict(neighbor_count=3, loop_recency_gap=s.gap, voxel_resolution=s.r, device=local)
+    backend_note = args.dist_backend
+    if world > 1 and args.dist_backend == "nccl":
+        # the library's NCCL communicator; should it fail to come up on any rank, every rank
+        # falls back (collectively) to the host transport over a gloo group, and the line says so
+        ctx, err = None, ""
+        try:
+            ctx = mcs.Context(N, K, S, **ckw, **extra)
+        except Exception as e:  # noqa: BLE001 - reported in the JSON line
+            err = repr(e)[:160]
+        ok = torch.tensor([1 if ctx is not None else 0], device=dev)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if int(ok.item()) == 0:
+            if ctx is not None:
+                ctx.close()
+            gloo = dist.new_group(backend="gloo")
+            ctx = mcs.Context(N, K, S, **ckw, world_size=world, rank=rank,
+                              transport=mcs.TorchDistTransport(gloo))
+            backend_note = f"host transport over gloo: the library NCCL init failed ({err})"
+    else:
+        ctx = mcs.Context(N, K, S, **ckw, **extra)
     ctx.set_stream(stream)
     t0 = time.perf_counter()
     for k, ((m3, c6), d) in enumerate(zip(s.keyframes, s.D)):
@@ -379,6 +398,7 @@ def run_gpu(args):
         ctx.update_async(d_m, d_c, s.D_now, s.U, out, stream=stream)
     torch.cuda.synchronize()
     use_graph = not args.no_graph and (world == 1 or (args.dist_backend == "nccl" and
+                                                      backend_note == "nccl" and
                                                       ctx.peer_migration_state == 1))
     graph = None
     # the library's phase events are recorded inside the captured update, so every timed
@@ -493,7 +513,7 @@ def run_gpu(args):
         "scaling": args.scaling, "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": CONFIGS[args.config][2].format(N=n_total),
                    "particles": n_total, "particles_per_gpu": N, "scan_points": S,
-                   "keyframes": K, "parallelism": f"particle shards x{world} ({args.dist_backend})",
+                   "keyframes": K, "parallelism": f"particle shards x{world} ({backend_note})",
                    "keyframe_cells": int(sum(len(k[0]) for k in s.keyframes)),
                    "l2": "particle state restored from a device snapshot and 256 MiB L2 flush "
                          "before every timed step (untimed)",
