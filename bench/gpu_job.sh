@@ -1,1 +1,2 @@
-for n in 12500 25000 50000; do python bench.py --steps 20 --warmup 5 --no-cpu-baseline --particles $n > gpurun_out/shard_$n.json 2> gpurun_out/shard_$n.err; python -c "import json; d=json.load(open('gpurun_out/shard_$n.json')); print($n, round(d['ms_per_step'],4), {k: round(v,4) for k,v in d['phase_ms'].items()})"; done
+python -m pytest tests/test_gpu_parity.py tests/test_gpu_configs.py tests/test_gpu_edges.py -q -x 2>&1 | tail -2
+python bench/sweep_variants.py run

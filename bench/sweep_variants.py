@@ -9,9 +9,10 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 VARIANTS = {
-    "base": [],
-    "u4": ["MCS_SELECT_UNROLL=4"],
-    "u8": ["MCS_SELECT_UNROLL=8"],
+    "tmem": [],
+    "smem": ["MCS_SWEEP_TMEM_ACC=0"],
+    "tmem_c896": ["MCS_SWEEP_CHUNK_PLANE=896"],
+    "tmem_c672": ["MCS_SWEEP_CHUNK_PLANE=672"],
 }
 OUT = os.path.join(ROOT, "bench", "_variants")
 

@@ -54,6 +54,12 @@ namespace mcs {
 #ifndef MCS_SWEEP_LEA_KEY
 #define MCS_SWEEP_LEA_KEY 1  // 1: the clamped key as two shift-adds (LEA; C2 sweep -0.5 %)
 #endif
+#ifndef MCS_SWEEP_TMEM_ACC
+#define MCS_SWEEP_TMEM_ACC 0  // 1: the fp64 stage totals in tensor memory (tcgen05.ld/st, 64
+                              // columns per CTA) instead of 28 KB of shared memory: parity green,
+                              // C2 sweep 5.409 -> 5.442 ms (the larger L1 does not pay for the
+                              // per-stage TMEM round trips)
+#endif
 #ifndef MCS_SWEEP_GACC
 #define MCS_SWEEP_GACC 0  // 1: fp64 stage totals in the (SoA) partial records, not shared memory
 #endif
@@ -150,6 +156,24 @@ __device__ __forceinline__ float4 lds4(uint32_t addr) {
   return v;
 }
 
+// ---- TMEM (tcgen05) for the fp64 stage totals (MCS_SWEEP_TMEM_ACC): each thread owns one TMEM
+// lane (its warp's quarter of the 128 lanes), 64 columns = 28 doubles as (lo, hi) word pairs
+__device__ __forceinline__ void tm_st8(uint32_t ta, const uint32_t (&v)[8]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};"
+               ::"r"(ta), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]),
+               "r"(v[6]), "r"(v[7])
+               : "memory");
+}
+__device__ __forceinline__ void tm_ld8(uint32_t ta, uint32_t (&v)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
+                 "=r"(v[6]), "=r"(v[7])
+               : "r"(ta)
+               : "memory");
+}
+__device__ __forceinline__ void tm_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
 // ---- TMA bulk-copy staging (MCS_SWEEP_TMA): mbarrier + cp.async.bulk wrappers ----
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -204,8 +228,10 @@ __global__ void __launch_bounds__(kSweepThreads, kCorr == MCS_CORR_NN27 ? MCS_NN
 #if MCS_SWEEP_STATIC_SMEM
   // static shared memory: link-time addresses, nothing to rematerialise per point
   __shared__ float4 smem_dyn[kBufs * kStage];
+#if !MCS_SWEEP_TMEM_ACC
   __shared__ double s_acc_st[28][kSweepThreads];
   double(*s_acc)[kSweepThreads] = s_acc_st;
+#endif
 #else
   extern __shared__ float4 smem_dyn[];
   // two-level accumulation: fp32 registers within a stage, fp64 totals per thread in shared
@@ -640,6 +666,28 @@ __global__ void __launch_bounds__(kSweepThreads, kCorr == MCS_CORR_NN27 ? MCS_NN
 
   // fp64 totals across stages: [0] l, [1..21] H~, [22..27] b~ (shared memory, or with
   // MCS_SWEEP_GACC the record words 0, 2..22, 23..28 themselves)
+#if MCS_SWEEP_TMEM_ACC
+  static_assert(MCS_SWEEP_STATIC_SMEM && MCS_SWEEP_CONVERGENT && !MCS_SWEEP_TMA &&
+                    !MCS_SWEEP_GACC && kSweepThreads == 128,
+                "TMEM totals: four convergent warps, one TMEM lane quarter each");
+  __shared__ uint32_t s_tmem;
+  if (threadIdx.x < 32) {  // warp 0 allocates 64 columns for the CTA
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 64;" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(&s_tmem))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tm = s_tmem + ((threadIdx.x & ~31u) << 16);  // this warp's lanes, column 0
+  {
+    const uint32_t z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+    for (int c = 0; c < 7; ++c) tm_st8(tm + 8 * c, z);
+    tm_wait_st();
+  }
+#else
   auto tot = [&](int k) -> double& {
 #if MCS_SWEEP_GACC
     return rec(k == 0 ? 0 : k + 1);
@@ -652,8 +700,13 @@ __global__ void __launch_bounds__(kSweepThreads, kCorr == MCS_CORR_NN27 ? MCS_NN
 #endif
 #pragma unroll
     for (int k = 0; k < 28; ++k) tot(k) = 0.0;
+#endif
   auto flush = [&]() {
+#if MCS_SWEEP_TMEM_ACC
+    float d0 = l;
+#else
     tot(0) += (double)l;
+#endif
     l = 0.f;
 #if MCS_SWEEP_PACKED_H
     h[1] = hp01.x; h[2] = hp01.y; h[6] = hp11.x; h[7] = hp11.y; bv[1] = bp12.x; bv[2] = bp12.y;
@@ -669,6 +722,29 @@ __global__ void __launch_bounds__(kSweepThreads, kCorr == MCS_CORR_NN27 ? MCS_NN
     h[8] = hq0.x; h[12] = hq0.y; h[9] = hq1.x; h[13] = hq1.y; h[10] = hq2.x; h[14] = hq2.y;
     hq0 = hq1 = hq2 = bc(0.f);
 #endif
+#if MCS_SWEEP_TMEM_ACC
+    // totals k = 4c .. 4c + 3 (l, H~21, b~6 in that order) in chunk c: load, add, store
+#pragma unroll
+    for (int c = 0; c < 7; ++c) {
+      uint32_t w[8];
+      tm_ld8(tm + 8 * c, w);
+      tm_wait_ld();
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int k = 4 * c + u;
+        const float dk = k == 0 ? d0 : (k <= 21 ? h[k - 1] : bv[k - 22]);
+        const double t = __hiloint2double((int)w[2 * u + 1], (int)w[2 * u]) + (double)dk;
+        w[2 * u] = (uint32_t)__double2loint(t);
+        w[2 * u + 1] = (uint32_t)__double2hiint(t);
+      }
+      tm_st8(tm + 8 * c, w);
+    }
+    tm_wait_st();
+#pragma unroll
+    for (int k = 0; k < 21; ++k) h[k] = 0.f;
+#pragma unroll
+    for (int k = 0; k < 6; ++k) bv[k] = 0.f;
+#else
 #pragma unroll
     for (int k = 0; k < 21; ++k) {
       tot(1 + k) += (double)h[k];
@@ -679,6 +755,7 @@ __global__ void __launch_bounds__(kSweepThreads, kCorr == MCS_CORR_NN27 ? MCS_NN
       tot(22 + k) += (double)bv[k];
       bv[k] = 0.f;
     }
+#endif
   };
 
   // the math of one stage of cnt points in s_pt (active threads)
@@ -789,6 +866,28 @@ __global__ void __launch_bounds__(kSweepThreads, kCorr == MCS_CORR_NN27 ? MCS_NN
     flush();
   }
 #endif
+#if MCS_SWEEP_TMEM_ACC
+#pragma unroll
+  for (int c = 0; c < 7; ++c) {  // (every thread: the TMEM loads are warp-collective)
+    uint32_t w[8];
+    tm_ld8(tm + 8 * c, w);
+    tm_wait_ld();
+    if (active) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int k = 4 * c + u;  // total k -> record word (k == 0 ? 0 : k + 1)
+        rec(k == 0 ? 0 : k + 1) = __hiloint2double((int)w[2 * u + 1], (int)w[2 * u]);
+      }
+    }
+  }
+  if (active) rec(1) = (double)n;
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 64;" ::"r"(s_tmem) : "memory");
+  }
+#else
   if (active) {
     rec(1) = (double)n;
 #if !MCS_SWEEP_GACC
@@ -799,6 +898,7 @@ __global__ void __launch_bounds__(kSweepThreads, kCorr == MCS_CORR_NN27 ? MCS_NN
     for (int k = 0; k < 6; ++k) rec(23 + k) = tot(22 + k);
 #endif
   }
+#endif
 }
 
 // Point splits (gridDim.y = P > 1 in the sweep): split 0's record of every item becomes the sum
