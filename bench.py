@@ -194,6 +194,10 @@ CONFIGS = {
                           "r = 1 m, 4 lattice-shifted modes, per-particle keyframe poses)"),
     "c5": ("c5", 100_000, "C5: {N} particles x 4096-pt scan vs 2 x 20 keyframes (two "
                           "near-identical floors, particles over both)"),
+    "c4_survival": ("c4_survival", 1_000_000,
+                    "C4 survival variant: {N} particles at 0.1 mm / 0.01 mrad spread (keyframe "
+                    "drift 0.01 mm / 1 urad; ~36 % survive the 8,192-point likelihoods) x "
+                    "8192-pt scan vs 20 keyframes"),
     "c2_survival": ("c2_survival", 100_000,
                     "C2 survival variant: {N} particles at 1 mm / 0.1 mrad spread (keyframe "
                     "drift 0.1 mm / 0.01 mrad) x 4096-pt scan vs 20 keyframes"),
@@ -208,6 +212,9 @@ def make_scene(config: str, particles: int, seed: int = 0):
         return synth.c3(seed=seed, N=particles)
     if config == "c5":
         return synth.c5(seed=seed, N=particles)
+    if config == "c4_survival":
+        return synth.c4(seed=seed, N=particles, sig_t=1e-4, sig_r=1e-5, drift_t=1e-5,
+                        drift_r=1e-6)
     if config == "c2_survival":
         return synth.c2(seed=seed, N=particles, sig_t=1e-3, sig_r=1e-4, drift_t=1e-4,
                         drift_r=1e-5)
@@ -548,6 +555,9 @@ def run_gpu(args):
         "match_rate": matched / max(triples, 1),
         "a0_ms_per_keyframe": a0_ms,
         "n_dead": int(out["n_dead"][0]),
+        # the clones a6 writes per update (T_t, every T_k, L: mcs_state_bytes_per_particle);
+        # across GPUs the share whose donor lives on another rank is the migration
+        "clone_bytes_per_step": int(out["n_dead"][0]) * mcs.state_bytes_per_particle(K),
         "paper_context": PAPER_CONTEXT,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

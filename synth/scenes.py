@@ -444,14 +444,17 @@ def c5(seed: int = 0, N: int = 100_000, S: int = 4096, K_floor: int = 20, gap: i
 
 
 @functools.lru_cache(maxsize=1)
-def c4(seed: int = 0, N: int = 1_000_000, S: int = 8192) -> Scene:
-    """C4: the C2 scene with an 8,192-point scan and 1M particles (sharded over 2/4/8 GPUs)."""
+def c4(seed: int = 0, N: int = 1_000_000, S: int = 8192, sig_t: float = 0.1, sig_r: float = 0.01,
+       drift_t: float = 0.01, drift_r: float = 0.001) -> Scene:
+    """C4: the C2 scene with an 8,192-point scan and 1M particles (sharded over 2/4/8 GPUs).
+    A tighter spread (bench --config c4_survival) lets a share of the particles survive P:190's
+    floors, so a6 clones (and, across GPUs, migrates) a realistic fraction."""
     base = c2(seed, N=1000)
     world = loop_corridor(seed)
     scan = sensor_cloud(world, base.T_gt, base.r / 2, S, rng(seed, "c4/scan"), 1200, 200)
     g = rng(seed, "c4/particles")
-    Tt = perturb(base.T_gt, 0.1, 0.01, g, N)
-    Tk = _kf_poses_drift(base.kf_gt, N, g, 0.01, 0.001)
+    Tt = perturb(base.T_gt, sig_t, sig_r, g, N)
+    Tk = _kf_poses_drift(base.kf_gt, N, g, drift_t, drift_r)
     import dataclasses
     return dataclasses.replace(base, name="C4", scan_mean3=scan[0], scan_cov6=scan[1],
                                pose12=to12(Tt), kf_pose12=Tk,
